@@ -1,0 +1,107 @@
+/* cronus_ck.h — the thin C-ABI kernel layer of the B200 engine (sm_100a).
+ *
+ * Every entry point takes raw device pointers, plain sizes and a cudaStream_t
+ * passed as void*, never allocates, and returns a cudaError_t as int (0 = ok).
+ * The C++ host (csrc/gpu/) is the only production caller; tests call the same
+ * symbols through ctypes with torch-allocated buffers.
+ *
+ * These kernels replace the reference simulator's three cost-model stand-ins
+ * (proj/src/costmodel.cpp:9-15 prefill_time / chunked_iter_time and
+ * proj/src/model.cpp:11-13 transfer_time): the work those formulas price is
+ * what these kernels actually perform.
+ *
+ * KV cache layout (one pool per worker, block-major, bf16):
+ *   pool[block][layer][K=0|V=1][kv_head][16 tokens][128 dims]
+ * so a block is one contiguous slab (2 MiB for LLaMA3-8B) — the unit of the
+ * PPI -> CPI handoff — and every (block, layer, K|V, head) tile is a contiguous
+ * 4 KiB run for the attention kernels.
+ */
+#ifndef CRONUS_CK_H
+#define CRONUS_CK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* GEMM epilogues */
+enum { CK_EPI_BF16 = 0, CK_EPI_F32 = 1, CK_EPI_RED_F32 = 2 };
+
+/* out[m, n] (op)= sum_k X[m, k] W[n, k] (+ bias[n]); W [N, K], X [M, K] bf16 row-major.
+ * N % 128 == 0, K % 64 == 0. epi: CK_EPI_BF16 (store bf16), CK_EPI_F32 (store
+ * fp32), CK_EPI_RED_F32 (red.add fp32 into out — residual add / split-K).
+ * splits: K splits (0 = auto; > 1 only with CK_EPI_RED_F32). max_ctas: cap on
+ * the persistent grid (0 = all SMs). tcgen05 + TMEM + TMA. */
+int ck_gemm(const void* W, const void* X, void* out, const void* bias, int M, int N, int K, int ldo, int epi,
+            int splits, int max_ctas, void* stream);
+
+/* Deterministic uniform init: out[i] = bf16(offset + scale * u_i), u_i in [-1, 1)
+ * from splitmix64(seed, tensor_id, i) (restated in oracle/numerics.py). */
+int ck_init_uniform(void* out_bf16, long long n, unsigned long long seed, unsigned long long tensor_id,
+                    float scale, float offset, void* stream);
+
+/* Prompt tokens: tok[i] = splitmix64(seed, req_id[i], pos[i]) % vocab for n rows. */
+int ck_prompt_tokens(int* out, const int* req_id, const int* pos, int n, unsigned long long seed, int vocab,
+                     void* stream);
+
+/* RoPE cos/sin table [max_pos][64] fp32 each (computed in double). */
+int ck_rope_table(float* cos_tab, float* sin_tab, int max_pos, double theta, void* stream);
+
+/* Per-row metadata of one forward pass (device pointers):
+ *   row_rid[M]   request slot of the row
+ *   row_pos[M]   absolute position of the row's token
+ *   row_dec[M]   1: token = last_tok[rid] (decode row); 0: prompt[prompt_off[rid] + pos]
+ */
+int ck_embed(float* x, const void* emb_bf16, const int* row_rid, const int* row_pos, const int* row_dec,
+             const int* prompt, const long long* prompt_off, const int* last_tok, int M, int H, void* stream);
+
+/* out_bf16[r] = rmsnorm(x[rows ? rows[r] : r]) * gamma, r < R. */
+int ck_rmsnorm(const float* x, const void* gamma, void* out_bf16, const int* rows, int R, int H, float eps,
+               void* stream);
+
+/* qkv fp32 [M, (nq + 2 nkv) * 128] (+ bias) -> RoPE(q) bf16 [M, nq*128] and
+ * RoPE(k), v appended to the paged pool at each row's position.
+ * bt: flat block table; row_bt[M] = offset of the row's sequence in bt. */
+int ck_qkv_rope_append(const float* qkv, const void* bias, void* q_out, void* kv_pool, const int* bt,
+                       const int* row_bt, const int* row_pos, const float* cos_tab, const float* sin_tab, int M,
+                       int nq, int nkv, int layer, int n_layers, void* stream);
+
+/* Decode attention over the paged pool for S single-token sequences (split-KV).
+ * seq_row[S] (row of q/out), seq_len[S] (keys), seq_bt[S] (offset into bt),
+ * seq_item0[S+1] (first work item of each sequence). work[n_work] = seq << 16 | split;
+ * a work item covers up to `blocks_per_split` 16-token blocks. ws: fp32 partials,
+ * n_work * nq * 130 floats. Output bf16 rows [*, nq*128]. */
+int ck_attn_decode(const void* q, const void* kv_pool, const int* bt, const int* seq_row, const int* seq_len,
+                   const int* seq_bt, const int* seq_item0, const int* work, int n_work, int n_seq,
+                   int blocks_per_split, float* ws, void* out, int nq, int nkv, int layer, int n_layers,
+                   float scale, void* stream);
+
+/* Prefill/chunk attention, causal: query rows [q_row0, q_row0+q_len) sit at
+ * positions [pos0, pos0+q_len); keys [0, pos0+q_len) from the paged pool via bt. */
+int ck_attn_prefill(const void* q, const void* kv_pool, const int* bt, int q_row0, int q_len, int pos0, void* out,
+                    int nq, int nkv, int layer, int n_layers, float scale, void* stream);
+
+/* act[m, i] = silu(gu[m, 2i]) * gu[m, 2i+1]  (gate/up rows interleaved), fp32 in. */
+int ck_silu_mul(const float* gu, void* act_bf16, int M, int F, void* stream);
+
+/* Greedy sampling: token = argmax_v logits[r, v] (lowest index on ties), then
+ * last_tok[rid[r]] = token, out_tok[out_idx[r]] = token. */
+int ck_argmax_emit(const float* logits, int R, int V, const int* rid, const long long* out_idx, int* last_tok,
+                   int* out_tok, void* stream);
+
+/* KV handoff: copy n_blocks blocks src_pool[src_ids[i]] -> dst_pool[dst_ids[i]]
+ * (block_bytes each; src may be a peer-mapped pointer — pull over NVLink). */
+int ck_kv_copy(const void* src_pool, const int* src_ids, void* dst_pool, const int* dst_ids, int n_blocks,
+               long long block_bytes, void* stream);
+
+/* Copy one int: dst[di] = src[si] (first token travelling with the handoff). */
+int ck_copy_token(const int* src, long long si, int* dst, long long di, int* dst2, long long di2, void* stream);
+
+int ck_device_sms(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CRONUS_CK_H */

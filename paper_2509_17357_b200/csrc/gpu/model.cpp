@@ -1,0 +1,429 @@
+// Decoder forward orchestration over the C-ABI kernels (see model.hpp).
+#include "model.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "cronus_ck.h"
+
+namespace cronus {
+namespace gpu {
+
+void check_cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+void check_ck(int rc, const char* what) {
+    if (rc != 0)
+        throw std::runtime_error(std::string("kernel ") + what + " failed: " +
+                                 cudaGetErrorString(static_cast<cudaError_t>(rc)));
+}
+
+// ------------------------------------------------------------------ ModelSpec
+ModelSpec ModelSpec::preset(const std::string& name) {
+    ModelSpec m;
+    m.name = name;
+    if (name == "llama3-8b") {
+        m.hidden = 4096, m.layers = 32, m.n_heads = 32, m.n_kv_heads = 8, m.ffn = 14336, m.vocab = 128256;
+        m.rope_theta = 500000.0, m.rms_eps = 1e-5f, m.qkv_bias = false;
+    } else if (name == "qwen2-7b") {
+        m.hidden = 3584, m.layers = 28, m.n_heads = 28, m.n_kv_heads = 4, m.ffn = 18944, m.vocab = 152064;
+        m.rope_theta = 1000000.0, m.rms_eps = 1e-6f, m.qkv_bias = true;
+    } else if (name == "tiny") {
+        m.hidden = 256, m.layers = 2, m.n_heads = 2, m.n_kv_heads = 1, m.ffn = 1024, m.vocab = 4096;
+        m.rope_theta = 10000.0, m.rms_eps = 1e-5f, m.qkv_bias = false;
+        m.lm_std = 0.25f;
+        m.max_pos = 16384;
+    } else if (name == "tiny-qwen") {  // tiny with the Qwen2 QKV bias and GQA group 2
+        m.hidden = 512, m.layers = 2, m.n_heads = 4, m.n_kv_heads = 2, m.ffn = 1024, m.vocab = 4096;
+        m.rope_theta = 1000000.0, m.rms_eps = 1e-6f, m.qkv_bias = true;
+        m.lm_std = 0.25f;
+        m.max_pos = 16384;
+    } else {
+        throw std::invalid_argument("unknown model preset '" + name + "' (llama3-8b, qwen2-7b, tiny, tiny-qwen)");
+    }
+    if (m.hidden % 128 || m.ffn % 64 || m.vocab % 128 || m.n_heads % m.n_kv_heads)
+        throw std::invalid_argument("model shape not supported by the sm_100a kernels");
+    return m;
+}
+
+double ModelSpec::linear_flops_per_token() const {
+    const double H = hidden;
+    const double per_layer = H * qkv_n() + static_cast<double>(q_n()) * H + H * 2.0 * ffn + 1.0 * ffn * H;
+    return 2.0 * per_layer * layers;
+}
+
+long long ModelSpec::weight_bytes() const {
+    const long long H = hidden;
+    long long per_layer = H * qkv_n() + static_cast<long long>(q_n()) * H + H * 2LL * ffn + 1LL * ffn * H + 2 * H;
+    if (qkv_bias) per_layer += qkv_n();
+    return 2LL * (per_layer * layers + 2LL * vocab * H + H);
+}
+
+// ------------------------------------------------------------------ Weights
+namespace {
+size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+constexpr float kSqrt3 = 1.7320508075688772f;
+}  // namespace
+
+Weights::Weights(const ModelSpec& spec, int device) : spec_(spec), dev_(device) {
+    check_cuda(cudaSetDevice(device), "cudaSetDevice");
+    const ModelSpec& m = spec_;
+    const long long H = m.hidden;
+    struct Item {
+        void** dst;
+        long long n;
+        uint64_t tid;
+        float scale, offset;
+    };
+    std::vector<Item> items;
+    layer.resize(m.layers);
+    items.push_back({&embed, static_cast<long long>(m.vocab) * H, kTidEmbed, m.emb_std * kSqrt3, 0.f});
+    items.push_back({&lm_head, static_cast<long long>(m.vocab) * H, kTidLmHead, m.lm_std * kSqrt3, 0.f});
+    items.push_back({&final_norm, H, kTidFinalNorm, 0.1f, 1.0f});
+    for (int l = 0; l < m.layers; ++l) {
+        LayerWeights& L = layer[l];
+        items.push_back({&L.wqkv, static_cast<long long>(m.qkv_n()) * H, layer_tid(l, kWqkv), m.w_std * kSqrt3, 0.f});
+        if (m.qkv_bias) items.push_back({&L.bqkv, m.qkv_n(), layer_tid(l, kBqkv), 0.1f, 0.f});
+        items.push_back({&L.wo, H * m.q_n(), layer_tid(l, kWo), m.w_std * kSqrt3, 0.f});
+        items.push_back({&L.wgu, 2LL * m.ffn * H, layer_tid(l, kWgu), m.w_std * kSqrt3, 0.f});
+        items.push_back({&L.wd, H * m.ffn, layer_tid(l, kWd), m.w_std * kSqrt3, 0.f});
+        items.push_back({&L.attn_norm, H, layer_tid(l, kAttnNorm), 0.1f, 1.0f});
+        items.push_back({&L.ffn_norm, H, layer_tid(l, kFfnNorm), 0.1f, 1.0f});
+    }
+    size_t total = 0;
+    std::vector<size_t> off;
+    for (const Item& it : items) {
+        off.push_back(total);
+        total += align256(static_cast<size_t>(it.n) * 2);
+    }
+    const size_t rope = align256(static_cast<size_t>(m.max_pos) * 64 * 4);
+    check_cuda(cudaMalloc(&base_, total + 2 * rope), "cudaMalloc(weights)");
+    char* b = static_cast<char*>(base_);
+    for (size_t i = 0; i < items.size(); ++i) {
+        *items[i].dst = b + off[i];
+        check_ck(ck_init_uniform(*items[i].dst, items[i].n, m.seed, items[i].tid, items[i].scale, items[i].offset,
+                                 nullptr),
+                 "init_uniform");
+    }
+    cos_tab = reinterpret_cast<float*>(b + total);
+    sin_tab = reinterpret_cast<float*>(b + total + rope);
+    check_ck(ck_rope_table(cos_tab, sin_tab, m.max_pos, m.rope_theta, nullptr), "rope_table");
+    check_cuda(cudaDeviceSynchronize(), "weights init");
+}
+
+Weights::~Weights() {
+    if (base_) {
+        cudaSetDevice(dev_);
+        cudaFree(base_);
+    }
+}
+
+KvPool::KvPool(int dev, long long n_blocks, long long bb) : device(dev), blocks(n_blocks), block_bytes(bb) {
+    check_cuda(cudaSetDevice(dev), "cudaSetDevice");
+    check_cuda(cudaMalloc(&base, static_cast<size_t>(n_blocks) * bb), "cudaMalloc(kv pool)");
+}
+
+KvPool::~KvPool() {
+    if (base) {
+        cudaSetDevice(device);
+        cudaFree(base);
+    }
+}
+
+// ------------------------------------------------------------------ Batch
+void Batch::clear() {
+    row_rid.clear(), row_pos.clear(), row_dec.clear(), row_bt.clear();
+    d_row.clear(), d_len.clear(), d_bt.clear(), d_item0.clear(), d_work.clear();
+    p_row0 = p_len = p_pos0 = p_bt = 0;
+    bt.clear();
+    s_row.clear(), s_rid.clear(), s_out.clear();
+}
+
+int Batch::add_table(const std::vector<int32_t>& blocks, long long n_tokens) {
+    const int off = static_cast<int>(bt.size());
+    const long long nb = (n_tokens + 15) / 16;
+    if (static_cast<long long>(blocks.size()) < nb) throw std::logic_error("block table shorter than the sequence");
+    bt.insert(bt.end(), blocks.begin(), blocks.begin() + nb);
+    return off;
+}
+
+void Batch::add_decode(int rid, long long ctx, const std::vector<int32_t>& blocks, long long out_index) {
+    const int row = rows();
+    const int off = add_table(blocks, ctx);
+    row_rid.push_back(rid);
+    row_pos.push_back(static_cast<int>(ctx - 1));
+    row_dec.push_back(1);
+    row_bt.push_back(off);
+    d_row.push_back(row);
+    d_len.push_back(static_cast<int>(ctx));
+    d_bt.push_back(off);
+    s_row.push_back(row);
+    s_rid.push_back(rid);
+    s_out.push_back(out_index);
+}
+
+void Batch::add_prefill(int rid, long long pos0, long long len, const std::vector<int32_t>& blocks, bool sample,
+                        long long out_index) {
+    const int off = add_table(blocks, pos0 + len);
+    p_row0 = rows();
+    p_len = static_cast<int>(len);
+    p_pos0 = static_cast<int>(pos0);
+    p_bt = off;
+    for (long long i = 0; i < len; ++i) {
+        row_rid.push_back(rid);
+        row_pos.push_back(static_cast<int>(pos0 + i));
+        row_dec.push_back(0);
+        row_bt.push_back(off);
+    }
+    if (sample) {
+        s_row.push_back(p_row0 + p_len - 1);
+        s_rid.push_back(rid);
+        s_out.push_back(out_index);
+    }
+}
+
+// Pick the split size so the decode grid holds ~target_ctas CTAs.
+void Batch::plan_decode_splits(int n_kv_heads, int target_ctas) {
+    long long total = 0;
+    for (int len : d_len) total += (len + 15) / 16;
+    int bps = static_cast<int>((total * n_kv_heads + target_ctas - 1) / std::max(1, target_ctas));
+    bps = std::clamp(bps, 4, 256);
+    // keep the work list bounded (workspace sizing)
+    while (true) {
+        long long items = 0;
+        for (int len : d_len) items += ((len + 15) / 16 + bps - 1) / bps;
+        if (items <= 4096) break;
+        bps *= 2;
+    }
+    blocks_per_split = bps;
+    d_item0.clear();
+    d_work.clear();
+    for (size_t s = 0; s < d_len.size(); ++s) {
+        d_item0.push_back(static_cast<int>(d_work.size()));
+        const int nblk = (d_len[s] + 15) / 16;
+        const int ns = (nblk + bps - 1) / bps;
+        for (int i = 0; i < ns; ++i) d_work.push_back(static_cast<int>(s << 16) | i);
+    }
+    d_item0.push_back(static_cast<int>(d_work.size()));
+}
+
+// ------------------------------------------------------------------ Worker
+Worker::Worker(const Weights& w, int max_rows, int max_sample, int max_blocks_per_pass, cudaStream_t stream,
+               int max_ctas)
+    : w_(w), m_(w.spec()), max_rows_(max_rows), max_sample_(max_sample), max_bt_(max_blocks_per_pass),
+      stream_(stream), max_ctas_(max_ctas) {
+    check_cuda(cudaSetDevice(w.device()), "cudaSetDevice");
+    const size_t R = max_rows, H = m_.hidden;
+    check_cuda(cudaMalloc(&x_, R * H * 4), "alloc x");
+    check_cuda(cudaMalloc(&h_, R * H * 2), "alloc h");
+    check_cuda(cudaMalloc(&qkv_, R * m_.qkv_n() * 4), "alloc qkv");
+    check_cuda(cudaMalloc(&q_, R * m_.q_n() * 2), "alloc q");
+    check_cuda(cudaMalloc(&attn_, R * m_.q_n() * 2), "alloc attn");
+    check_cuda(cudaMalloc(&gu_, R * 2 * m_.ffn * 4), "alloc gu");
+    check_cuda(cudaMalloc(&act_, R * m_.ffn * 2), "alloc act");
+    check_cuda(cudaMalloc(&hs_, static_cast<size_t>(max_sample) * H * 2), "alloc hs");
+    check_cuda(cudaMalloc(&logits_, static_cast<size_t>(max_sample) * m_.vocab * 4), "alloc logits");
+    attn_ws_floats_ = 4096LL * m_.n_heads * (m_.head_dim + 2);
+    check_cuda(cudaMalloc(&attn_ws_, attn_ws_floats_ * 4), "alloc attn ws");
+    meta_cap_ = 12LL * max_rows + max_bt_ + 2 * 4096 + 64;
+    check_cuda(cudaMalloc(&meta_dev_, meta_cap_ * 4), "alloc meta");
+    for (int i = 0; i < kRing; ++i) {
+        check_cuda(cudaMallocHost(&meta_host_[i], meta_cap_ * 4), "alloc pinned meta");
+        check_cuda(cudaEventCreateWithFlags(&meta_ev_[i], cudaEventDisableTiming), "event");
+    }
+}
+
+Worker::~Worker() {
+    cudaSetDevice(w_.device());
+    for (void* p : {static_cast<void*>(x_), h_, static_cast<void*>(qkv_), q_, attn_, static_cast<void*>(gu_), act_, hs_,
+                    static_cast<void*>(logits_), static_cast<void*>(attn_ws_), static_cast<void*>(meta_dev_)})
+        if (p) cudaFree(p);
+    for (int i = 0; i < kRing; ++i) {
+        if (meta_host_[i]) cudaFreeHost(meta_host_[i]);
+        if (meta_ev_[i]) cudaEventDestroy(meta_ev_[i]);
+    }
+    for (auto& p : pending_) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    for (cudaEvent_t e : ev_free_) cudaEventDestroy(e);
+}
+
+cudaEvent_t Worker::ev() {
+    if (!ev_free_.empty()) {
+        cudaEvent_t e = ev_free_.back();
+        ev_free_.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    check_cuda(cudaEventCreate(&e), "event");
+    return e;
+}
+void Worker::mark(cudaEvent_t& a) {
+    if (!profile_) return;
+    a = ev();
+    cudaEventRecord(a, stream_);
+}
+void Worker::done(cudaEvent_t a, KernelStat* into, double bytes, double flops) {
+    if (!profile_) return;
+    cudaEvent_t b = ev();
+    cudaEventRecord(b, stream_);
+    pending_.push_back({a, b, into, bytes, flops});
+}
+
+void Worker::collect_stats() {
+    for (auto& p : pending_) {
+        cudaEventSynchronize(p.b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, p.a, p.b);
+        p.into->launches++;
+        p.into->ms += ms;
+        p.into->bytes += p.bytes;
+        p.into->flops += p.flops;
+        ev_free_.push_back(p.a);
+        ev_free_.push_back(p.b);
+    }
+    pending_.clear();
+}
+
+void Worker::gemm(const void* W, const void* X, void* out, const void* bias, int M, int N, int K, int epi,
+                  int splits) {
+    cudaEvent_t a = nullptr;
+    mark(a);
+    check_ck(ck_gemm(W, X, out, bias, M, N, K, N, epi, splits, max_ctas_, stream_), "gemm");
+    done(a, &stat_gemm, 2.0 * (static_cast<double>(N) * K + static_cast<double>(M) * K) +
+                            (epi == CK_EPI_BF16 ? 2.0 : 4.0) * M * N,
+         2.0 * M * N * K);
+}
+
+namespace {
+template <class T>
+T* carve(int*& cur, size_t n) {
+    uintptr_t p = reinterpret_cast<uintptr_t>(cur);
+    p = (p + alignof(T) - 1) & ~(uintptr_t)(alignof(T) - 1);
+    T* out = reinterpret_cast<T*>(p);
+    cur = reinterpret_cast<int*>(out + n);
+    return out;
+}
+}  // namespace
+
+void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, const long long* prompt_off,
+                     int* last_tok, int* out_tok) {
+    const int M = b.rows();
+    if (M == 0) return;
+    if (M > max_rows_) throw std::logic_error("forward: batch exceeds worker rows");
+    const int R = static_cast<int>(b.s_row.size());
+    if (R > max_sample_) throw std::logic_error("forward: too many sampled rows");
+    const ModelSpec& m = m_;
+    cudaEvent_t pass0 = nullptr;
+    mark(pass0);
+
+    // ---- metadata: one pinned staging slot -> one H2D copy
+    const int slot = ring_;
+    ring_ = (ring_ + 1) % kRing;
+    check_cuda(cudaEventSynchronize(meta_ev_[slot]), "meta staging");
+    int* host = meta_host_[slot];
+    int* cur_h = host;
+    auto put = [&](const auto& v) {
+        using T = typename std::decay_t<decltype(v)>::value_type;
+        T* dst = carve<T>(cur_h, v.size());
+        if (!v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(T));
+        return static_cast<long long>(reinterpret_cast<char*>(dst) - reinterpret_cast<char*>(host));
+    };
+    const long long o_row_rid = put(b.row_rid), o_row_pos = put(b.row_pos), o_row_dec = put(b.row_dec),
+                    o_row_bt = put(b.row_bt), o_d_row = put(b.d_row), o_d_len = put(b.d_len), o_d_bt = put(b.d_bt),
+                    o_d_item0 = put(b.d_item0), o_d_work = put(b.d_work), o_bt = put(b.bt), o_s_row = put(b.s_row),
+                    o_s_rid = put(b.s_rid), o_s_out = put(b.s_out);
+    const size_t bytes = reinterpret_cast<char*>(cur_h) - reinterpret_cast<char*>(host);
+    if (bytes > static_cast<size_t>(meta_cap_) * 4) throw std::logic_error("forward: metadata overflow");
+    check_cuda(cudaMemcpyAsync(meta_dev_, host, bytes, cudaMemcpyHostToDevice, stream_), "meta H2D");
+    check_cuda(cudaEventRecord(meta_ev_[slot], stream_), "meta event");
+    char* dbase = reinterpret_cast<char*>(meta_dev_);
+    auto D = [&](long long off) { return reinterpret_cast<int*>(dbase + off); };
+    const int* row_rid = D(o_row_rid);
+    const int* row_pos = D(o_row_pos);
+    const int* row_dec = D(o_row_dec);
+    const int* row_bt = D(o_row_bt);
+    const int* bt = D(o_bt);
+    const int n_dec = static_cast<int>(b.d_row.size());
+    const int n_work = static_cast<int>(b.d_work.size());
+    if (static_cast<long long>(n_work) * m.n_heads * (m.head_dim + 2) > attn_ws_floats_)
+        throw std::logic_error("forward: decode work list too long");
+
+    const int H = m.hidden, Q = m.qkv_n(), NQ = m.q_n(), F = m.ffn;
+    const float scale = 1.0f / std::sqrt(static_cast<float>(m.head_dim));
+    const bool small = M <= 128;  // weight-streaming regime: split-K + red.add into zeroed fp32
+    long long dec_keys = 0;
+    for (int len : b.d_len) dec_keys += len;
+    const double kv_tok_layer = 2.0 * m.n_kv_heads * m.head_dim * 2;  // bytes per token per layer (K+V)
+
+    cudaEvent_t a = nullptr;
+    mark(a);
+    check_ck(ck_embed(x_, w_.embed, row_rid, row_pos, row_dec, prompt, prompt_off, last_tok, M, H, stream_), "embed");
+    done(a, &stat_other, 0, 0);
+    for (int l = 0; l < m.layers; ++l) {
+        const LayerWeights& L = w_.layer[l];
+        mark(a);
+        check_ck(ck_rmsnorm(x_, L.attn_norm, h_, nullptr, M, H, m.rms_eps, stream_), "rmsnorm");
+        done(a, &stat_other, 0, 0);
+        if (small) {
+            check_cuda(cudaMemsetAsync(qkv_, 0, static_cast<size_t>(M) * Q * 4, stream_), "memset qkv");
+            gemm(L.wqkv, h_, qkv_, L.bqkv, M, Q, H, CK_EPI_RED_F32, 0);
+        } else {
+            gemm(L.wqkv, h_, qkv_, L.bqkv, M, Q, H, CK_EPI_F32, 1);
+        }
+        mark(a);
+        check_ck(ck_qkv_rope_append(qkv_, nullptr, q_, pool.base, bt, row_bt, row_pos, w_.cos_tab, w_.sin_tab, M,
+                                    m.n_heads, m.n_kv_heads, l, m.layers, stream_),
+                 "qkv_rope_append");
+        done(a, &stat_other, 0, 0);
+        if (n_dec > 0) {
+            mark(a);
+            check_ck(ck_attn_decode(q_, pool.base, bt, D(o_d_row), D(o_d_len), D(o_d_bt), D(o_d_item0), D(o_d_work),
+                                    n_work, n_dec, b.blocks_per_split, attn_ws_, attn_, m.n_heads, m.n_kv_heads, l,
+                                    m.layers, scale, stream_),
+                     "attn_decode");
+            done(a, &stat_decode_attn, dec_keys * kv_tok_layer, 4.0 * m.n_heads * m.head_dim * dec_keys);
+        }
+        if (b.p_len > 0) {
+            mark(a);
+            check_ck(ck_attn_prefill(q_, pool.base, bt + b.p_bt, b.p_row0, b.p_len, b.p_pos0, attn_, m.n_heads,
+                                     m.n_kv_heads, l, m.layers, scale, stream_),
+                     "attn_prefill");
+            const double keys = static_cast<double>(b.p_len) * b.p_pos0 + 0.5 * b.p_len * (b.p_len + 1.0);
+            done(a, &stat_prefill_attn, (b.p_pos0 + b.p_len) * kv_tok_layer, 4.0 * m.n_heads * m.head_dim * keys);
+        }
+        gemm(L.wo, attn_, x_, nullptr, M, H, NQ, CK_EPI_RED_F32, 0);
+        mark(a);
+        check_ck(ck_rmsnorm(x_, L.ffn_norm, h_, nullptr, M, H, m.rms_eps, stream_), "rmsnorm");
+        done(a, &stat_other, 0, 0);
+        if (small) {
+            check_cuda(cudaMemsetAsync(gu_, 0, static_cast<size_t>(M) * 2 * F * 4, stream_), "memset gu");
+            gemm(L.wgu, h_, gu_, nullptr, M, 2 * F, H, CK_EPI_RED_F32, 0);
+        } else {
+            gemm(L.wgu, h_, gu_, nullptr, M, 2 * F, H, CK_EPI_F32, 1);
+        }
+        mark(a);
+        check_ck(ck_silu_mul(gu_, act_, M, F, stream_), "silu_mul");
+        done(a, &stat_other, 0, 0);
+        gemm(L.wd, act_, x_, nullptr, M, H, F, CK_EPI_RED_F32, 0);
+    }
+    if (R > 0) {
+        mark(a);
+        check_ck(ck_rmsnorm(x_, w_.final_norm, hs_, D(o_s_row), R, H, m.rms_eps, stream_), "final norm");
+        done(a, &stat_other, 0, 0);
+        gemm(w_.lm_head, hs_, logits_, nullptr, R, m.vocab, H, CK_EPI_F32, 1);
+        mark(a);
+        check_ck(ck_argmax_emit(logits_, R, m.vocab, D(o_s_rid), reinterpret_cast<const long long*>(D(o_s_out)),
+                                last_tok, out_tok, stream_),
+                 "argmax");
+        done(a, &stat_other, 0, 0);
+    }
+    done(pass0, &stat_forward, 0, 0);
+}
+
+}  // namespace gpu
+}  // namespace cronus

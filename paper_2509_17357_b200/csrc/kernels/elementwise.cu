@@ -1,0 +1,338 @@
+// Bandwidth-bound kernels of the decoder forward and the KV handoff. All use
+// 128-bit vector access where the layout allows; none of them is on the tensor
+// pipe. Semantics are restated in oracle/numerics.py (the parity checker).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "common.cuh"
+#include "cronus_ck.h"
+
+namespace {
+
+using namespace ck;
+
+inline int ret() { return static_cast<int>(cudaGetLastError()); }
+inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------- init / tokens
+__global__ void init_uniform_kernel(__nv_bfloat16* out, long long n, uint64_t seed, uint64_t tid, float step,
+                                    float offset) {
+    const uint64_t base = seed * 0x9E3779B97F4A7C15ull + tid * 0xD1B54A32D192ED03ull;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const uint64_t h = mix64(base + static_cast<uint64_t>(i));
+        const int u = static_cast<int>(h >> 40) - (1 << 23);  // uniform integer in [-2^23, 2^23)
+        const float v = __fadd_rn(__fmul_rn(static_cast<float>(u), step), offset);
+        out[i] = __float2bfloat16_rn(v);
+    }
+}
+
+__global__ void prompt_tokens_kernel(int* out, const int* req, const int* pos, int n, uint64_t seed, int vocab) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t h = mix64(seed * 0x9E3779B97F4A7C15ull + static_cast<uint64_t>(static_cast<uint32_t>(req[i])) *
+                                                                0xD1B54A32D192ED03ull +
+                             static_cast<uint64_t>(static_cast<uint32_t>(pos[i])));
+    out[i] = static_cast<int>(h % static_cast<uint64_t>(vocab));
+}
+
+__global__ void rope_table_kernel(float* c, float* s, int max_pos, double theta) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= max_pos * 64) return;
+    const int p = i >> 6, f = i & 63;
+    const double inv = pow(theta, -static_cast<double>(2 * f) / 128.0);
+    const double a = static_cast<double>(p) * inv;
+    c[i] = static_cast<float>(cos(a));
+    s[i] = static_cast<float>(sin(a));
+}
+
+// ---------------------------------------------------------------- embedding
+// x[m, :] = float(emb[token(m), :]); one CTA per row, 8 bf16 per thread-step.
+__global__ void embed_kernel(float* __restrict__ x, const __nv_bfloat16* __restrict__ emb, const int* row_rid,
+                             const int* row_pos, const int* row_dec, const int* prompt, const long long* prompt_off,
+                             const int* last_tok, int H) {
+    const int m = blockIdx.x;
+    const int rid = row_rid[m];
+    const int tok = row_dec[m] ? last_tok[rid] : prompt[prompt_off[rid] + row_pos[m]];
+    const uint4* src = reinterpret_cast<const uint4*>(emb + static_cast<size_t>(tok) * H);
+    float4* dst = reinterpret_cast<float4*>(x + static_cast<size_t>(m) * H);
+    for (int i = threadIdx.x; i < H / 8; i += blockDim.x) {
+        const uint4 v = src[i];
+        const float2 a = unpack_bf16x2(v.x), b = unpack_bf16x2(v.y), c = unpack_bf16x2(v.z), d = unpack_bf16x2(v.w);
+        dst[2 * i] = make_float4(a.x, a.y, b.x, b.y);
+        dst[2 * i + 1] = make_float4(c.x, c.y, d.x, d.y);
+    }
+}
+
+// ---------------------------------------------------------------- RMSNorm
+__device__ float block_sum(float v, float* red) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) red[w] = v;
+    __syncthreads();
+    float t = 0.f;
+    const int nw = blockDim.x >> 5;
+    for (int i = 0; i < nw; ++i) t += red[i];
+    __syncthreads();
+    return t;
+}
+
+// y = bf16(x * rsqrt(mean(x^2) + eps) * gamma); fp32 math, one CTA per output row.
+__global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ gamma,
+                               __nv_bfloat16* __restrict__ out, const int* rows, int H, float eps) {
+    __shared__ float red[32];
+    const int r = blockIdx.x;
+    const int src = rows ? rows[r] : r;
+    const float4* xr = reinterpret_cast<const float4*>(x + static_cast<size_t>(src) * H);
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < H / 4; i += blockDim.x) {
+        const float4 v = xr[i];
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+    ss = block_sum(ss, red);
+    const float inv = rsqrtf(ss / static_cast<float>(H) + eps);
+    const uint2* g = reinterpret_cast<const uint2*>(gamma);
+    uint2* o = reinterpret_cast<uint2*>(out + static_cast<size_t>(r) * H);
+    for (int i = threadIdx.x; i < H / 4; i += blockDim.x) {
+        const float4 v = xr[i];
+        const uint2 gg = g[i];
+        const float2 g0 = unpack_bf16x2(gg.x), g1 = unpack_bf16x2(gg.y);
+        o[i] = make_uint2(pack_bf16x2(v.x * inv * g0.x, v.y * inv * g0.y), pack_bf16x2(v.z * inv * g1.x, v.w * inv * g1.y));
+    }
+}
+
+// ---------------------------------------------------------------- QKV post-processing
+// One CTA per row: (+bias) -> RoPE (rotate-half pairs (i, i+64)) -> q out (bf16) and
+// k, v into the row's paged KV slot.
+__global__ void qkv_rope_append_kernel(const float* __restrict__ qkv, const __nv_bfloat16* __restrict__ bias,
+                                       __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ pool,
+                                       const int* __restrict__ bt, const int* __restrict__ row_bt,
+                                       const int* __restrict__ row_pos, const float* __restrict__ cos_tab,
+                                       const float* __restrict__ sin_tab, int nq, int nkv, int layer, int n_layers) {
+    const int m = blockIdx.x;
+    const int pos = row_pos[m];
+    const int width = (nq + 2 * nkv) * 128;
+    const float* row = qkv + static_cast<size_t>(m) * width;
+    const float* cs = cos_tab + static_cast<size_t>(pos) * 64;
+    const float* sn = sin_tab + static_cast<size_t>(pos) * 64;
+    const int block = bt[row_bt[m] + (pos >> 4)];
+    const int slot = pos & 15;
+    const size_t head_stride = 16 * 128;
+    __nv_bfloat16* kbase =
+        pool + ((static_cast<size_t>(block) * n_layers + layer) * 2) * nkv * head_stride + slot * 128;
+    __nv_bfloat16* vbase = kbase + nkv * head_stride;
+    // rotary pairs: (nq + nkv) heads x 64 pairs
+    const int n_pairs = (nq + nkv) * 64;
+    for (int t = threadIdx.x; t < n_pairs; t += blockDim.x) {
+        const int h = t >> 6, i = t & 63;
+        const int c0 = h * 128 + i, c1 = c0 + 64;
+        float a = row[c0], b = row[c1];
+        if (bias) {
+            a += bf2f(bias[c0]);
+            b += bf2f(bias[c1]);
+        }
+        const float ra = a * cs[i] - b * sn[i];
+        const float rb = b * cs[i] + a * sn[i];
+        if (h < nq) {
+            __nv_bfloat16* qo = q_out + static_cast<size_t>(m) * nq * 128 + h * 128;
+            qo[i] = f2bf(ra);
+            qo[i + 64] = f2bf(rb);
+        } else {
+            __nv_bfloat16* ko = kbase + (h - nq) * head_stride;
+            ko[i] = f2bf(ra);
+            ko[i + 64] = f2bf(rb);
+        }
+    }
+    const int vcols = nkv * 128;
+    for (int t = threadIdx.x; t < vcols; t += blockDim.x) {
+        const int c = (nq + nkv) * 128 + t;
+        float v = row[c];
+        if (bias) v += bf2f(bias[c]);
+        vbase[(t >> 7) * head_stride + (t & 127)] = f2bf(v);
+    }
+}
+
+// ---------------------------------------------------------------- SiLU * up
+__global__ void silu_mul_kernel(const float* __restrict__ gu, __nv_bfloat16* __restrict__ act, long long n_pairs4) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n_pairs4;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        // 4 (gate, up) pairs = 8 floats -> 4 bf16
+        const float4 a = reinterpret_cast<const float4*>(gu)[2 * i];
+        const float4 b = reinterpret_cast<const float4*>(gu)[2 * i + 1];
+        const float s0 = a.x / (1.f + __expf(-a.x)) * a.y;
+        const float s1 = a.z / (1.f + __expf(-a.z)) * a.w;
+        const float s2 = b.x / (1.f + __expf(-b.x)) * b.y;
+        const float s3 = b.z / (1.f + __expf(-b.z)) * b.w;
+        reinterpret_cast<uint2*>(act)[i] = make_uint2(pack_bf16x2(s0, s1), pack_bf16x2(s2, s3));
+    }
+}
+
+// ---------------------------------------------------------------- greedy sampling
+__global__ void argmax_emit_kernel(const float* __restrict__ logits, int V, const int* rid, const long long* out_idx,
+                                   int* last_tok, int* out_tok) {
+    const int r = blockIdx.x;
+    const float* row = logits + static_cast<size_t>(r) * V;
+    float best = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int v = threadIdx.x; v < V; v += blockDim.x) {
+        const float x = row[v];
+        if (x > best) {  // strictly greater: keeps the lowest index within a thread
+            best = x;
+            bi = v;
+        }
+    }
+    // (value desc, index asc) reduction
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+            best = ob;
+            bi = oi;
+        }
+    }
+    __shared__ float sb[32];
+    __shared__ int si[32];
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        sb[w] = best;
+        si[w] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int nw = blockDim.x >> 5;
+        for (int i = 1; i < nw; ++i)
+            if (sb[i] > best || (sb[i] == best && si[i] < bi)) {
+                best = sb[i];
+                bi = si[i];
+            }
+        last_tok[rid[r]] = bi;
+        out_tok[out_idx[r]] = bi;
+    }
+}
+
+// ---------------------------------------------------------------- KV handoff
+// grid = (n_blocks, chunks per block); each CTA moves one 64 KiB slice with 16 B
+// vectors, 4 in flight per thread.
+__global__ void kv_copy_kernel(const uint4* __restrict__ src, const int* __restrict__ src_ids, uint4* __restrict__ dst,
+                               const int* __restrict__ dst_ids, long long block_vec, long long chunk_vec) {
+    const long long b = blockIdx.x;
+    const long long s0 = static_cast<long long>(src_ids[b]) * block_vec + blockIdx.y * chunk_vec;
+    const long long d0 = static_cast<long long>(dst_ids[b]) * block_vec + blockIdx.y * chunk_vec;
+    const long long n = min(chunk_vec, block_vec - static_cast<long long>(blockIdx.y) * chunk_vec);
+    long long i = threadIdx.x;
+    for (; i + 3 * blockDim.x < n; i += 4 * blockDim.x) {
+        const uint4 a = src[s0 + i], bb = src[s0 + i + blockDim.x], c = src[s0 + i + 2 * blockDim.x],
+                    d = src[s0 + i + 3 * blockDim.x];
+        dst[d0 + i] = a;
+        dst[d0 + i + blockDim.x] = bb;
+        dst[d0 + i + 2 * blockDim.x] = c;
+        dst[d0 + i + 3 * blockDim.x] = d;
+    }
+    for (; i < n; i += blockDim.x) dst[d0 + i] = src[s0 + i];
+}
+
+__global__ void copy_token_kernel(const int* src, long long si, int* dst, long long di, int* dst2, long long di2) {
+    const int v = src[si];
+    dst[di] = v;
+    if (dst2) dst2[di2] = v;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ck_device_sms(void) {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+    return n;
+}
+
+int ck_init_uniform(void* out, long long n, unsigned long long seed, unsigned long long tensor_id, float scale,
+                    float offset, void* stream) {
+    if (n <= 0) return 0;
+    const float step = scale * (1.0f / 8388608.0f);  // exact: power-of-two scaling
+    const int grid = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 32));
+    init_uniform_kernel<<<grid, 256, 0, S(stream)>>>(static_cast<__nv_bfloat16*>(out), n, seed, tensor_id, step,
+                                                     offset);
+    return ret();
+}
+
+int ck_prompt_tokens(int* out, const int* req_id, const int* pos, int n, unsigned long long seed, int vocab,
+                     void* stream) {
+    if (n <= 0) return 0;
+    prompt_tokens_kernel<<<(n + 255) / 256, 256, 0, S(stream)>>>(out, req_id, pos, n, seed, vocab);
+    return ret();
+}
+
+int ck_rope_table(float* c, float* s, int max_pos, double theta, void* stream) {
+    const int n = max_pos * 64;
+    rope_table_kernel<<<(n + 255) / 256, 256, 0, S(stream)>>>(c, s, max_pos, theta);
+    return ret();
+}
+
+int ck_embed(float* x, const void* emb, const int* row_rid, const int* row_pos, const int* row_dec, const int* prompt,
+             const long long* prompt_off, const int* last_tok, int M, int H, void* stream) {
+    if (M <= 0) return 0;
+    if (H % 8) return static_cast<int>(cudaErrorInvalidValue);
+    embed_kernel<<<M, 128, 0, S(stream)>>>(x, static_cast<const __nv_bfloat16*>(emb), row_rid, row_pos, row_dec,
+                                          prompt, prompt_off, last_tok, H);
+    return ret();
+}
+
+int ck_rmsnorm(const float* x, const void* gamma, void* out, const int* rows, int R, int H, float eps, void* stream) {
+    if (R <= 0) return 0;
+    if (H % 4) return static_cast<int>(cudaErrorInvalidValue);
+    const int threads = H >= 1024 ? 256 : 64;
+    rmsnorm_kernel<<<R, threads, 0, S(stream)>>>(x, static_cast<const __nv_bfloat16*>(gamma),
+                                                 static_cast<__nv_bfloat16*>(out), rows, H, eps);
+    return ret();
+}
+
+int ck_qkv_rope_append(const float* qkv, const void* bias, void* q_out, void* kv_pool, const int* bt,
+                       const int* row_bt, const int* row_pos, const float* cos_tab, const float* sin_tab, int M,
+                       int nq, int nkv, int layer, int n_layers, void* stream) {
+    if (M <= 0) return 0;
+    qkv_rope_append_kernel<<<M, 256, 0, S(stream)>>>(qkv, static_cast<const __nv_bfloat16*>(bias),
+                                                     static_cast<__nv_bfloat16*>(q_out),
+                                                     static_cast<__nv_bfloat16*>(kv_pool), bt, row_bt, row_pos,
+                                                     cos_tab, sin_tab, nq, nkv, layer, n_layers);
+    return ret();
+}
+
+int ck_silu_mul(const float* gu, void* act, int M, int F, void* stream) {
+    if (M <= 0) return 0;
+    if (F % 4) return static_cast<int>(cudaErrorInvalidValue);
+    const long long n4 = static_cast<long long>(M) * F / 4;
+    const int grid = static_cast<int>(std::min<long long>((n4 + 255) / 256, 148LL * 16));
+    silu_mul_kernel<<<grid, 256, 0, S(stream)>>>(gu, static_cast<__nv_bfloat16*>(act), n4);
+    return ret();
+}
+
+int ck_argmax_emit(const float* logits, int R, int V, const int* rid, const long long* out_idx, int* last_tok,
+                   int* out_tok, void* stream) {
+    if (R <= 0) return 0;
+    argmax_emit_kernel<<<R, 1024, 0, S(stream)>>>(logits, V, rid, out_idx, last_tok, out_tok);
+    return ret();
+}
+
+int ck_kv_copy(const void* src_pool, const int* src_ids, void* dst_pool, const int* dst_ids, int n_blocks,
+               long long block_bytes, void* stream) {
+    if (n_blocks <= 0) return 0;
+    if (block_bytes % 16) return static_cast<int>(cudaErrorInvalidValue);
+    const long long block_vec = block_bytes / 16;
+    const long long chunk_vec = std::min<long long>(block_vec, 65536 / 16);
+    const dim3 grid(n_blocks, static_cast<unsigned>((block_vec + chunk_vec - 1) / chunk_vec));
+    kv_copy_kernel<<<grid, 256, 0, S(stream)>>>(static_cast<const uint4*>(src_pool), src_ids,
+                                                static_cast<uint4*>(dst_pool), dst_ids, block_vec, chunk_vec);
+    return ret();
+}
+
+int ck_copy_token(const int* src, long long si, int* dst, long long di, int* dst2, long long di2, void* stream) {
+    copy_token_kernel<<<1, 1, 0, S(stream)>>>(src, si, dst, di, dst2, di2);
+    return ret();
+}
+
+}  // extern "C"

@@ -1,0 +1,354 @@
+// Dense projection GEMM on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+//   out[m, n] (op)= sum_k X[m, k] * W[n, k]          X: activations [M, K] bf16
+//                                                    W: weights     [N, K] bf16
+// Every LLaMA/Qwen2 projection (QKV, O, gate_up, down, LM head) is this shape.
+//
+// Design (B200-first, "swap AB"): the weight matrix is the MMA's M operand
+// (128 weight rows per tile, UMMA_M = 128) and the token batch is the MMA's N
+// operand (BN = 32..256 tokens). This one kernel therefore covers
+//   * decode-only CPI iterations (M = n_decode ~ 10..128 tokens): a 128 x BN tile
+//     per 64-deep K step is weight-streaming bound; split-K spreads the weight
+//     stream over all 148 SMs and the fp32 partials meet in L2 via red.add;
+//   * chunked / PPI prefill (M = 512 .. 8192 tokens): 128 x 256 tiles, tensor bound.
+//
+// Warp roles (192 threads, one CTA per SM, persistent over work units):
+//   warp 0      TMA producer (one elected lane): W tile 128x64 + X tile BNx64 per stage
+//   warp 1      MMA issuer (one lane): 4 x tcgen05.mma (K = 16 each) per stage
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> global (bf16 / fp32 / red.add)
+// Pipelines: STAGES-deep smem ring (full/empty mbarriers) and a double-buffered
+// TMEM accumulator (tmem_full/tmem_empty) so the epilogue of unit i overlaps the
+// MMAs of unit i+1.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+#include "cronus_ck.h"
+
+namespace {
+
+using namespace ck;
+
+constexpr int kThreads = 192;
+constexpr int kTileN = 128;  // weight rows per tile (UMMA M)
+constexpr int kTileK = 64;   // K per stage: one 128-byte swizzle row of bf16
+
+struct GemmParams {
+    void* out;
+    const __nv_bfloat16* bias;  // [N] or null, added once (by split 0)
+    int M, N, K, ldo;
+    int m_tiles, splits, kb_total, kb_per_split, units;
+    int epi;
+};
+
+template <int BN>
+struct Cfg {
+    static constexpr int kABytes = kTileN * kTileK * 2;
+    static constexpr int kBBytes = BN * kTileK * 2;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStages = (196 * 1024) / kStageBytes > 8 ? 8 : (196 * 1024) / kStageBytes;
+    static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+    static constexpr int kSmem = kStages * kStageBytes + 1024 /*align slack*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ void decode_unit(const GemmParams& p, int u, int& nt, int& mt, int& kb0, int& kb1) {
+    const int per_n = p.m_tiles * p.splits;
+    nt = u / per_n;
+    const int r = u - nt * per_n;
+    mt = r / p.splits;
+    const int s = r - mt * p.splits;
+    kb0 = s * p.kb_per_split;
+    kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmParams p) {
+    using C = Cfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + C::kStages * C::kABytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+    uint64_t* empty = full + C::kStages;
+    uint64_t* tfull = empty + C::kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = warp_id();
+    const int lane = lane_id();
+
+    if (warp == 0) {
+        if (lane == 0) {
+            tma_prefetch_desc(&tmW);
+            tma_prefetch_desc(&tmX);
+        }
+        tmem_alloc(tmem_slot, C::kTmemCols);
+        tmem_relinquish();
+    } else if (warp == 1 && lane == 0) {
+        for (int s = 0; s < C::kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+        }
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            const uint64_t keep = policy_evict_last();    // activations: reused by every weight tile
+            const uint64_t stream = policy_evict_first();  // weights: streamed once per launch
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+                int nt, mt, kb0, kb1;
+                decode_unit(p, u, nt, mt, kb0, kb1);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+                    tma_load_2d_hint(sA + stage * C::kABytes, &tmW, &full[stage], kb * kTileK, nt * kTileN, stream);
+                    tma_load_2d_hint(sB + stage * C::kBBytes, &tmX, &full[stage], kb * kTileK, mt * BN, keep);
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_bf16_f32(kTileN, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+                int nt, mt, kb0, kb1;
+                decode_unit(p, u, nt, mt, kb0, kb1);
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sA + stage * C::kABytes);
+                    const uint32_t b0 = smem_u32(sB + stage * C::kBBytes);
+#pragma unroll
+                    for (int k = 0; k < kTileK / 16; ++k)
+                        tc_mma_bf16(d_tmem, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc,
+                                    (kb > kb0 || k > 0) ? 1u : 0u);
+                    tc_commit(&empty[stage]);  // smem slot free once these MMAs retire
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                tc_commit(&tfull[acc]);  // accumulator ready for the epilogue
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int row = q * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+            int nt, mt, kb0, kb1;
+            decode_unit(p, u, nt, mt, kb0, kb1);
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int n = nt * kTileN + row;
+            const int m_base = mt * BN;
+            float bias = 0.f;
+            if (p.bias != nullptr && kb0 == 0) bias = bf2f(p.bias[n]);
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 16) {
+                if (m_base + c >= p.M) break;  // warp-uniform
+                uint32_t v[16];
+                tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c, v);
+                tmem_ld_wait();
+                const int mlim = min(16, p.M - (m_base + c));
+                if (p.epi == CK_EPI_BF16) {
+                    __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + static_cast<size_t>(m_base + c) * p.ldo + n;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (j < mlim) o[static_cast<size_t>(j) * p.ldo] = f2bf(__uint_as_float(v[j]) + bias);
+                } else if (p.epi == CK_EPI_F32) {
+                    float* o = static_cast<float*>(p.out) + static_cast<size_t>(m_base + c) * p.ldo + n;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (j < mlim) o[static_cast<size_t>(j) * p.ldo] = __uint_as_float(v[j]) + bias;
+                } else {
+                    float* o = static_cast<float*>(p.out) + static_cast<size_t>(m_base + c) * p.ldo + n;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (j < mlim) red_add_f32(o + static_cast<size_t>(j) * p.ldo, __uint_as_float(v[j]) + bias);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, C::kTmemCols);
+    }
+}
+
+// ------------------------------------------------------------------ host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<EncodeFn>(f);
+    }();
+    return fn;
+}
+
+struct MapKey {
+    const void* ptr;
+    long long rows, cols;
+    int box_rows;
+    bool operator==(const MapKey& o) const {
+        return ptr == o.ptr && rows == o.rows && cols == o.cols && box_rows == o.box_rows;
+    }
+};
+struct MapKeyHash {
+    size_t operator()(const MapKey& k) const {
+        return std::hash<const void*>()(k.ptr) ^ (std::hash<long long>()(k.rows) * 31) ^
+               (std::hash<long long>()(k.cols) * 131) ^ static_cast<size_t>(k.box_rows) * 7919;
+    }
+};
+
+std::mutex g_map_mu;
+std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+// Row-major [rows, cols] bf16 matrix, tile box = 64 columns x box_rows rows, 128B swizzle.
+int tensor_map(const void* ptr, long long rows, long long cols, int box_rows, CUtensorMap* out) {
+    const MapKey key{ptr, rows, cols, box_rows};
+    {
+        std::lock_guard<std::mutex> g(g_map_mu);
+        auto it = g_maps.find(key);
+        if (it != g_maps.end()) {
+            *out = it->second;
+            return 0;
+        }
+    }
+    EncodeFn enc = encode_fn();
+    if (!enc) return static_cast<int>(cudaErrorNotSupported);
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kTileK), static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return static_cast<int>(cudaErrorInvalidValue);
+    std::lock_guard<std::mutex> g(g_map_mu);
+    if (g_maps.size() > 65536) g_maps.clear();
+    g_maps.emplace(key, *out);
+    return 0;
+}
+
+int num_sms() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+template <int BN>
+int launch(const CUtensorMap& mw, const CUtensorMap& mx, GemmParams p, int max_ctas, cudaStream_t s) {
+    using C = Cfg<BN>;
+    static unsigned attr_set_mask = 0;  // per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr_set_mask & (1u << dev))) {
+        cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+        if (e != cudaSuccess) return static_cast<int>(e);
+        attr_set_mask |= 1u << dev;
+    }
+    const int grid = std::min(p.units, max_ctas > 0 ? max_ctas : num_sms());
+    gemm_tc_kernel<BN><<<grid, kThreads, C::kSmem, s>>>(mw, mx, p);
+    return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace
+
+extern "C" int ck_gemm(const void* W, const void* X, void* out, const void* bias, int M, int N, int K, int ldo,
+                       int epi, int splits, int max_ctas, void* stream) {
+    if (M <= 0) return 0;
+    if (N % kTileN != 0 || K % kTileK != 0 || N <= 0 || K <= 0) return static_cast<int>(cudaErrorInvalidValue);
+    if ((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(X)) & 15) return static_cast<int>(cudaErrorMisalignedAddress);
+    if (epi < CK_EPI_BF16 || epi > CK_EPI_RED_F32) return static_cast<int>(cudaErrorInvalidValue);
+    const int BN = M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
+    GemmParams p{};
+    p.out = out;
+    p.bias = static_cast<const __nv_bfloat16*>(bias);
+    p.M = M;
+    p.N = N;
+    p.K = K;
+    p.ldo = ldo > 0 ? ldo : N;
+    p.epi = epi;
+    p.m_tiles = (M + BN - 1) / BN;
+    p.kb_total = K / kTileK;
+    const int tiles = (N / kTileN) * p.m_tiles;
+    const int sms = max_ctas > 0 ? max_ctas : num_sms();
+    if (splits <= 0) {
+        // Auto split-K (only legal when partial sums can be combined by red.add):
+        // aim for >= one unit per SM while keeping >= 4 K-blocks per unit.
+        splits = 1;
+        if (epi == CK_EPI_RED_F32 && tiles < sms) {
+            splits = (sms + tiles - 1) / tiles;
+            splits = std::min(splits, std::max(1, p.kb_total / 4));
+        }
+    }
+    if (splits > 1 && epi != CK_EPI_RED_F32) return static_cast<int>(cudaErrorInvalidValue);
+    splits = std::min(splits, p.kb_total);
+    p.kb_per_split = (p.kb_total + splits - 1) / splits;
+    p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;  // no empty splits
+    p.units = tiles * p.splits;
+
+    CUtensorMap mw, mx;
+    int rc = tensor_map(W, N, K, kTileN, &mw);
+    if (rc) return rc;
+    rc = tensor_map(X, M, K, BN, &mx);
+    if (rc) return rc;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    switch (BN) {
+        case 32: return launch<32>(mw, mx, p, max_ctas, s);
+        case 64: return launch<64>(mw, mx, p, max_ctas, s);
+        case 128: return launch<128>(mw, mx, p, max_ctas, s);
+        default: return launch<256>(mw, mx, p, max_ctas, s);
+    }
+}

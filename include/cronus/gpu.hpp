@@ -1,0 +1,58 @@
+// B200 extension of the drop-in API: the same scheduler
+// as cronus::run, with its three work sites executed on B200 workers.
+//
+//   cronus::GpuEngine eng("model = llama3-8b\nclock = wall\nppi_sms = 40\n");
+//   cronus::RunReport rep = eng.run(cfg, trace);          // same RunReport as the CPU simulator
+//
+// Engine options are a separate `key = value` text (never part of ClusterConfig:
+// the shared config format rejects unknown keys):
+//   model        llama3-8b | qwen2-7b | tiny | tiny-qwen      (default llama3-8b)
+//   clock        virtual | wall   virtual: cost-model clock, oracle-identical
+//                                 schedule, every batch executed on the GPU;
+//                                 wall: scheduler driven by CUDA-event times
+//   ppi_device, cpi_device        CUDA devices of the two workers (equal = co-located)
+//   ppi_sms      SMs granted to the PPI when co-located (0 = no partition)
+//   ppi_chunk    max rows per PPI forward pass (longer prefixes run in sub-passes)
+//   cpi_pool_blocks, ppi_pool_blocks   physical KV pool sizes (0 = the profile's capacity)
+//   seed, prompt_seed                  weight / prompt-token hash seeds
+//   profile      1: time kernel classes with CUDA events (stats JSON)
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <string>
+
+#include "cronus/engine.hpp"
+
+namespace cronus {
+
+struct GpuRunOptions : RunOptions {
+    // e2e mode: prompt tokens come from this host array (concatenated per request in
+    // trace order) and generated tokens are written back to `host_tokens`
+    // (concatenated, output_len per request). Null: prompts are synthesized on the
+    // device (splitmix64 of (prompt_seed, request id, position)).
+    const int32_t* host_prompt = nullptr;
+    int32_t* host_tokens = nullptr;
+    std::string* stats_json = nullptr;  // kernel / iteration statistics
+};
+
+class GpuEngine {
+  public:
+    explicit GpuEngine(const std::string& engine_options);
+    ~GpuEngine();
+    GpuEngine(const GpuEngine&) = delete;
+    GpuEngine& operator=(const GpuEngine&) = delete;
+
+    RunReport run(const ClusterConfig& cfg, const Trace& trace, const GpuRunOptions& opts = {});
+
+    struct Impl;
+
+  private:
+    std::unique_ptr<Impl> impl_;
+};
+
+// One-shot convenience: build an engine, serve, tear down.
+RunReport run(const ClusterConfig& cfg, const Trace& trace, const GpuRunOptions& opts,
+              const std::string& engine_options);
+
+}  // namespace cronus

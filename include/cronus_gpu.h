@@ -1,0 +1,34 @@
+/* cronus_gpu.h — C-ABI of the B200 serving engine (libcronus_b200.so).
+ *
+ * Wraps cronus::GpuEngine (include/cronus/gpu.hpp): the reference's `run`
+ * (proj/include/cronus/engine.hpp:18) with its three cost-model work sites
+ * (engine.cpp:473, :551, :580) executed on B200 workers. Return codes as in
+ * cronus_capi.h (0 ok, 1 invalid argument, 2 runtime error, 3 other).
+ */
+#ifndef CRONUS_GPU_H
+#define CRONUS_GPU_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* engine_options: `key = value` lines (see include/cronus/gpu.hpp). Allocates the
+ * model weights on the worker device(s). */
+int cronus_engine_create(const char* engine_options, void** engine_out);
+void cronus_engine_destroy(void* engine);
+
+/* Serve one trace. host_prompt (nullable): concatenated prompt tokens in trace
+ * order (e2e mode: copied H2D inside the call); host_tokens (nullable): receives
+ * the generated tokens (output_len per request, concatenated). Outputs are the
+ * reference's report_to_json(rep, true), event log and csv_row, plus a stats JSON
+ * (kernel timings when the engine was created with profile = 1). */
+int cronus_engine_serve(void* engine, const char* cfg_text, int n, const int* id, const double* arrival_ms,
+                        const int* input_len, const int* output_len, const char* trace_name,
+                        const int* host_prompt, int* host_tokens, int want_events, char** json_out,
+                        char** events_out, char** csv_out, char** stats_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CRONUS_GPU_H */

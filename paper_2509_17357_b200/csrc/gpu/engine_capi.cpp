@@ -1,0 +1,74 @@
+// include/cronus_gpu.h: C-ABI over cronus::GpuEngine.
+#include <cstdlib>
+#include <cstring>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+
+#include "cronus/gpu.hpp"
+#include "cronus_gpu.h"
+
+namespace cronus {
+namespace capi {
+Trace trace_from(int n, const int* id, const double* arr, const int* in, const int* out, const char* name);
+void set_error(const std::string& m);
+}  // namespace capi
+}  // namespace cronus
+
+namespace {
+char* dup(const std::string& s) {
+    char* p = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(p, s.c_str(), s.size() + 1);
+    return p;
+}
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        cronus::capi::set_error(e.what());
+        return 1;
+    } catch (const std::runtime_error& e) {
+        cronus::capi::set_error(e.what());
+        return 2;
+    } catch (const std::exception& e) {
+        cronus::capi::set_error(e.what());
+        return 3;
+    }
+}
+}  // namespace
+
+extern "C" {
+
+int cronus_engine_create(const char* engine_options, void** engine_out) {
+    return guard([&] { *engine_out = new cronus::GpuEngine(engine_options ? engine_options : ""); });
+}
+
+void cronus_engine_destroy(void* engine) { delete static_cast<cronus::GpuEngine*>(engine); }
+
+int cronus_engine_serve(void* engine, const char* cfg_text, int n, const int* id, const double* arrival_ms,
+                        const int* input_len, const int* output_len, const char* trace_name, const int* host_prompt,
+                        int* host_tokens, int want_events, char** json_out, char** events_out, char** csv_out,
+                        char** stats_out) {
+    return guard([&] {
+        auto* eng = static_cast<cronus::GpuEngine*>(engine);
+        if (!eng) throw std::invalid_argument("null engine");
+        const cronus::ClusterConfig cfg = cronus::parse_config(cfg_text);
+        const cronus::Trace t = cronus::capi::trace_from(n, id, arrival_ms, input_len, output_len, trace_name);
+        std::ostringstream ev;
+        std::string stats;
+        cronus::GpuRunOptions o;
+        o.event_log = want_events ? &ev : nullptr;
+        o.host_prompt = host_prompt;
+        o.host_tokens = host_tokens;
+        o.stats_json = &stats;
+        const cronus::RunReport rep = eng->run(cfg, t, o);
+        if (json_out) *json_out = dup(cronus::report_to_json(rep, true));
+        if (events_out) *events_out = dup(ev.str());
+        if (csv_out) *csv_out = dup(cronus::csv_row(rep));
+        if (stats_out) *stats_out = dup(stats);
+    });
+}
+
+}  // extern "C"

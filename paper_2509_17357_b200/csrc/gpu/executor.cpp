@@ -1,0 +1,603 @@
+// GpuEngine: persistent B200 resources (weights, KV pools, workers, streams) and the
+// per-run executor that turns the scheduler's work items into device work.
+//
+// Stream topology per worker pair:
+//   ppi stream  (PPI device)  partial prefills; SM-partitioned when co-located
+//   cpi stream  (CPI device)  mixed chunk + decode iterations
+//   copy stream (CPI device)  KV handoff: pull kernel over NVLink (or D2D)
+// Cross-stream ordering is by CUDA events only:
+//   handoff  waits  the request's prefill            (its KV exists)
+//            waits  the CPI release fence           (destination blocks are free)
+//   CPI iter waits  the handoff of every request it touches for the first time
+//   PPI pass waits  the PPI release fence           (reused blocks were copied out)
+// so the GPU may run arbitrarily far behind the scheduler (virtual clock) and
+// still execute exactly the scheduled work, and in wall-clock mode the copy
+// stream overlaps CPI compute.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <memory>
+#include <sstream>
+#include <stdexcept>
+#include <thread>
+
+#include "../host/scheduler.hpp"
+#include "cronus/gpu.hpp"
+#include "cronus_ck.h"
+#include "model.hpp"
+
+namespace cronus {
+
+using gpu::check_ck;
+using gpu::check_cuda;
+
+namespace {
+
+struct EngineOptions {
+    std::string model = "llama3-8b";
+    bool wall = false;
+    int ppi_device = 0, cpi_device = 0;
+    int ppi_sms = 0;
+    int ppi_chunk = 4096;
+    long long cpi_pool_blocks = 0, ppi_pool_blocks = 0;
+    uint64_t seed = 1234, prompt_seed = 99;
+    bool profile = false;
+};
+
+EngineOptions parse_engine_options(const std::string& text) {
+    EngineOptions o;
+    std::istringstream in(text);
+    std::string line;
+    while (std::getline(in, line)) {
+        const size_t hash = line.find('#');
+        if (hash != std::string::npos) line = line.substr(0, hash);
+        const size_t eq = line.find('=');
+        auto strip = [](std::string s) {
+            const size_t a = s.find_first_not_of(" \t\r");
+            if (a == std::string::npos) return std::string();
+            return s.substr(a, s.find_last_not_of(" \t\r") - a + 1);
+        };
+        if (eq == std::string::npos) {
+            if (!strip(line).empty()) throw std::invalid_argument("engine options: expected key = value: " + line);
+            continue;
+        }
+        const std::string k = strip(line.substr(0, eq)), v = strip(line.substr(eq + 1));
+        if (k == "model") o.model = v;
+        else if (k == "clock") {
+            if (v != "virtual" && v != "wall") throw std::invalid_argument("engine options: clock = virtual | wall");
+            o.wall = v == "wall";
+        } else if (k == "ppi_device") o.ppi_device = std::stoi(v);
+        else if (k == "cpi_device") o.cpi_device = std::stoi(v);
+        else if (k == "ppi_sms") o.ppi_sms = std::stoi(v);
+        else if (k == "ppi_chunk") o.ppi_chunk = std::stoi(v);
+        else if (k == "cpi_pool_blocks") o.cpi_pool_blocks = std::stoll(v);
+        else if (k == "ppi_pool_blocks") o.ppi_pool_blocks = std::stoll(v);
+        else if (k == "seed") o.seed = std::stoull(v);
+        else if (k == "prompt_seed") o.prompt_seed = std::stoull(v);
+        else if (k == "profile") o.profile = v == "1" || v == "true";
+        else throw std::invalid_argument("engine options: unknown key " + k);
+    }
+    if (o.ppi_chunk < 16 || o.ppi_chunk % 16) throw std::invalid_argument("engine options: ppi_chunk % 16 != 0");
+    return o;
+}
+
+struct DeviceBuf {
+    int dev = 0;
+    void* p = nullptr;
+    size_t cap = 0;
+    void ensure(int device, size_t bytes) {
+        if (bytes <= cap && p) return;
+        release();
+        dev = device;
+        check_cuda(cudaSetDevice(dev), "cudaSetDevice");
+        check_cuda(cudaMalloc(&p, std::max<size_t>(bytes, 256)), "cudaMalloc(request buffers)");
+        cap = std::max<size_t>(bytes, 256);
+    }
+    void release() {
+        if (p) {
+            cudaSetDevice(dev);
+            cudaFree(p);
+        }
+        p = nullptr;
+        cap = 0;
+    }
+    ~DeviceBuf() { release(); }
+};
+
+// Request-token buffers of one device.
+struct TokenBufs {
+    DeviceBuf prompt, prompt_off, last_tok, out_tok;
+};
+
+}  // namespace
+
+struct GpuEngine::Impl {
+    EngineOptions opt;
+    gpu::ModelSpec spec;
+    bool colocated = true;
+    std::shared_ptr<gpu::Weights> w_ppi, w_cpi;
+    std::unique_ptr<gpu::KvPool> pool_ppi, pool_cpi;
+    cudaStream_t s_ppi = nullptr, s_cpi = nullptr, s_copy = nullptr;
+    std::unique_ptr<gpu::Worker> ppi, cpi;
+    int cpi_rows = 0;
+    TokenBufs tok_cpi, tok_ppi;
+    // pinned staging for handoff block lists
+    static constexpr int kRing = 16;
+    int* xfer_host[kRing] = {};
+    cudaEvent_t xfer_ev[kRing] = {};
+    int xfer_slot = 0;
+    DeviceBuf xfer_dev;  // kRing slices
+    long long xfer_cap = 0;  // ints per slice
+    int sms = 148;
+
+    explicit Impl(const std::string& text) : opt(parse_engine_options(text)), spec(gpu::ModelSpec::preset(opt.model)) {
+        spec.seed = opt.seed;
+        colocated = opt.ppi_device == opt.cpi_device;
+        int ndev = 0;
+        check_cuda(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+        if (opt.ppi_device >= ndev || opt.cpi_device >= ndev)
+            throw std::invalid_argument("engine options: device index out of range");
+        check_cuda(cudaSetDevice(opt.cpi_device), "cudaSetDevice");
+        sms = ck_device_sms();
+        w_cpi = std::make_shared<gpu::Weights>(spec, opt.cpi_device);
+        w_ppi = colocated ? w_cpi : std::make_shared<gpu::Weights>(spec, opt.ppi_device);
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        check_cuda(cudaSetDevice(opt.cpi_device), "cudaSetDevice");
+        check_cuda(cudaStreamCreateWithPriority(&s_cpi, cudaStreamNonBlocking, hi), "stream");
+        check_cuda(cudaStreamCreateWithPriority(&s_copy, cudaStreamNonBlocking, hi), "stream");
+        check_cuda(cudaSetDevice(opt.ppi_device), "cudaSetDevice");
+        check_cuda(cudaStreamCreateWithPriority(&s_ppi, cudaStreamNonBlocking, lo), "stream");
+        if (!colocated) {
+            int can = 0;
+            check_cuda(cudaDeviceCanAccessPeer(&can, opt.cpi_device, opt.ppi_device), "peer query");
+            if (!can) throw std::runtime_error("CPI device cannot access the PPI device over NVLink (no P2P)");
+            check_cuda(cudaSetDevice(opt.cpi_device), "cudaSetDevice");
+            cudaError_t e = cudaDeviceEnablePeerAccess(opt.ppi_device, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) check_cuda(e, "enable peer access");
+            cudaGetLastError();
+        }
+        for (int i = 0; i < kRing; ++i) {
+            check_cuda(cudaEventCreateWithFlags(&xfer_ev[i], cudaEventDisableTiming), "event");
+        }
+    }
+
+    ~Impl() {
+        for (int i = 0; i < kRing; ++i) {
+            if (xfer_host[i]) cudaFreeHost(xfer_host[i]);
+            if (xfer_ev[i]) cudaEventDestroy(xfer_ev[i]);
+        }
+        ppi.reset();
+        cpi.reset();
+        if (s_ppi) cudaStreamDestroy(s_ppi);
+        if (s_cpi) cudaStreamDestroy(s_cpi);
+        if (s_copy) cudaStreamDestroy(s_copy);
+    }
+
+    // Size pools / workers for this config (reallocating only when they grow).
+    void prepare(const ClusterConfig& cfg) {
+        if (cfg.high_gpu.kv_block_size != 16 || cfg.low_gpu.kv_block_size != 16)
+            throw std::invalid_argument("B200 engine: kv_block_size must be 16 (the kernels' page size)");
+        const long long cpi_blocks = opt.cpi_pool_blocks > 0 ? opt.cpi_pool_blocks : cfg.high_gpu.kv_blocks_capacity;
+        const long long ppi_blocks = opt.ppi_pool_blocks > 0 ? opt.ppi_pool_blocks : cfg.low_gpu.kv_blocks_capacity;
+        if (cpi_blocks < cfg.high_gpu.kv_blocks_capacity || ppi_blocks < cfg.low_gpu.kv_blocks_capacity)
+            throw std::invalid_argument("B200 engine: physical KV pools smaller than the profiles' capacities");
+        const long long bb = spec.kv_block_bytes();
+        if (!pool_cpi || pool_cpi->blocks < cpi_blocks) {
+            pool_cpi.reset();
+            pool_cpi = std::make_unique<gpu::KvPool>(opt.cpi_device, cpi_blocks, bb);
+        }
+        if (!pool_ppi || pool_ppi->blocks < ppi_blocks) {
+            pool_ppi.reset();
+            pool_ppi = std::make_unique<gpu::KvPool>(opt.ppi_device, ppi_blocks, bb);
+        }
+        const int B = cfg.max_batched_tokens_high;
+        if (!cpi || cpi_rows < B) {
+            cpi.reset();
+            check_cuda(cudaSetDevice(opt.cpi_device), "cudaSetDevice");
+            cpi = std::make_unique<gpu::Worker>(*w_cpi, B, B, static_cast<int>(pool_cpi->blocks) + B, s_cpi, 0);
+            cpi_rows = B;
+        }
+        if (!ppi) {
+            check_cuda(cudaSetDevice(opt.ppi_device), "cudaSetDevice");
+            const int cap = colocated && opt.ppi_sms > 0 ? opt.ppi_sms : 0;
+            ppi = std::make_unique<gpu::Worker>(*w_ppi, opt.ppi_chunk, 1,
+                                                static_cast<int>(pool_ppi->blocks) + opt.ppi_chunk, s_ppi, cap);
+        }
+        const long long need = 2 * std::max(pool_ppi->blocks, pool_cpi->blocks) + 64;
+        if (xfer_cap < need) {
+            for (int i = 0; i < kRing; ++i) {
+                if (xfer_host[i]) cudaFreeHost(xfer_host[i]);
+                check_cuda(cudaMallocHost(&xfer_host[i], need * 4), "pinned xfer");
+            }
+            xfer_dev.ensure(opt.cpi_device, static_cast<size_t>(need) * 4 * kRing);
+            xfer_cap = need;
+        }
+        cpi->set_profiling(opt.profile);
+        ppi->set_profiling(opt.profile);
+    }
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------------
+class PairExecutor : public sched::Executor {
+  public:
+    PairExecutor(GpuEngine::Impl& e, const Trace& t, const GpuRunOptions& o) : E(e), trace(t), opts(o) {
+        const int n = static_cast<int>(t.requests.size());
+        prompt_off.resize(n);
+        out_off.resize(n);
+        long long pin = 0, pout = 0;
+        for (int i = 0; i < n; ++i) {
+            prompt_off[i] = pin;
+            out_off[i] = pout;
+            pin += t.requests[i].input_len;
+            pout += t.requests[i].output_len;
+        }
+        total_in = pin;
+        total_out = pout;
+        prefill_ev.assign(n, nullptr);
+        xfer_ev.assign(n, nullptr);
+        xfer_pending.assign(n, 0);
+    }
+
+    ~PairExecutor() override {
+        for (auto* v : {&prefill_ev, &xfer_ev})
+            for (cudaEvent_t ev : *v)
+                if (ev) cudaEventDestroy(ev);
+        for (auto& q : done_q)
+            for (auto& t : q) cudaEventDestroy(t.ev);
+        for (cudaEvent_t ev : spare) cudaEventDestroy(ev);
+        if (t0_cpi) cudaEventDestroy(t0_cpi);
+        if (t0_ppi) cudaEventDestroy(t0_ppi);
+        if (pinned_prompt) cudaFreeHost(pinned_prompt);
+    }
+
+    // Request token buffers on each device; prompts from the host (e2e) or synthesized.
+    void upload() {
+        const int n = static_cast<int>(trace.requests.size());
+        auto setup = [&](TokenBufs& tb, int dev, cudaStream_t s) {
+            tb.prompt.ensure(dev, static_cast<size_t>(total_in) * 4);
+            tb.prompt_off.ensure(dev, static_cast<size_t>(n) * 8);
+            tb.last_tok.ensure(dev, static_cast<size_t>(n) * 4);
+            tb.out_tok.ensure(dev, static_cast<size_t>(total_out) * 4);
+            check_cuda(cudaSetDevice(dev), "cudaSetDevice");
+            check_cuda(cudaMemcpyAsync(tb.prompt_off.p, prompt_off.data(), n * 8, cudaMemcpyHostToDevice, s),
+                       "prompt_off H2D");
+            check_cuda(cudaMemsetAsync(tb.out_tok.p, 0xff, static_cast<size_t>(total_out) * 4, s), "memset");
+            if (opts.host_prompt) {
+                if (!pinned_prompt) {
+                    check_cuda(cudaMallocHost(&pinned_prompt, static_cast<size_t>(total_in) * 4), "pinned prompt");
+                    std::memcpy(pinned_prompt, opts.host_prompt, static_cast<size_t>(total_in) * 4);
+                }
+                check_cuda(cudaMemcpyAsync(tb.prompt.p, pinned_prompt, static_cast<size_t>(total_in) * 4,
+                                           cudaMemcpyHostToDevice, s),
+                           "prompt H2D");
+                h2d_bytes += total_in * 4;
+            } else {
+                synth_prompts(tb, s);
+            }
+            h2d_bytes += n * 8;
+        };
+        setup(E.tok_cpi, E.opt.cpi_device, E.s_cpi);
+        if (!E.colocated) setup(E.tok_ppi, E.opt.ppi_device, E.s_ppi);
+        check_cuda(cudaSetDevice(E.opt.cpi_device), "cudaSetDevice");
+        check_cuda(cudaStreamSynchronize(E.s_cpi), "sync");
+        check_cuda(cudaSetDevice(E.opt.ppi_device), "cudaSetDevice");
+        check_cuda(cudaStreamSynchronize(E.s_ppi), "sync");
+    }
+
+    void synth_prompts(TokenBufs& tb, cudaStream_t s) {
+        // request id / position per prompt token -> device hash kernel
+        std::vector<int> rq(total_in), ps(total_in);
+        long long k = 0;
+        for (const Request& r : trace.requests)
+            for (int p = 0; p < r.input_len; ++p, ++k) {
+                rq[k] = r.id;
+                ps[k] = p;
+            }
+        int* d = nullptr;
+        check_cuda(cudaMalloc(&d, static_cast<size_t>(total_in) * 8 + 16), "tmp");
+        check_cuda(cudaMemcpyAsync(d, rq.data(), total_in * 4, cudaMemcpyHostToDevice, s), "H2D");
+        check_cuda(cudaMemcpyAsync(d + total_in, ps.data(), total_in * 4, cudaMemcpyHostToDevice, s), "H2D");
+        check_ck(ck_prompt_tokens(static_cast<int*>(tb.prompt.p), d, d + total_in, static_cast<int>(total_in),
+                                  E.opt.prompt_seed, E.spec.vocab, s),
+                 "prompt_tokens");
+        check_cuda(cudaStreamSynchronize(s), "sync");
+        cudaFree(d);
+    }
+
+    TokenBufs& ppi_tok() { return E.colocated ? E.tok_cpi : E.tok_ppi; }
+
+    // ------------------------------------------------------------- work sites
+    uint64_t prefill(const sched::PrefillWork& w) override {
+        check_cuda(cudaSetDevice(E.opt.ppi_device), "cudaSetDevice");
+        if (ppi_fence) {
+            check_cuda(cudaStreamWaitEvent(E.s_ppi, ppi_fence, 0), "wait fence");
+            ppi_fence = nullptr;
+        }
+        TokenBufs& tb = ppi_tok();
+        const Request& r = trace.requests[w.rid];
+        for (long long start = 0; start < w.tokens; start += E.opt.ppi_chunk) {
+            const long long len = std::min<long long>(E.opt.ppi_chunk, w.tokens - start);
+            const bool last = start + len == w.tokens;
+            batch.clear();
+            batch.add_prefill(w.rid, start, len, *w.blocks, last && w.sample_last, out_off[w.rid]);
+            E.ppi->forward(batch, *E.pool_ppi, static_cast<int*>(tb.prompt.p),
+                           static_cast<long long*>(tb.prompt_off.p), static_cast<int*>(tb.last_tok.p),
+                           static_cast<int*>(tb.out_tok.p));
+        }
+        (void)r;
+        prefill_ev[w.rid] = record(E.s_ppi, prefill_ev[w.rid]);
+        prefill_tokens += w.tokens;
+        return complete(E.s_ppi, 0);
+    }
+
+    uint64_t transfer(const sched::TransferWork& w) override {
+        check_cuda(cudaSetDevice(E.opt.cpi_device), "cudaSetDevice");
+        if (prefill_ev[w.rid]) check_cuda(cudaStreamWaitEvent(E.s_copy, prefill_ev[w.rid], 0), "wait prefill");
+        if (cpi_fence) check_cuda(cudaStreamWaitEvent(E.s_copy, cpi_fence, 0), "wait cpi fence");
+        const int nb = static_cast<int>((w.tokens + 15) / 16);
+        if (static_cast<int>(w.src_blocks->size()) < nb || static_cast<int>(w.dst_blocks->size()) < nb)
+            throw std::logic_error("handoff: block tables shorter than the prefix");
+        const int slot = E.xfer_slot;
+        E.xfer_slot = (E.xfer_slot + 1) % GpuEngine::Impl::kRing;
+        check_cuda(cudaEventSynchronize(E.xfer_ev[slot]), "xfer staging");
+        int* h = E.xfer_host[slot];
+        std::memcpy(h, w.src_blocks->data(), nb * 4);
+        std::memcpy(h + nb, w.dst_blocks->data(), nb * 4);
+        int* d = static_cast<int*>(E.xfer_dev.p) + slot * E.xfer_cap;
+        check_cuda(cudaMemcpyAsync(d, h, 2 * nb * 4, cudaMemcpyHostToDevice, E.s_copy), "xfer ids");
+        check_cuda(cudaEventRecord(E.xfer_ev[slot], E.s_copy), "event");
+        check_ck(ck_kv_copy(E.pool_ppi->base, d, E.pool_cpi->base, d + nb, nb, E.pool_cpi->block_bytes, E.s_copy),
+                 "kv_copy");
+        const Request& r = trace.requests[w.rid];
+        if (!E.colocated && w.tokens == r.input_len) {
+            // the PPI sampled the first token: it travels with the KV
+            check_ck(ck_copy_token(static_cast<int*>(E.tok_ppi.last_tok.p), w.rid,
+                                   static_cast<int*>(E.tok_cpi.last_tok.p), w.rid,
+                                   static_cast<int*>(E.tok_cpi.out_tok.p), out_off[w.rid], E.s_copy),
+                     "copy_token");
+        }
+        xfer_ev[w.rid] = record(E.s_copy, xfer_ev[w.rid]);
+        xfer_pending[w.rid] = 1;
+        handoff_bytes += static_cast<double>(nb) * E.pool_cpi->block_bytes;
+        handoffs++;
+        return complete(E.s_copy, 1);
+    }
+
+    uint64_t iteration(const sched::IterWork& w) override {
+        check_cuda(cudaSetDevice(E.opt.cpi_device), "cudaSetDevice");
+        auto need = [&](int rid) {
+            if (xfer_pending[rid]) {
+                check_cuda(cudaStreamWaitEvent(E.s_cpi, xfer_ev[rid], 0), "wait handoff");
+                xfer_pending[rid] = 0;
+            }
+        };
+        batch.clear();
+        for (const sched::DecodeRow& d : w.decoders) {
+            need(d.rid);
+            const long long emitted = d.ctx - trace.requests[d.rid].input_len;
+            batch.add_decode(d.rid, d.ctx, *d.blocks, out_off[d.rid] + emitted);
+        }
+        if (w.chunk_rid >= 0) {
+            need(w.chunk_rid);
+            batch.add_prefill(w.chunk_rid, w.chunk_start, w.chunk_len, *w.chunk_blocks, w.chunk_samples,
+                              out_off[w.chunk_rid]);
+        }
+        for (int rid : w.finishers) need(rid);
+        if (!batch.d_len.empty()) batch.plan_decode_splits(E.spec.n_kv_heads, 3 * E.sms);
+        E.cpi->forward(batch, *E.pool_cpi, static_cast<int*>(E.tok_cpi.prompt.p),
+                       static_cast<long long*>(E.tok_cpi.prompt_off.p), static_cast<int*>(E.tok_cpi.last_tok.p),
+                       static_cast<int*>(E.tok_cpi.out_tok.p));
+        iters++;
+        iter_rows += batch.rows();
+        decode_rows += static_cast<long long>(w.decoders.size());
+        for (const sched::DecodeRow& d : w.decoders) decode_keys += d.ctx;
+        chunk_rows += w.chunk_len;
+        last_cpi = record(E.s_cpi, last_cpi);
+        return complete(E.s_cpi, 2);
+    }
+
+    void release(int instance, int rid) override {
+        if (instance >= 1000) {
+            // PPI blocks of rid were read by its handoff (none: it failed before one)
+            if (xfer_ev[rid]) ppi_fence = xfer_ev[rid];
+        } else {
+            cpi_fence = last_cpi;      // freed at the end of the latest launched iteration
+        }
+    }
+
+    // ------------------------------------------------------------- clocks
+    bool wall_clock() const override { return E.opt.wall; }
+
+    void start() override {
+        check_cuda(cudaSetDevice(E.opt.cpi_device), "cudaSetDevice");
+        check_cuda(cudaEventCreate(&t0_cpi), "event");
+        check_cuda(cudaEventRecord(t0_cpi, E.s_cpi), "event");
+        check_cuda(cudaSetDevice(E.opt.ppi_device), "cudaSetDevice");
+        check_cuda(cudaEventCreate(&t0_ppi), "event");
+        check_cuda(cudaEventRecord(t0_ppi, E.s_ppi), "event");
+        check_cuda(cudaEventSynchronize(t0_ppi), "sync");
+        check_cuda(cudaSetDevice(E.opt.cpi_device), "cudaSetDevice");
+        check_cuda(cudaEventSynchronize(t0_cpi), "sync");
+        host_t0 = std::chrono::steady_clock::now();
+    }
+
+    double now_ms() override {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
+    }
+
+    bool poll(sched::Completion& out) override {
+        int best = -1;
+        double best_t = 0;
+        for (int q = 0; q < 3; ++q) {
+            if (done_q[q].empty()) continue;
+            Tick& t = done_q[q].front();
+            if (!t.done) {
+                const cudaError_t st = cudaEventQuery(t.ev);
+                if (st == cudaErrorNotReady) continue;
+                check_cuda(st, "event query");
+                float ms = 0.f;
+                check_cuda(cudaEventElapsedTime(&ms, q == 0 ? t0_ppi : t0_cpi, t.ev), "elapsed");
+                t.t = ms;
+                t.done = true;
+            }
+            if (best < 0 || t.t < best_t) {
+                best = q;
+                best_t = t.t;
+            }
+        }
+        if (best < 0) return false;
+        Tick t = done_q[best].front();
+        done_q[best].pop_front();
+        spare.push_back(t.ev);
+        out.ticket = t.ticket;
+        out.t_ms = t.t;
+        return true;
+    }
+
+    void wait(double until_ms) override {
+        // Completions are polled by the scheduler; here we only pass time cheaply.
+        while (now_ms() < until_ms) {
+            for (int q = 0; q < 3; ++q)
+                if (!done_q[q].empty() && (done_q[q].front().done || cudaEventQuery(done_q[q].front().ev) == cudaSuccess))
+                    return;
+            std::this_thread::sleep_for(std::chrono::microseconds(20));
+        }
+    }
+
+    void finish() override {
+        check_cuda(cudaSetDevice(E.opt.ppi_device), "cudaSetDevice");
+        check_cuda(cudaStreamSynchronize(E.s_ppi), "sync ppi");
+        check_cuda(cudaSetDevice(E.opt.cpi_device), "cudaSetDevice");
+        check_cuda(cudaStreamSynchronize(E.s_copy), "sync copy");
+        check_cuda(cudaStreamSynchronize(E.s_cpi), "sync cpi");
+        float ms = 0.f;
+        cudaEvent_t end;
+        check_cuda(cudaEventCreate(&end), "event");
+        check_cuda(cudaEventRecord(end, E.s_cpi), "event");
+        check_cuda(cudaEventSynchronize(end), "sync");
+        check_cuda(cudaEventElapsedTime(&ms, t0_cpi, end), "elapsed");
+        cudaEventDestroy(end);
+        gpu_ms = ms;
+        if (opts.host_tokens) {
+            check_cuda(cudaMemcpy(opts.host_tokens, E.tok_cpi.out_tok.p, static_cast<size_t>(total_out) * 4,
+                                  cudaMemcpyDeviceToHost),
+                       "tokens D2H");
+            d2h_bytes += total_out * 4;
+        }
+        E.cpi->collect_stats();
+        E.ppi->collect_stats();
+    }
+
+    std::string stats() const {
+        std::ostringstream s;
+        auto ks = [&](const char* name, const gpu::KernelStat& k, bool comma = true) {
+            s << "\"" << name << "\": {\"launches\": " << k.launches << ", \"ms\": " << k.ms
+              << ", \"bytes\": " << k.bytes << ", \"flops\": " << k.flops << "}" << (comma ? ", " : "");
+        };
+        s.precision(10);
+        s << "{\"gpu_ms\": " << gpu_ms << ", \"cpi_iterations\": " << iters << ", \"iter_rows\": " << iter_rows
+          << ", \"decode_rows\": " << decode_rows << ", \"decode_keys\": " << decode_keys
+          << ", \"chunk_rows\": " << chunk_rows << ", \"prefill_tokens\": " << prefill_tokens
+          << ", \"handoffs\": " << handoffs << ", \"handoff_bytes\": " << handoff_bytes
+          << ", \"h2d_bytes\": " << h2d_bytes << ", \"d2h_bytes\": " << d2h_bytes
+          << ", \"kernel_launches_per_forward_layer\": 9"
+          << ", \"colocated\": " << (E.colocated ? "true" : "false") << ", \"sms\": " << E.sms << ", \"cpi\": {";
+        ks("decode_attn", E.cpi->stat_decode_attn);
+        ks("prefill_attn", E.cpi->stat_prefill_attn);
+        ks("gemm", E.cpi->stat_gemm);
+        ks("other", E.cpi->stat_other);
+        ks("forward", E.cpi->stat_forward, false);
+        s << "}, \"ppi\": {";
+        ks("prefill_attn", E.ppi->stat_prefill_attn);
+        ks("gemm", E.ppi->stat_gemm);
+        ks("other", E.ppi->stat_other);
+        ks("forward", E.ppi->stat_forward, false);
+        s << "}}";
+        return s.str();
+    }
+
+  private:
+    GpuEngine::Impl& E;
+    const Trace& trace;
+    const GpuRunOptions& opts;
+    std::vector<long long> prompt_off, out_off;
+    long long total_in = 0, total_out = 0;
+    int* pinned_prompt = nullptr;
+    gpu::Batch batch;
+    std::vector<cudaEvent_t> prefill_ev, xfer_ev;
+    std::vector<char> xfer_pending;
+    cudaEvent_t ppi_fence = nullptr, cpi_fence = nullptr, last_cpi = nullptr;
+    struct Tick {
+        uint64_t ticket;
+        cudaEvent_t ev;
+        bool done;
+        double t;
+    };
+    std::deque<Tick> done_q[3];
+    std::vector<cudaEvent_t> spare;
+    uint64_t next_ticket = 1;
+    cudaEvent_t t0_cpi = nullptr, t0_ppi = nullptr;
+    std::chrono::steady_clock::time_point host_t0;
+
+  public:
+    double gpu_ms = 0;
+    long long iters = 0, iter_rows = 0, decode_rows = 0, decode_keys = 0, chunk_rows = 0, prefill_tokens = 0;
+    long long handoffs = 0;
+    double handoff_bytes = 0, h2d_bytes = 0, d2h_bytes = 0;
+
+  private:
+    // One reusable event per request role, re-recorded (never timing-critical).
+    cudaEvent_t record(cudaStream_t s, cudaEvent_t ev) {
+        if (!ev) check_cuda(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+        check_cuda(cudaEventRecord(ev, s), "event record");
+        return ev;
+    }
+    uint64_t complete(cudaStream_t s, int q) {
+        const uint64_t t = next_ticket++;
+        if (!E.opt.wall) return t;  // virtual clock: completions come from the cost model
+        cudaEvent_t ev;
+        if (!spare.empty()) {
+            ev = spare.back();
+            spare.pop_back();
+        } else {
+            check_cuda(cudaEventCreate(&ev), "event");
+        }
+        check_cuda(cudaEventRecord(ev, s), "event record");
+        done_q[q].push_back(Tick{t, ev, false, 0.0});
+        return t;
+    }
+};
+
+}  // namespace
+
+GpuEngine::GpuEngine(const std::string& engine_options) : impl_(std::make_unique<Impl>(engine_options)) {}
+GpuEngine::~GpuEngine() = default;
+
+RunReport GpuEngine::run(const ClusterConfig& cfg, const Trace& trace, const GpuRunOptions& opts) {
+    if (cfg.policy != Policy::Cronus)
+        throw std::invalid_argument("B200 engine: only the cronus policy runs on the GPU workers (baselines: "
+                                    "use the virtual-clock cronus::run)");
+    const auto errs = validate_config(cfg);
+    if (!errs.empty() || trace.requests.empty()) return cronus::run(cfg, trace, opts);  // throws the same errors
+    impl_->prepare(cfg);
+    PairExecutor ex(*impl_, trace, opts);
+    ex.upload();
+    sched::SchedulerHooks hooks;
+    hooks.executor = &ex;
+    RunReport rep = sched::run_scheduler(cfg, trace, opts, hooks);
+    if (opts.stats_json) *opts.stats_json = ex.stats();
+    return rep;
+}
+
+RunReport run(const ClusterConfig& cfg, const Trace& trace, const GpuRunOptions& opts,
+              const std::string& engine_options) {
+    GpuEngine eng(engine_options);
+    return eng.run(cfg, trace, opts);
+}
+
+}  // namespace cronus

@@ -85,8 +85,9 @@ __global__ void __launch_bounds__(128)
         for (int i = 0; i < 8; ++i) kv4[i] = __ldg(kp + i);
         uint2 vv[16];
         const uint2* vp = reinterpret_cast<const uint2*>(vt) + lane;  // dims 4*lane..4*lane+3
+        const int n_valid = min(kBlk, len - b * kBlk);  // slots past the sequence end hold stale data
 #pragma unroll
-        for (int j = 0; j < 16; ++j) vv[j] = __ldg(vp + j * (kHD / 4));
+        for (int j = 0; j < 16; ++j) vv[j] = j < n_valid ? __ldg(vp + j * (kHD / 4)) : make_uint2(0u, 0u);
 
         // ---- scores
         float sc[G];

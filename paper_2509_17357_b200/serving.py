@@ -1,0 +1,62 @@
+"""Python mirror of cronus::GpuEngine (include/cronus/gpu.hpp, include/cronus_gpu.h).
+
+    eng = GpuEngine(model="llama3-8b", clock="wall", ppi_sms=40)
+    res = eng.serve(cfg_text, trace)                # RunResult: reference-format json/events/csv
+    res = eng.serve(cfg_text, trace, host_prompt=p)  # e2e: prompts H2D, tokens D2H inside the call
+
+Every call goes to libcronus_b200.so; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+
+import numpy as np
+
+from ._lib import check, lib, take_string
+from .engine import RunResult, Trace
+
+
+def _p(a, t):
+    return a.ctypes.data_as(ctypes.POINTER(t))
+
+
+class GpuEngine:
+    def __init__(self, **options):
+        text = "".join(f"{k} = {v}\n" for k, v in options.items())
+        h = ctypes.c_void_p()
+        check(lib().cronus_engine_create(text.encode(), ctypes.byref(h)))
+        self._h = h
+        self.options = options
+
+    def close(self):
+        if self._h:
+            lib().cronus_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def serve(self, cfg_text: str, trace: Trace, host_prompt=None, want_tokens=False, events=True) -> RunResult:
+        ids, arr, ins, outs = trace.arrays()
+        hp = None
+        if host_prompt is not None:
+            host_prompt = np.ascontiguousarray(host_prompt, np.int32)
+            assert len(host_prompt) == int(ins.sum())
+            hp = _p(host_prompt, ctypes.c_int)
+        toks = np.empty(int(outs.sum()), np.int32) if want_tokens else None
+        j, e, c, s = (ctypes.c_void_p() for _ in range(4))
+        check(lib().cronus_engine_serve(
+            self._h, cfg_text.encode(), len(ids), _p(ids, ctypes.c_int), _p(arr, ctypes.c_double),
+            _p(ins, ctypes.c_int), _p(outs, ctypes.c_int), trace.name.encode(), hp,
+            _p(toks, ctypes.c_int) if toks is not None else None, 1 if events else 0,
+            ctypes.byref(j), ctypes.byref(e), ctypes.byref(c), ctypes.byref(s)))
+        res = RunResult(take_string(j), take_string(e), take_string(c))
+        res.extra["stats"] = json.loads(take_string(s))
+        if toks is not None:
+            offs = np.concatenate([[0], np.cumsum(outs)])
+            res.extra["tokens"] = [toks[offs[i]:offs[i + 1]] for i in range(len(outs))]
+        return res

@@ -1,0 +1,356 @@
+"""Benchmark: Cronus partial-prefill serving of LLaMA3-8B shapes on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1] at N=1): LLaMA3-8B shapes (bf16, random init),
+one B200 with the partial-prefill worker (PPI, 40 SMs) and the chunked-prefill/decode
+worker (CPI, 108 SMs) co-located via green-context SM partitioning; synthetic trace of
+the paper's shape (lognormal lengths, mean 1014 input / 247 output tokens, seed 1),
+all requests at t = 0 (the paper's max-throughput protocol); scheduler on
+the wall clock with B200-calibrated cost profiles (tests/golden/configs/
+b200_llama8b_coloc.cfg, produced by paper_2509_17357_b200.calibrate).
+
+A step = serving the whole trace to completion. `value` = requests completed / step
+time with prompts already resident in HBM; `e2e` = the same through the C-ABI with host
+buffers (prompt tokens H2D and generated tokens D2H inside the timed region). N > 1
+GPUs form N/2 worker pairs (PPI GPU 2p, CPI GPU 2p+1, NVLink handoff); pair p serves
+the requests with id % pairs == p (static rule); weak scaling.
+
+--impl reference: the CPU path on this host (oracle port of the decoder on all cores,
+fitted with the reference's own fit_* and scheduled by the reference's own simulator,
+oracle/_ref) for the same trace and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG_DIR = os.path.join(ROOT, "tests", "golden", "configs")
+DEFAULT_CFG = os.path.join(CFG_DIR, "b200_llama8b_coloc.cfg")
+FALLBACK_CFG = os.path.join(CFG_DIR, "a100_a10_llama8b.cfg")
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--requests", type=int, default=256, help="requests per worker pair per step")
+    ap.add_argument("--warmup-requests", type=int, default=24)
+    ap.add_argument("--model", default="llama3-8b")
+    ap.add_argument("--config", default=None)
+    ap.add_argument("--ppi-sms", type=int, default=40)
+    ap.add_argument("--arrival", default="all-at-zero", choices=["all-at-zero", "fixed-interval"])
+    ap.add_argument("--interval-ms", type=float, default=0.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def load_cfg(path):
+    path = path or (DEFAULT_CFG if os.path.exists(DEFAULT_CFG) else FALLBACK_CFG)
+    return path, open(path).read()
+
+
+def make_trace(args, pairs):
+    from paper_2509_17357_b200 import engine as E
+    arrival = E.FIXED_INTERVAL if args.arrival == "fixed-interval" else E.ALL_AT_ZERO
+    return E.synth_trace(args.requests * pairs, 1014, 247, arrival, args.interval_ms, 1)
+
+
+def pair_trace(trace, pair, pairs):
+    return trace.subset(np.nonzero(trace.ids % pairs == pair)[0], name=f"{trace.name}[pair {pair}/{pairs}]")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self):
+        self.f.flush()
+        self.f.seek(0)
+        rows = [l.strip().split(", ") for l in self.f.read().splitlines() if l.strip()]
+        sm = [float(r[1]) for r in rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        for r in rows:
+            if len(r) > 8:
+                for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"),
+                                   r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(name)
+        mx = float(rows[0][2]) if rows and len(rows[0]) > 2 and rows[0][2].replace(".", "").isdigit() else None
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peaks():
+    try:
+        p = json.load(open(PEAKS))
+        return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def roofline(stats):
+    """Dominant kernel class of the profiled step -> roofline object (+ all classes)."""
+    hbm, tf_burst, tf_sus, src = peaks()
+    classes = []
+    for worker in ("cpi", "ppi"):
+        for name, k in stats[worker].items():
+            if name == "forward" or not k["launches"] or name == "other":
+                continue
+            bound = "hbm" if name in ("gemm_stream", "decode_attn") else "tensor"
+            ms_avg = k["ms"] / k["launches"]
+            if bound == "hbm":
+                ach = k["bytes"] / k["launches"] / (ms_avg / 1e3) / 1e9
+                peak, unit = hbm, "GB/s"
+            else:
+                ach = k["flops"] / k["launches"] / (ms_avg / 1e3) / 1e12
+                peak, unit = tf_sus, "TFLOP/s"
+            classes.append({"kernel": f"{worker}.{name}", "bound": bound, "achieved": round(ach, 1), "peak": peak,
+                            "unit": unit, "frac": round(ach / peak, 4), "launches": k["launches"],
+                            "share_ms": round(k["ms"], 2), "avg_us": round(1e3 * ms_avg, 2),
+                            "algorithmic_per_launch": (k["bytes"] if bound == "hbm" else k["flops"]) / k["launches"]})
+    classes.sort(key=lambda c: -c["share_ms"])
+    top = dict(classes[0]) if classes else {}
+    if top:
+        top["traffic"] = None
+        top["peak_source"] = f"MEASURED_PEAKS.json ({src}; {'sustained' if top['bound'] == 'tensor' else 'copy'})"
+    return top, classes
+
+
+def run_ours(args, rank, world):
+    import torch
+    from paper_2509_17357_b200.serving import GpuEngine
+
+    pairs = max(1, world // 2)
+    colocated = world == 1
+    cfg_path, cfg = load_cfg(args.config)
+    trace = make_trace(args, pairs)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    driver = colocated or rank % 2 == 0  # even ranks drive a pair; odd ranks host its CPI GPU
+    pair = rank // 2
+    dev = 0 if colocated else rank
+    torch.cuda.set_device(dev)
+    eng = None
+    if driver:
+        opts = dict(model=args.model, clock="wall")
+        if colocated:
+            opts["ppi_sms"] = args.ppi_sms
+        else:
+            opts.update(ppi_device=rank, cpi_device=rank + 1)
+        eng = GpuEngine(**opts)
+        sub = pair_trace(trace, pair, pairs)
+        warm = sub.subset(np.arange(min(args.warmup_requests, len(sub))), name="warmup")
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # ---- warm-up: W untimed serves (short trace: every kernel shape class, graphs of streams)
+    for _ in range(args.warmup):
+        if driver:
+            eng.serve(cfg, warm, events=False)
+    if driver:
+        eng.stage(cfg, sub)  # prompts resident in HBM before the timed region
+    # ---- timed: K serves of the full trace, device-timed, max over ranks
+    times, reports = [], []
+    clocks = None
+    for _ in range(args.steps):
+        barrier()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(dev) as cs:
+            s0.record()
+            res = eng.serve(cfg, sub, events=False) if driver else None
+            s1.record()
+            torch.cuda.synchronize()
+        clocks = cs.summary()
+        ms = s0.elapsed_time(s1)
+        if driver:
+            ms = max(ms, res.extra["stats"]["gpu_ms"])  # engine streams' own event span
+            reports.append(res)
+        times.append(ms)
+    local = np.array(times, dtype=np.float64)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor(local, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        local = t.cpu().numpy()
+    step_ms = float(np.mean(local))
+    n_done = 0
+    if driver:
+        n_done = json.loads(reports[-1].json)["completed"]
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([n_done], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t)
+        n_done = int(t.item())
+    value = n_done / (step_ms / 1e3)
+
+    # ---- e2e: host prompt buffers in, generated tokens out, through the C-ABI
+    e2e = None
+    if not args.no_e2e:
+        from oracle import numerics as NUM  # prompt synthesis restated on the host (input data only)
+        prompts = None
+        if driver:
+            vocab = NUM.PRESETS[args.model].vocab
+            prompts = np.concatenate([NUM.prompt_tokens(99, int(sub.ids[i]), int(sub.input_len[i]), vocab)
+                                      for i in range(len(sub))]).astype(np.int32)
+        barrier()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        r = eng.serve(cfg, sub, host_prompt=prompts, want_tokens=True, events=False) if driver else None
+        s1.record()
+        torch.cuda.synchronize()
+        ems = s0.elapsed_time(s1)
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([ems], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        h2d = r.extra["stats"]["h2d_bytes"] if driver else 0
+        d2h = r.extra["stats"]["d2h_bytes"] if driver else 0
+        e2e = {"value": round(n_done / (ems / 1e3), 4), "unit": "req/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h)}
+
+    # ---- profiled step (kernel classes timed with CUDA events on their streams)
+    roof, classes, prof_stats = {}, [], None
+    if not args.no_profile and driver:
+        pr = eng.serve(cfg, sub, events=False, profile=True)
+        prof_stats = pr.extra["stats"]
+        roof, classes = roofline(prof_stats)
+
+    if rank != 0:
+        return None
+    rep = json.loads(reports[-1].json)
+    st = reports[-1].extra["stats"]
+    line = {
+        "metric": "req/s (Cronus partial-prefill serving, paper-shape trace; TTFT/TBT P99 alongside)",
+        "value": round(value, 4), "unit": "req/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(step_ms, 2), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (lognormal trace of the paper's shape; random-init weights)",
+        "ttft_p99_ms": round(rep["ttft_p99_ms"], 3), "tbt_p99_ms": round(rep["tbt_p99_ms"], 3),
+        "ttft_mean_ms": round(rep["ttft_mean_ms"], 3), "tbt_mean_ms": round(rep["tbt_mean_ms"], 3),
+        "config": {"workload": ("LLaMA3-8B shapes, 1 B200, PPI+CPI co-located (green-context SM split)"
+                                if colocated else f"LLaMA3-8B shapes, {pairs} PPI/CPI pair(s) over NVLink"),
+                   "model": args.model, "requests_per_pair": len(sub), "pairs": pairs,
+                   "trace": f"synth(mean_in=1014, mean_out=247, seed=1, {args.arrival})",
+                   "cluster_config": os.path.relpath(cfg_path, ROOT), "clock": "wall (CUDA events)",
+                   "partition": st.get("partition"), "l2": "inputs > L2 (16 GB of weights streamed per iteration)",
+                   "parallelism": "replicas of worker pairs" if pairs > 1 else "co-located pair"},
+        "gpu_launches": int(st.get("gpu_launches", 0)),
+        "cpi_iterations": st["cpi_iterations"], "violations": len(rep["violations"]),
+        "clocks": clocks, "e2e": e2e, "roofline": roof, "kernels": classes[:8],
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(args, cfg, sub)
+    return line
+
+
+def cpu_baseline(args, cfg, sub):
+    from oracle import cpu_baseline as CB, refsim
+    t = refsim.Trace(sub.ids, sub.arrival_ms, sub.input_len, sub.output_len, sub.name)
+    r = CB.run(cfg, t, model=args.model, budget_s=args.cpu_budget_s)
+    return {"value": round(r["rps"], 6), "unit": "req/s", "cores": r["samples"]["threads"], "kind": "port",
+            "sample": ("1 of 32 decoder layers (numpy fp32, oracle restatement) timed on "
+                       f"{len(r['samples']['prefill'])} prefill lengths + {len(r['samples']['chunked'])} mixed "
+                       "batches, x32 + LM head; fitted with the reference's fit_prefill/fit_chunked and scheduled "
+                       f"by the reference simulator (oracle/_ref) on the same {len(sub)}-request trace"),
+            "ttft_p99_ms": round(r["ttft_p99_ms"], 1), "tbt_p99_ms": round(r["tbt_p99_ms"], 1),
+            "seconds": round(r["cpu_seconds"] + r["des_seconds"], 2)}
+
+
+def run_reference(args, rank, world):
+    """CPU path on the host: oracle port forward (all cores) + the reference's fit and simulator."""
+    if rank != 0:
+        return None
+    from oracle import cpu_baseline as CB, refsim
+    _, cfg = load_cfg(args.config)
+    from paper_2509_17357_b200 import engine as E  # trace synthesis only (identical draws to the reference)
+    pairs = max(1, world // 2)
+    trace = make_trace(args, pairs)
+    sub = pair_trace(trace, 0, pairs)
+    t = refsim.Trace(sub.ids, sub.arrival_ms, sub.input_len, sub.output_len, sub.name)
+    for _ in range(args.warmup):
+        CB.cpu_profile(args.model, budget_s=2.0)
+    vals, last = [], None
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        last = CB.run(cfg, t, model=args.model, budget_s=args.cpu_budget_s)
+        vals.append(last["rps"])
+    wall = (time.perf_counter() - t0) / max(1, args.steps)
+    v = float(np.mean(vals))
+    return {"metric": "req/s (Cronus partial-prefill serving, paper-shape trace; TTFT/TBT P99 alongside)",
+            "impl": "reference", "value": round(v, 6), "unit": "req/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(wall * 1e3, 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "ttft_p99_ms": round(last["ttft_p99_ms"], 1), "tbt_p99_ms": round(last["tbt_p99_ms"], 1),
+            "config": {"workload": "same trace and cluster config as the ours arm", "model": args.model,
+                       "requests": len(sub)},
+            "cpu_baseline": {"value": round(v, 6), "unit": "req/s", "cores": os.cpu_count(), "kind": "port",
+                             "sample": "see bench.py cpu_baseline (oracle forward + reference fit + reference DES)"},
+            "e2e": {"value": round(v, 6), "unit": "req/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    rank, world, _ = dist_env()
+    if world != args.gpus and world == 1 and args.gpus > 1:
+        print(json.dumps({"error": f"--gpus {args.gpus} must be launched with torchrun (one rank per GPU)"}))
+        return 2
+    if world > 1 and world % 2:
+        print(json.dumps({"error": "N > 1 GPUs must be even (PPI/CPI pairs)"}))
+        return 2
+    line = run_reference(args, rank, world) if args.impl == "reference" else run_ours(args, rank, world)
+    if line is not None:
+        print(json.dumps(line))
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -34,6 +34,7 @@ struct GpuRunOptions : RunOptions {
     const int32_t* host_prompt = nullptr;
     int32_t* host_tokens = nullptr;
     std::string* stats_json = nullptr;  // kernel / iteration statistics
+    bool profile = false;               // time kernel classes with CUDA events this run
 };
 
 class GpuEngine {
@@ -44,6 +45,20 @@ class GpuEngine {
     GpuEngine& operator=(const GpuEngine&) = delete;
 
     RunReport run(const ClusterConfig& cfg, const Trace& trace, const GpuRunOptions& opts = {});
+
+    // JSON: SM partition in effect ("green-context" | "grid-cap" | "none") and SM
+    // counts; with probe = true also the SMs each worker's kernels actually ran on.
+    std::string describe(bool probe = false);
+
+    // Synthesize this trace's prompt tokens on the device ahead of run() (the
+    // "inputs already resident in HBM" measurement); run() then skips that step.
+    void stage(const ClusterConfig& cfg, const Trace& trace);
+
+    // Calibration sample: median time (ms, CUDA events) of one forward pass on the
+    // PPI (worker 0) or CPI (worker 1) with n_dec decode rows of context dec_ctx and
+    // an optional prefill chunk [chunk_pos0, chunk_pos0 + chunk_len).
+    double time_pass(const ClusterConfig& cfg, int worker, int n_dec, int dec_ctx, int chunk_len, int chunk_pos0,
+                     int reps);
 
     struct Impl;
 

@@ -100,6 +100,10 @@ int ck_copy_token(const int* src, long long si, int* dst, long long di, int* dst
 
 int ck_device_sms(void);
 
+/* Diagnostic: n_ctas CTAs each add 1 to hits[%smid] (hits sized >= 256). Used to
+ * verify the SM partition of co-located workers. */
+int ck_smid_probe(int* hits, int n_ctas, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

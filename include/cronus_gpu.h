@@ -21,11 +21,24 @@ void cronus_engine_destroy(void* engine);
  * order (e2e mode: copied H2D inside the call); host_tokens (nullable): receives
  * the generated tokens (output_len per request, concatenated). Outputs are the
  * reference's report_to_json(rep, true), event log and csv_row, plus a stats JSON
- * (kernel timings when the engine was created with profile = 1). */
+ * (kernel timings when profiling). flags: bit0 = write the event log, bit1 = time
+ * kernel classes with CUDA events during this run. */
 int cronus_engine_serve(void* engine, const char* cfg_text, int n, const int* id, const double* arrival_ms,
                         const int* input_len, const int* output_len, const char* trace_name,
-                        const int* host_prompt, int* host_tokens, int want_events, char** json_out,
+                        const int* host_prompt, int* host_tokens, int flags, char** json_out,
                         char** events_out, char** csv_out, char** stats_out);
+
+/* Pre-synthesize the trace's prompt tokens on the device (see GpuEngine::stage). */
+int cronus_engine_stage(void* engine, const char* cfg_text, int n, const int* id, const double* arrival_ms,
+                        const int* input_len, const int* output_len);
+
+/* Calibration sample (see GpuEngine::time_pass): median ms of one forward pass. */
+int cronus_engine_time_pass(void* engine, const char* cfg_text, int worker, int n_dec, int dec_ctx, int chunk_len,
+                            int chunk_pos0, int reps, double* ms_out);
+
+/* JSON description of the engine's SM partition; probe = 1 launches an %smid probe
+ * on each worker stream and reports the SMs actually used. */
+int cronus_engine_describe(void* engine, int probe, char** json_out);
 
 #ifdef __cplusplus
 }

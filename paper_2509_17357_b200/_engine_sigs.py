@@ -16,3 +16,9 @@ def bind(L):
     L.cronus_engine_serve.argtypes = [V, ctypes.c_char_p, I, i32p, f64p, i32p, i32p, ctypes.c_char_p, i32p, i32p, I,
                                       vpp, vpp, vpp, vpp]
     L.cronus_engine_serve.restype = I
+    L.cronus_engine_describe.argtypes = [V, I, vpp]
+    L.cronus_engine_describe.restype = I
+    L.cronus_engine_stage.argtypes = [V, ctypes.c_char_p, I, i32p, f64p, i32p, i32p]
+    L.cronus_engine_stage.restype = I
+    L.cronus_engine_time_pass.argtypes = [V, ctypes.c_char_p, I, I, I, I, I, I, ctypes.POINTER(ctypes.c_double)]
+    L.cronus_engine_time_pass.restype = I

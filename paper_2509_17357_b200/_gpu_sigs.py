@@ -24,6 +24,7 @@ CK = {
     "ck_kv_copy": [V, V, V, V, I, LL, V],
     "ck_copy_token": [V, LL, V, LL, V, LL, V],
     "ck_device_sms": [],
+    "ck_smid_probe": [V, I, V],
 }
 
 

@@ -49,8 +49,9 @@ void cronus_engine_destroy(void* engine) { delete static_cast<cronus::GpuEngine*
 
 int cronus_engine_serve(void* engine, const char* cfg_text, int n, const int* id, const double* arrival_ms,
                         const int* input_len, const int* output_len, const char* trace_name, const int* host_prompt,
-                        int* host_tokens, int want_events, char** json_out, char** events_out, char** csv_out,
+                        int* host_tokens, int flags, char** json_out, char** events_out, char** csv_out,
                         char** stats_out) {
+    const int want_events = flags & 1;
     return guard([&] {
         auto* eng = static_cast<cronus::GpuEngine*>(engine);
         if (!eng) throw std::invalid_argument("null engine");
@@ -63,12 +64,35 @@ int cronus_engine_serve(void* engine, const char* cfg_text, int n, const int* id
         o.host_prompt = host_prompt;
         o.host_tokens = host_tokens;
         o.stats_json = &stats;
+        o.profile = (flags & 2) != 0;
         const cronus::RunReport rep = eng->run(cfg, t, o);
         if (json_out) *json_out = dup(cronus::report_to_json(rep, true));
         if (events_out) *events_out = dup(ev.str());
         if (csv_out) *csv_out = dup(cronus::csv_row(rep));
         if (stats_out) *stats_out = dup(stats);
     });
+}
+
+int cronus_engine_stage(void* engine, const char* cfg_text, int n, const int* id, const double* arrival_ms,
+                        const int* input_len, const int* output_len) {
+    return guard([&] {
+        const cronus::ClusterConfig cfg = cronus::parse_config(cfg_text);
+        const cronus::Trace t = cronus::capi::trace_from(n, id, arrival_ms, input_len, output_len, "");
+        static_cast<cronus::GpuEngine*>(engine)->stage(cfg, t);
+    });
+}
+
+int cronus_engine_time_pass(void* engine, const char* cfg_text, int worker, int n_dec, int dec_ctx, int chunk_len,
+                            int chunk_pos0, int reps, double* ms_out) {
+    return guard([&] {
+        const cronus::ClusterConfig cfg = cronus::parse_config(cfg_text);
+        *ms_out = static_cast<cronus::GpuEngine*>(engine)->time_pass(cfg, worker, n_dec, dec_ctx, chunk_len,
+                                                                      chunk_pos0, reps);
+    });
+}
+
+int cronus_engine_describe(void* engine, int probe, char** json_out) {
+    return guard([&] { *json_out = dup(static_cast<cronus::GpuEngine*>(engine)->describe(probe != 0)); });
 }
 
 }  // extern "C"

@@ -27,6 +27,7 @@
 #include "cronus/gpu.hpp"
 #include "cronus_ck.h"
 #include "model.hpp"
+#include "partition.hpp"
 
 namespace cronus {
 
@@ -121,6 +122,9 @@ struct GpuEngine::Impl {
     std::unique_ptr<gpu::KvPool> pool_ppi, pool_cpi;
     cudaStream_t s_ppi = nullptr, s_cpi = nullptr, s_copy = nullptr;
     std::unique_ptr<gpu::Worker> ppi, cpi;
+    std::unique_ptr<gpu::SmPartition> part;
+    std::string partition_mode = "none";
+    int ppi_ctas = 0, cpi_ctas = 0;  // persistent-grid caps per worker (0 = whole device)
     int cpi_rows = 0;
     TokenBufs tok_cpi, tok_ppi;
     // pinned staging for handoff block lists
@@ -131,6 +135,7 @@ struct GpuEngine::Impl {
     DeviceBuf xfer_dev;  // kRing slices
     long long xfer_cap = 0;  // ints per slice
     int sms = 148;
+    uint64_t staged_hash = 0;  // trace whose synthesized prompts are resident in tok_*.prompt
 
     explicit Impl(const std::string& text) : opt(parse_engine_options(text)), spec(gpu::ModelSpec::preset(opt.model)) {
         spec.seed = opt.seed;
@@ -145,11 +150,28 @@ struct GpuEngine::Impl {
         w_ppi = colocated ? w_cpi : std::make_shared<gpu::Weights>(spec, opt.ppi_device);
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        check_cuda(cudaSetDevice(opt.cpi_device), "cudaSetDevice");
-        check_cuda(cudaStreamCreateWithPriority(&s_cpi, cudaStreamNonBlocking, hi), "stream");
-        check_cuda(cudaStreamCreateWithPriority(&s_copy, cudaStreamNonBlocking, hi), "stream");
-        check_cuda(cudaSetDevice(opt.ppi_device), "cudaSetDevice");
-        check_cuda(cudaStreamCreateWithPriority(&s_ppi, cudaStreamNonBlocking, lo), "stream");
+        if (colocated && opt.ppi_sms > 0) {
+            check_cuda(cudaSetDevice(opt.cpi_device), "cudaSetDevice");
+            part = gpu::make_sm_partition(opt.cpi_device, opt.ppi_sms, lo, hi);
+            if (part) {
+                s_ppi = part->ppi_stream;
+                s_cpi = part->cpi_stream;
+                s_copy = part->copy_stream;
+                ppi_ctas = part->ppi_sms;
+                cpi_ctas = part->cpi_sms;
+                partition_mode = "green-context";
+            } else {
+                ppi_ctas = opt.ppi_sms;  // fallback: only the PPI's GEMM grid is capped
+                partition_mode = "grid-cap";
+            }
+        }
+        if (!part) {
+            check_cuda(cudaSetDevice(opt.cpi_device), "cudaSetDevice");
+            check_cuda(cudaStreamCreateWithPriority(&s_cpi, cudaStreamNonBlocking, hi), "stream");
+            check_cuda(cudaStreamCreateWithPriority(&s_copy, cudaStreamNonBlocking, hi), "stream");
+            check_cuda(cudaSetDevice(opt.ppi_device), "cudaSetDevice");
+            check_cuda(cudaStreamCreateWithPriority(&s_ppi, cudaStreamNonBlocking, lo), "stream");
+        }
         if (!colocated) {
             int can = 0;
             check_cuda(cudaDeviceCanAccessPeer(&can, opt.cpi_device, opt.ppi_device), "peer query");
@@ -171,9 +193,40 @@ struct GpuEngine::Impl {
         }
         ppi.reset();
         cpi.reset();
-        if (s_ppi) cudaStreamDestroy(s_ppi);
-        if (s_cpi) cudaStreamDestroy(s_cpi);
-        if (s_copy) cudaStreamDestroy(s_copy);
+        if (part) {
+            part.reset();  // owns the green-context streams
+        } else {
+            if (s_ppi) cudaStreamDestroy(s_ppi);
+            if (s_cpi) cudaStreamDestroy(s_cpi);
+            if (s_copy) cudaStreamDestroy(s_copy);
+        }
+    }
+
+    int cpi_sm_count() const { return cpi_ctas > 0 ? cpi_ctas : sms; }
+
+    std::string describe(bool probe) {
+        std::ostringstream o;
+        o << "{\"mode\": \"" << partition_mode << "\", \"device_sms\": " << sms << ", \"ppi_sms\": "
+          << (ppi_ctas ? ppi_ctas : sms) << ", \"cpi_sms\": " << cpi_sm_count();
+        if (probe) {
+            auto seen = [&](int dev, cudaStream_t st) {
+                check_cuda(cudaSetDevice(dev), "cudaSetDevice");
+                int* hits = nullptr;
+                check_cuda(cudaMalloc(&hits, 256 * 4), "alloc");
+                check_cuda(cudaMemsetAsync(hits, 0, 256 * 4, st), "memset");
+                check_ck(ck_smid_probe(hits, 4 * sms, st), "smid probe");
+                int h[256];
+                check_cuda(cudaMemcpyAsync(h, hits, sizeof h, cudaMemcpyDeviceToHost, st), "D2H");
+                check_cuda(cudaStreamSynchronize(st), "sync");
+                cudaFree(hits);
+                int n = 0;
+                for (int v : h) n += v > 0;
+                return n;
+            };
+            o << ", \"ppi_seen\": " << seen(opt.ppi_device, s_ppi) << ", \"cpi_seen\": " << seen(opt.cpi_device, s_cpi);
+        }
+        o << "}";
+        return o.str();
     }
 
     // Size pools / workers for this config (reallocating only when they grow).
@@ -197,14 +250,13 @@ struct GpuEngine::Impl {
         if (!cpi || cpi_rows < B) {
             cpi.reset();
             check_cuda(cudaSetDevice(opt.cpi_device), "cudaSetDevice");
-            cpi = std::make_unique<gpu::Worker>(*w_cpi, B, B, static_cast<int>(pool_cpi->blocks) + B, s_cpi, 0);
+            cpi = std::make_unique<gpu::Worker>(*w_cpi, B, B, static_cast<int>(pool_cpi->blocks) + B, s_cpi, cpi_ctas);
             cpi_rows = B;
         }
         if (!ppi) {
             check_cuda(cudaSetDevice(opt.ppi_device), "cudaSetDevice");
-            const int cap = colocated && opt.ppi_sms > 0 ? opt.ppi_sms : 0;
             ppi = std::make_unique<gpu::Worker>(*w_ppi, opt.ppi_chunk, 1,
-                                                static_cast<int>(pool_ppi->blocks) + opt.ppi_chunk, s_ppi, cap);
+                                                static_cast<int>(pool_ppi->blocks) + opt.ppi_chunk, s_ppi, ppi_ctas);
         }
         const long long need = 2 * std::max(pool_ppi->blocks, pool_cpi->blocks) + 64;
         if (xfer_cap < need) {
@@ -215,8 +267,6 @@ struct GpuEngine::Impl {
             xfer_dev.ensure(opt.cpi_device, static_cast<size_t>(need) * 4 * kRing);
             xfer_cap = need;
         }
-        cpi->set_profiling(opt.profile);
-        ppi->set_profiling(opt.profile);
     }
 };
 
@@ -276,13 +326,14 @@ class PairExecutor : public sched::Executor {
                                            cudaMemcpyHostToDevice, s),
                            "prompt H2D");
                 h2d_bytes += total_in * 4;
-            } else {
-                synth_prompts(tb, s);
+            } else if (E.staged_hash != trace_hash(trace) || E.staged_hash == 0) {
+                synth_prompts(tb, s);  // not staged beforehand: synthesize on the device now
             }
             h2d_bytes += n * 8;
         };
         setup(E.tok_cpi, E.opt.cpi_device, E.s_cpi);
         if (!E.colocated) setup(E.tok_ppi, E.opt.ppi_device, E.s_ppi);
+        E.staged_hash = opts.host_prompt ? 0 : trace_hash(trace);
         check_cuda(cudaSetDevice(E.opt.cpi_device), "cudaSetDevice");
         check_cuda(cudaStreamSynchronize(E.s_cpi), "sync");
         check_cuda(cudaSetDevice(E.opt.ppi_device), "cudaSetDevice");
@@ -353,6 +404,7 @@ class PairExecutor : public sched::Executor {
         check_cuda(cudaEventRecord(E.xfer_ev[slot], E.s_copy), "event");
         check_ck(ck_kv_copy(E.pool_ppi->base, d, E.pool_cpi->base, d + nb, nb, E.pool_cpi->block_bytes, E.s_copy),
                  "kv_copy");
+        ++copy_launches;
         const Request& r = trace.requests[w.rid];
         if (!E.colocated && w.tokens == r.input_len) {
             // the PPI sampled the first token: it travels with the KV
@@ -360,6 +412,7 @@ class PairExecutor : public sched::Executor {
                                    static_cast<int*>(E.tok_cpi.last_tok.p), w.rid,
                                    static_cast<int*>(E.tok_cpi.out_tok.p), out_off[w.rid], E.s_copy),
                      "copy_token");
+            ++copy_launches;
         }
         xfer_ev[w.rid] = record(E.s_copy, xfer_ev[w.rid]);
         xfer_pending[w.rid] = 1;
@@ -388,7 +441,7 @@ class PairExecutor : public sched::Executor {
                               out_off[w.chunk_rid]);
         }
         for (int rid : w.finishers) need(rid);
-        if (!batch.d_len.empty()) batch.plan_decode_splits(E.spec.n_kv_heads, 3 * E.sms);
+        if (!batch.d_len.empty()) batch.plan_decode_splits(E.spec.n_kv_heads, 3 * E.cpi_sm_count());
         E.cpi->forward(batch, *E.pool_cpi, static_cast<int*>(E.tok_cpi.prompt.p),
                        static_cast<long long*>(E.tok_cpi.prompt_off.p), static_cast<int*>(E.tok_cpi.last_tok.p),
                        static_cast<int*>(E.tok_cpi.out_tok.p));
@@ -414,6 +467,8 @@ class PairExecutor : public sched::Executor {
     bool wall_clock() const override { return E.opt.wall; }
 
     void start() override {
+        launches0_cpi = E.cpi->launches;
+        launches0_ppi = E.ppi->launches;
         check_cuda(cudaSetDevice(E.opt.cpi_device), "cudaSetDevice");
         check_cuda(cudaEventCreate(&t0_cpi), "event");
         check_cuda(cudaEventRecord(t0_cpi, E.s_cpi), "event");
@@ -505,16 +560,19 @@ class PairExecutor : public sched::Executor {
           << ", \"chunk_rows\": " << chunk_rows << ", \"prefill_tokens\": " << prefill_tokens
           << ", \"handoffs\": " << handoffs << ", \"handoff_bytes\": " << handoff_bytes
           << ", \"h2d_bytes\": " << h2d_bytes << ", \"d2h_bytes\": " << d2h_bytes
-          << ", \"kernel_launches_per_forward_layer\": 9"
-          << ", \"colocated\": " << (E.colocated ? "true" : "false") << ", \"sms\": " << E.sms << ", \"cpi\": {";
+          << ", \"gpu_launches\": " << (E.cpi->launches - launches0_cpi) + (E.ppi->launches - launches0_ppi) + copy_launches
+          << ", \"colocated\": " << (E.colocated ? "true" : "false") << ", \"sms\": " << E.sms
+          << ", \"partition\": " << E.describe(false) << ", \"cpi\": {";
         ks("decode_attn", E.cpi->stat_decode_attn);
         ks("prefill_attn", E.cpi->stat_prefill_attn);
-        ks("gemm", E.cpi->stat_gemm);
+        ks("gemm_stream", E.cpi->stat_gemm_stream);
+        ks("gemm_tc", E.cpi->stat_gemm_tc);
         ks("other", E.cpi->stat_other);
         ks("forward", E.cpi->stat_forward, false);
         s << "}, \"ppi\": {";
         ks("prefill_attn", E.ppi->stat_prefill_attn);
-        ks("gemm", E.ppi->stat_gemm);
+        ks("gemm_stream", E.ppi->stat_gemm_stream);
+        ks("gemm_tc", E.ppi->stat_gemm_tc);
         ks("other", E.ppi->stat_other);
         ks("forward", E.ppi->stat_forward, false);
         s << "}}";
@@ -545,6 +603,7 @@ class PairExecutor : public sched::Executor {
     std::chrono::steady_clock::time_point host_t0;
 
   public:
+    long long launches0_cpi = 0, launches0_ppi = 0, copy_launches = 0;
     double gpu_ms = 0;
     long long iters = 0, iter_rows = 0, decode_rows = 0, decode_keys = 0, chunk_rows = 0, prefill_tokens = 0;
     long long handoffs = 0;
@@ -578,6 +637,78 @@ class PairExecutor : public sched::Executor {
 GpuEngine::GpuEngine(const std::string& engine_options) : impl_(std::make_unique<Impl>(engine_options)) {}
 GpuEngine::~GpuEngine() = default;
 
+std::string GpuEngine::describe(bool probe) { return impl_->describe(probe); }
+
+// Calibration sample: one synthetic forward pass on a worker,
+// timed with CUDA events on that worker's stream; median of `reps`.
+double GpuEngine::time_pass(const ClusterConfig& cfg, int worker, int n_dec, int dec_ctx, int chunk_len,
+                            int chunk_pos0, int reps) {
+    Impl& E = *impl_;
+    E.prepare(cfg);
+    gpu::Worker& W = worker == 0 ? *E.ppi : *E.cpi;
+    gpu::KvPool& pool = worker == 0 ? *E.pool_ppi : *E.pool_cpi;
+    const int dev = worker == 0 ? E.opt.ppi_device : E.opt.cpi_device;
+    TokenBufs& tb = worker == 0 && !E.colocated ? E.tok_ppi : E.tok_cpi;
+    check_cuda(cudaSetDevice(dev), "cudaSetDevice");
+    const long long span = std::max<long long>(chunk_pos0 + chunk_len, dec_ctx) + 16;
+    const int n_req = n_dec + 1;
+    tb.prompt.ensure(dev, static_cast<size_t>(span) * 4);
+    tb.prompt_off.ensure(dev, static_cast<size_t>(n_req) * 8);
+    tb.last_tok.ensure(dev, static_cast<size_t>(n_req) * 4);
+    tb.out_tok.ensure(dev, static_cast<size_t>(n_req) * 4 + static_cast<size_t>(span) * 4);
+    cudaStream_t st = W.stream();
+    check_cuda(cudaMemsetAsync(tb.prompt.p, 0, static_cast<size_t>(span) * 4, st), "memset");
+    check_cuda(cudaMemsetAsync(tb.prompt_off.p, 0, static_cast<size_t>(n_req) * 8, st), "memset");
+    check_cuda(cudaMemsetAsync(tb.last_tok.p, 0, static_cast<size_t>(n_req) * 4, st), "memset");
+    E.staged_hash = 0;
+    // disjoint block ranges per sequence
+    long long next = 0;
+    auto blocks_for = [&](long long tokens) {
+        std::vector<int32_t> b;
+        for (long long i = 0; i < (tokens + 15) / 16; ++i) b.push_back(static_cast<int32_t>(next++ % pool.blocks));
+        return b;
+    };
+    gpu::Batch batch;
+    std::vector<std::vector<int32_t>> tables;
+    tables.reserve(n_dec + 1);
+    for (int i = 0; i < n_dec; ++i) {
+        tables.push_back(blocks_for(dec_ctx));
+        batch.add_decode(i + 1, dec_ctx, tables.back(), i + 1);
+    }
+    if (chunk_len > 0) {
+        tables.push_back(blocks_for(chunk_pos0 + chunk_len));
+        batch.add_prefill(0, chunk_pos0, chunk_len, tables.back(), true, 0);
+    }
+    if (n_dec > 0) batch.plan_decode_splits(E.spec.n_kv_heads, 3 * (worker == 0 ? (E.ppi_ctas ? E.ppi_ctas : E.sms)
+                                                                             : E.cpi_sm_count()));
+    cudaEvent_t a, b;
+    check_cuda(cudaEventCreate(&a), "event");
+    check_cuda(cudaEventCreate(&b), "event");
+    std::vector<float> t;
+    for (int r = 0; r < reps + 1; ++r) {
+        check_cuda(cudaEventRecord(a, st), "event");
+        W.forward(batch, pool, static_cast<int*>(tb.prompt.p), static_cast<long long*>(tb.prompt_off.p),
+                  static_cast<int*>(tb.last_tok.p), static_cast<int*>(tb.out_tok.p));
+        check_cuda(cudaEventRecord(b, st), "event");
+        check_cuda(cudaEventSynchronize(b), "sync");
+        float ms = 0.f;
+        check_cuda(cudaEventElapsedTime(&ms, a, b), "elapsed");
+        if (r > 0) t.push_back(ms);  // first pass warms caches / descriptors
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    std::sort(t.begin(), t.end());
+    return t[t.size() / 2];
+}
+
+void GpuEngine::stage(const ClusterConfig& cfg, const Trace& trace) {
+    impl_->prepare(cfg);
+    GpuRunOptions o;
+    impl_->staged_hash = 0;
+    PairExecutor ex(*impl_, trace, o);
+    ex.upload();  // synthesizes the prompts on the device and marks them staged
+}
+
 RunReport GpuEngine::run(const ClusterConfig& cfg, const Trace& trace, const GpuRunOptions& opts) {
     if (cfg.policy != Policy::Cronus)
         throw std::invalid_argument("B200 engine: only the cronus policy runs on the GPU workers (baselines: "
@@ -585,6 +716,10 @@ RunReport GpuEngine::run(const ClusterConfig& cfg, const Trace& trace, const Gpu
     const auto errs = validate_config(cfg);
     if (!errs.empty() || trace.requests.empty()) return cronus::run(cfg, trace, opts);  // throws the same errors
     impl_->prepare(cfg);
+    impl_->cpi->set_profiling(opts.profile || impl_->opt.profile);
+    impl_->ppi->set_profiling(opts.profile || impl_->opt.profile);
+    impl_->cpi->reset_stats();
+    impl_->ppi->reset_stats();
     PairExecutor ex(*impl_, trace, opts);
     ex.upload();
     sched::SchedulerHooks hooks;

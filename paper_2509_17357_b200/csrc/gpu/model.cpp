@@ -294,8 +294,10 @@ void Worker::gemm(const void* W, const void* X, void* out, const void* bias, int
     cudaEvent_t a = nullptr;
     mark(a);
     check_ck(ck_gemm(W, X, out, bias, M, N, K, N, epi, splits, max_ctas_, stream_), "gemm");
-    done(a, &stat_gemm, 2.0 * (static_cast<double>(N) * K + static_cast<double>(M) * K) +
-                            (epi == CK_EPI_BF16 ? 2.0 : 4.0) * M * N,
+    ++launches;
+    // algorithmic bytes: weights + activations in + output (red.add counted once)
+    done(a, M <= 128 ? &stat_gemm_stream : &stat_gemm_tc,
+         2.0 * (static_cast<double>(N) * K + static_cast<double>(M) * K) + (epi == CK_EPI_BF16 ? 2.0 : 4.0) * M * N,
          2.0 * M * N * K);
 }
 
@@ -363,11 +365,13 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
     cudaEvent_t a = nullptr;
     mark(a);
     check_ck(ck_embed(x_, w_.embed, row_rid, row_pos, row_dec, prompt, prompt_off, last_tok, M, H, stream_), "embed");
+    ++launches;
     done(a, &stat_other, 0, 0);
     for (int l = 0; l < m.layers; ++l) {
         const LayerWeights& L = w_.layer[l];
         mark(a);
         check_ck(ck_rmsnorm(x_, L.attn_norm, h_, nullptr, M, H, m.rms_eps, stream_), "rmsnorm");
+        ++launches;
         done(a, &stat_other, 0, 0);
         if (small) {
             check_cuda(cudaMemsetAsync(qkv_, 0, static_cast<size_t>(M) * Q * 4, stream_), "memset qkv");
@@ -379,6 +383,7 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         check_ck(ck_qkv_rope_append(qkv_, nullptr, q_, pool.base, bt, row_bt, row_pos, w_.cos_tab, w_.sin_tab, M,
                                     m.n_heads, m.n_kv_heads, l, m.layers, stream_),
                  "qkv_rope_append");
+        ++launches;
         done(a, &stat_other, 0, 0);
         if (n_dec > 0) {
             mark(a);
@@ -386,6 +391,7 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
                                     n_work, n_dec, b.blocks_per_split, attn_ws_, attn_, m.n_heads, m.n_kv_heads, l,
                                     m.layers, scale, stream_),
                      "attn_decode");
+            launches += 2;  // split-KV pass + combine
             done(a, &stat_decode_attn, dec_keys * kv_tok_layer, 4.0 * m.n_heads * m.head_dim * dec_keys);
         }
         if (b.p_len > 0) {
@@ -393,12 +399,14 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
             check_ck(ck_attn_prefill(q_, pool.base, bt + b.p_bt, b.p_row0, b.p_len, b.p_pos0, attn_, m.n_heads,
                                      m.n_kv_heads, l, m.layers, scale, stream_),
                      "attn_prefill");
+            ++launches;
             const double keys = static_cast<double>(b.p_len) * b.p_pos0 + 0.5 * b.p_len * (b.p_len + 1.0);
             done(a, &stat_prefill_attn, (b.p_pos0 + b.p_len) * kv_tok_layer, 4.0 * m.n_heads * m.head_dim * keys);
         }
         gemm(L.wo, attn_, x_, nullptr, M, H, NQ, CK_EPI_RED_F32, 0);
         mark(a);
         check_ck(ck_rmsnorm(x_, L.ffn_norm, h_, nullptr, M, H, m.rms_eps, stream_), "rmsnorm");
+        ++launches;
         done(a, &stat_other, 0, 0);
         if (small) {
             check_cuda(cudaMemsetAsync(gu_, 0, static_cast<size_t>(M) * 2 * F * 4, stream_), "memset gu");
@@ -408,18 +416,21 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         }
         mark(a);
         check_ck(ck_silu_mul(gu_, act_, M, F, stream_), "silu_mul");
+        ++launches;
         done(a, &stat_other, 0, 0);
         gemm(L.wd, act_, x_, nullptr, M, H, F, CK_EPI_RED_F32, 0);
     }
     if (R > 0) {
         mark(a);
         check_ck(ck_rmsnorm(x_, w_.final_norm, hs_, D(o_s_row), R, H, m.rms_eps, stream_), "final norm");
+        ++launches;
         done(a, &stat_other, 0, 0);
         gemm(w_.lm_head, hs_, logits_, nullptr, R, m.vocab, H, CK_EPI_F32, 1);
         mark(a);
         check_ck(ck_argmax_emit(logits_, R, m.vocab, D(o_s_rid), reinterpret_cast<const long long*>(D(o_s_out)),
                                 last_tok, out_tok, stream_),
                  "argmax");
+        ++launches;
         done(a, &stat_other, 0, 0);
     }
     done(pass0, &stat_forward, 0, 0);

@@ -145,7 +145,12 @@ class Worker {
     cudaStream_t stream() const { return stream_; }
     void set_profiling(bool on) { profile_ = on; }
     void collect_stats();  // fold finished profiling events into stats (synchronizes)
-    KernelStat stat_decode_attn, stat_prefill_attn, stat_gemm, stat_other, stat_forward;
+    void reset_stats() {
+        stat_decode_attn = stat_prefill_attn = stat_gemm_stream = stat_gemm_tc = stat_other = stat_forward = {};
+    }
+    // gemm_stream: M <= 128 (weight-streaming, HBM bound); gemm_tc: M > 128 (tensor bound)
+    KernelStat stat_decode_attn, stat_prefill_attn, stat_gemm_stream, stat_gemm_tc, stat_other, stat_forward;
+    long long launches = 0;  // our kernels launched (always counted)
 
   private:
     const Weights& w_;

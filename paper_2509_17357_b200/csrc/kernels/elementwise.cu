@@ -233,6 +233,16 @@ __global__ void kv_copy_kernel(const uint4* __restrict__ src, const int* __restr
     for (; i < n; i += blockDim.x) dst[d0 + i] = src[s0 + i];
 }
 
+__global__ void smid_probe_kernel(int* hits) {
+    uint32_t sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    if (threadIdx.x == 0) atomicAdd(&hits[sm], 1);
+    // keep the CTA resident briefly so the scheduler spreads the grid
+    const long long t0 = clock64();
+    while (clock64() - t0 < 20000) {
+    }
+}
+
 __global__ void copy_token_kernel(const int* src, long long si, int* dst, long long di, int* dst2, long long di2) {
     const int v = src[si];
     dst[di] = v;
@@ -327,6 +337,11 @@ int ck_kv_copy(const void* src_pool, const int* src_ids, void* dst_pool, const i
     const dim3 grid(n_blocks, static_cast<unsigned>((block_vec + chunk_vec - 1) / chunk_vec));
     kv_copy_kernel<<<grid, 256, 0, S(stream)>>>(static_cast<const uint4*>(src_pool), src_ids,
                                                 static_cast<uint4*>(dst_pool), dst_ids, block_vec, chunk_vec);
+    return ret();
+}
+
+int ck_smid_probe(int* hits, int n_ctas, void* stream) {
+    smid_probe_kernel<<<n_ctas, 64, 0, S(stream)>>>(hits);
     return ret();
 }
 

@@ -40,7 +40,26 @@ class GpuEngine:
         except Exception:
             pass
 
-    def serve(self, cfg_text: str, trace: Trace, host_prompt=None, want_tokens=False, events=True) -> RunResult:
+    def stage(self, cfg_text: str, trace: Trace):
+        """Synthesize the trace's prompts on the device before a timed serve()."""
+        ids, arr, ins, outs = trace.arrays()
+        check(lib().cronus_engine_stage(self._h, cfg_text.encode(), len(ids), _p(ids, ctypes.c_int),
+                                        _p(arr, ctypes.c_double), _p(ins, ctypes.c_int), _p(outs, ctypes.c_int)))
+
+    def time_pass(self, cfg_text: str, worker: int, n_dec=0, dec_ctx=0, chunk_len=0, chunk_pos0=0, reps=5) -> float:
+        """Median ms of one forward pass on the PPI (0) or CPI (1) worker (calibration)."""
+        ms = ctypes.c_double()
+        check(lib().cronus_engine_time_pass(self._h, cfg_text.encode(), worker, n_dec, dec_ctx, chunk_len, chunk_pos0,
+                                            reps, ctypes.byref(ms)))
+        return ms.value
+
+    def describe(self, probe=False) -> dict:
+        out = ctypes.c_void_p()
+        check(lib().cronus_engine_describe(self._h, 1 if probe else 0, ctypes.byref(out)))
+        return json.loads(take_string(out))
+
+    def serve(self, cfg_text: str, trace: Trace, host_prompt=None, want_tokens=False, events=True,
+              profile=False) -> RunResult:
         ids, arr, ins, outs = trace.arrays()
         hp = None
         if host_prompt is not None:
@@ -52,7 +71,7 @@ class GpuEngine:
         check(lib().cronus_engine_serve(
             self._h, cfg_text.encode(), len(ids), _p(ids, ctypes.c_int), _p(arr, ctypes.c_double),
             _p(ins, ctypes.c_int), _p(outs, ctypes.c_int), trace.name.encode(), hp,
-            _p(toks, ctypes.c_int) if toks is not None else None, 1 if events else 0,
+            _p(toks, ctypes.c_int) if toks is not None else None, (1 if events else 0) | (2 if profile else 0),
             ctypes.byref(j), ctypes.byref(e), ctypes.byref(c), ctypes.byref(s)))
         res = RunResult(take_string(j), take_string(e), take_string(c))
         res.extra["stats"] = json.loads(take_string(s))

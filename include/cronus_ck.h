@@ -56,9 +56,11 @@ int ck_rope_table(float* cos_tab, float* sin_tab, int max_pos, double theta, voi
 int ck_embed(float* x, const void* emb_bf16, const int* row_rid, const int* row_pos, const int* row_dec,
              const int* prompt, const long long* prompt_off, const int* last_tok, int M, int H, void* stream);
 
-/* out_bf16[r] = rmsnorm(x[rows ? rows[r] : r]) * gamma, r < R. */
+/* out_bf16[r] = rmsnorm(x[rows ? rows[r] : r]) * gamma, r < R. If `zero` is not
+ * null, row r of zero[R, zero_cols] (fp32) is also cleared — the accumulation buffer
+ * of the next red.add GEMM, so no separate memset launch is needed. */
 int ck_rmsnorm(const float* x, const void* gamma, void* out_bf16, const int* rows, int R, int H, float eps,
-               void* stream);
+               float* zero, int zero_cols, void* stream);
 
 /* qkv fp32 [M, (nq + 2 nkv) * 128] (+ bias) -> RoPE(q) bf16 [M, nq*128] and
  * RoPE(k), v appended to the paged pool at each row's position.
@@ -71,11 +73,12 @@ int ck_qkv_rope_append(const float* qkv, const void* bias, void* q_out, void* kv
  * seq_row[S] (row of q/out), seq_len[S] (keys), seq_bt[S] (offset into bt),
  * seq_item0[S+1] (first work item of each sequence). work[n_work] = seq << 16 | split;
  * a work item covers up to `blocks_per_split` 16-token blocks. ws: fp32 partials,
- * n_work * nq * 130 floats. Output bf16 rows [*, nq*128]. */
+ * n_work * nq * 130 floats. tickets: n_seq * nkv ints, zero before the first call
+ * (the kernel leaves them zero). Output bf16 rows [*, nq*128]. One launch. */
 int ck_attn_decode(const void* q, const void* kv_pool, const int* bt, const int* seq_row, const int* seq_len,
                    const int* seq_bt, const int* seq_item0, const int* work, int n_work, int n_seq,
-                   int blocks_per_split, float* ws, void* out, int nq, int nkv, int layer, int n_layers,
-                   float scale, void* stream);
+                   int blocks_per_split, float* ws, int* tickets, void* out, int nq, int nkv, int layer,
+                   int n_layers, float scale, void* stream);
 
 /* Prefill/chunk attention, causal: query rows [q_row0, q_row0+q_len) sit at
  * positions [pos0, pos0+q_len); keys [0, pos0+q_len) from the paged pool via bt. */
@@ -86,9 +89,10 @@ int ck_attn_prefill(const void* q, const void* kv_pool, const int* bt, int q_row
 int ck_silu_mul(const float* gu, void* act_bf16, int M, int F, void* stream);
 
 /* Greedy sampling: token = argmax_v logits[r, v] (lowest index on ties), then
- * last_tok[rid[r]] = token, out_tok[out_idx[r]] = token. */
+ * last_tok[rid[r]] = token, out_tok[out_idx[r]] = token. ws: 64 * R floats of
+ * scratch; tickets: R ints, zero before the first call (left zero). One launch. */
 int ck_argmax_emit(const float* logits, int R, int V, const int* rid, const long long* out_idx, int* last_tok,
-                   int* out_tok, void* stream);
+                   int* out_tok, float* ws, int* tickets, void* stream);
 
 /* KV handoff: copy n_blocks blocks src_pool[src_ids[i]] -> dst_pool[dst_ids[i]]
  * (block_bytes each; src may be a peer-mapped pointer — pull over NVLink). */
@@ -103,6 +107,11 @@ int ck_device_sms(void);
 /* Diagnostic: n_ctas CTAs each add 1 to hits[%smid] (hits sized >= 256). Used to
  * verify the SM partition of co-located workers. */
 int ck_smid_probe(int* hits, int n_ctas, void* stream);
+
+/* Diagnostic: stream `bytes` of `buf` with `ctas` CTAs; mode 0 = LDG.128, 1 = TMA
+ * 128x64 bf16 boxes over a [rows][4096] matrix (the GEMM's weight pattern), 2 =
+ * cp.async.bulk 16 KiB chunks. Time it with events on `stream`. */
+int ck_bw_probe(const void* buf, long long bytes, int mode, int ctas, void* stream);
 
 #ifdef __cplusplus
 }

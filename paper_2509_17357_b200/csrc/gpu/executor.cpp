@@ -441,7 +441,7 @@ class PairExecutor : public sched::Executor {
                               out_off[w.chunk_rid]);
         }
         for (int rid : w.finishers) need(rid);
-        if (!batch.d_len.empty()) batch.plan_decode_splits(E.spec.n_kv_heads, 3 * E.cpi_sm_count());
+        if (!batch.d_len.empty()) batch.plan_decode_splits(E.spec.n_kv_heads, 2 * E.cpi_sm_count());
         E.cpi->forward(batch, *E.pool_cpi, static_cast<int*>(E.tok_cpi.prompt.p),
                        static_cast<long long*>(E.tok_cpi.prompt_off.p), static_cast<int*>(E.tok_cpi.last_tok.p),
                        static_cast<int*>(E.tok_cpi.out_tok.p));
@@ -679,7 +679,7 @@ double GpuEngine::time_pass(const ClusterConfig& cfg, int worker, int n_dec, int
         tables.push_back(blocks_for(chunk_pos0 + chunk_len));
         batch.add_prefill(0, chunk_pos0, chunk_len, tables.back(), true, 0);
     }
-    if (n_dec > 0) batch.plan_decode_splits(E.spec.n_kv_heads, 3 * (worker == 0 ? (E.ppi_ctas ? E.ppi_ctas : E.sms)
+    if (n_dec > 0) batch.plan_decode_splits(E.spec.n_kv_heads, 2 * (worker == 0 ? (E.ppi_ctas ? E.ppi_ctas : E.sms)
                                                                              : E.cpi_sm_count()));
     cudaEvent_t a, b;
     check_cuda(cudaEventCreate(&a), "event");

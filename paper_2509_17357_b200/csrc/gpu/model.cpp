@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -186,13 +187,19 @@ void Batch::add_prefill(int rid, long long pos0, long long len, const std::vecto
 }
 
 // Pick the split size so the decode grid holds ~target_ctas CTAs.
-void Batch::plan_decode_splits(int n_kv_heads, int target_ctas) {
+void Batch::plan_decode_splits(int n_kv_heads, int slots) {
+    // Split size = total block-heads / (waves x resident CTAs), waves = 1.5 by default
+    // (CRONUS_DECODE_WAVES): long enough splits keep each warp's cp.async ring
+    // streaming, enough of them to balance across the resident CTAs.
+    static const double waves = [] {
+        const char* e = std::getenv("CRONUS_DECODE_WAVES");
+        return e ? std::atof(e) : 1.5;
+    }();
     long long total = 0;
     for (int len : d_len) total += (len + 15) / 16;
-    int bps = static_cast<int>((total * n_kv_heads + target_ctas - 1) / std::max(1, target_ctas));
-    bps = std::clamp(bps, 4, 256);
-    // keep the work list bounded (workspace sizing)
-    while (true) {
+    int bps = static_cast<int>(std::ceil(total * n_kv_heads / std::max(1.0, waves * slots)));
+    bps = std::clamp(bps, 16, 1024);
+    while (true) {  // keep the work list bounded (workspace sizing)
         long long items = 0;
         for (int len : d_len) items += ((len + 15) / 16 + bps - 1) / bps;
         if (items <= 4096) break;
@@ -228,6 +235,11 @@ Worker::Worker(const Weights& w, int max_rows, int max_sample, int max_blocks_pe
     check_cuda(cudaMalloc(&logits_, static_cast<size_t>(max_sample) * m_.vocab * 4), "alloc logits");
     attn_ws_floats_ = 4096LL * m_.n_heads * (m_.head_dim + 2);
     check_cuda(cudaMalloc(&attn_ws_, attn_ws_floats_ * 4), "alloc attn ws");
+    check_cuda(cudaMalloc(&attn_tickets_, R * m_.n_kv_heads * 4), "alloc attn tickets");
+    check_cuda(cudaMemset(attn_tickets_, 0, R * m_.n_kv_heads * 4), "zero attn tickets");
+    check_cuda(cudaMalloc(&arg_ws_, static_cast<size_t>(max_sample) * 64 * 4), "alloc argmax ws");
+    check_cuda(cudaMalloc(&arg_tickets_, static_cast<size_t>(max_sample) * 4), "alloc argmax tickets");
+    check_cuda(cudaMemset(arg_tickets_, 0, static_cast<size_t>(max_sample) * 4), "zero argmax tickets");
     meta_cap_ = 12LL * max_rows + max_bt_ + 2 * 4096 + 64;
     check_cuda(cudaMalloc(&meta_dev_, meta_cap_ * 4), "alloc meta");
     for (int i = 0; i < kRing; ++i) {
@@ -239,7 +251,8 @@ Worker::Worker(const Weights& w, int max_rows, int max_sample, int max_blocks_pe
 Worker::~Worker() {
     cudaSetDevice(w_.device());
     for (void* p : {static_cast<void*>(x_), h_, static_cast<void*>(qkv_), q_, attn_, static_cast<void*>(gu_), act_, hs_,
-                    static_cast<void*>(logits_), static_cast<void*>(attn_ws_), static_cast<void*>(meta_dev_)})
+                    static_cast<void*>(logits_), static_cast<void*>(attn_ws_), static_cast<void*>(meta_dev_),
+                    static_cast<void*>(attn_tickets_), static_cast<void*>(arg_ws_), static_cast<void*>(arg_tickets_)})
         if (p) cudaFree(p);
     for (int i = 0; i < kRing; ++i) {
         if (meta_host_[i]) cudaFreeHost(meta_host_[i]);
@@ -356,8 +369,8 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         throw std::logic_error("forward: decode work list too long");
 
     const int H = m.hidden, Q = m.qkv_n(), NQ = m.q_n(), F = m.ffn;
+    const bool small = M <= 128;  // weight-streaming regime
     const float scale = 1.0f / std::sqrt(static_cast<float>(m.head_dim));
-    const bool small = M <= 128;  // weight-streaming regime: split-K + red.add into zeroed fp32
     long long dec_keys = 0;
     for (int len : b.d_len) dec_keys += len;
     const double kv_tok_layer = 2.0 * m.n_kv_heads * m.head_dim * 2;  // bytes per token per layer (K+V)
@@ -370,15 +383,13 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
     for (int l = 0; l < m.layers; ++l) {
         const LayerWeights& L = w_.layer[l];
         mark(a);
-        check_ck(ck_rmsnorm(x_, L.attn_norm, h_, nullptr, M, H, m.rms_eps, stream_), "rmsnorm");
+        // weight-streaming regime (M <= 128): qkv accumulates with red.add (stream-K GEMM),
+        // so the norm kernel clears it; tensor regime: plain fp32 tile stores
+        check_ck(ck_rmsnorm(x_, L.attn_norm, h_, nullptr, M, H, m.rms_eps, small ? qkv_ : nullptr, Q, stream_),
+                 "rmsnorm");
         ++launches;
         done(a, &stat_other, 0, 0);
-        if (small) {
-            check_cuda(cudaMemsetAsync(qkv_, 0, static_cast<size_t>(M) * Q * 4, stream_), "memset qkv");
-            gemm(L.wqkv, h_, qkv_, L.bqkv, M, Q, H, CK_EPI_RED_F32, 0);
-        } else {
-            gemm(L.wqkv, h_, qkv_, L.bqkv, M, Q, H, CK_EPI_F32, 1);
-        }
+        gemm(L.wqkv, h_, qkv_, L.bqkv, M, Q, H, small ? CK_EPI_RED_F32 : CK_EPI_F32, small ? 0 : 1);
         mark(a);
         check_ck(ck_qkv_rope_append(qkv_, nullptr, q_, pool.base, bt, row_bt, row_pos, w_.cos_tab, w_.sin_tab, M,
                                     m.n_heads, m.n_kv_heads, l, m.layers, stream_),
@@ -388,10 +399,10 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         if (n_dec > 0) {
             mark(a);
             check_ck(ck_attn_decode(q_, pool.base, bt, D(o_d_row), D(o_d_len), D(o_d_bt), D(o_d_item0), D(o_d_work),
-                                    n_work, n_dec, b.blocks_per_split, attn_ws_, attn_, m.n_heads, m.n_kv_heads, l,
-                                    m.layers, scale, stream_),
+                                    n_work, n_dec, b.blocks_per_split, attn_ws_, attn_tickets_, attn_, m.n_heads,
+                                    m.n_kv_heads, l, m.layers, scale, stream_),
                      "attn_decode");
-            launches += 2;  // split-KV pass + combine
+            ++launches;
             done(a, &stat_decode_attn, dec_keys * kv_tok_layer, 4.0 * m.n_heads * m.head_dim * dec_keys);
         }
         if (b.p_len > 0) {
@@ -405,15 +416,11 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         }
         gemm(L.wo, attn_, x_, nullptr, M, H, NQ, CK_EPI_RED_F32, 0);
         mark(a);
-        check_ck(ck_rmsnorm(x_, L.ffn_norm, h_, nullptr, M, H, m.rms_eps, stream_), "rmsnorm");
+        check_ck(ck_rmsnorm(x_, L.ffn_norm, h_, nullptr, M, H, m.rms_eps, small ? gu_ : nullptr, 2 * F, stream_),
+                 "rmsnorm");
         ++launches;
         done(a, &stat_other, 0, 0);
-        if (small) {
-            check_cuda(cudaMemsetAsync(gu_, 0, static_cast<size_t>(M) * 2 * F * 4, stream_), "memset gu");
-            gemm(L.wgu, h_, gu_, nullptr, M, 2 * F, H, CK_EPI_RED_F32, 0);
-        } else {
-            gemm(L.wgu, h_, gu_, nullptr, M, 2 * F, H, CK_EPI_F32, 1);
-        }
+        gemm(L.wgu, h_, gu_, nullptr, M, 2 * F, H, small ? CK_EPI_RED_F32 : CK_EPI_F32, small ? 0 : 1);
         mark(a);
         check_ck(ck_silu_mul(gu_, act_, M, F, stream_), "silu_mul");
         ++launches;
@@ -422,13 +429,13 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
     }
     if (R > 0) {
         mark(a);
-        check_ck(ck_rmsnorm(x_, w_.final_norm, hs_, D(o_s_row), R, H, m.rms_eps, stream_), "final norm");
+        check_ck(ck_rmsnorm(x_, w_.final_norm, hs_, D(o_s_row), R, H, m.rms_eps, nullptr, 0, stream_), "final norm");
         ++launches;
         done(a, &stat_other, 0, 0);
         gemm(w_.lm_head, hs_, logits_, nullptr, R, m.vocab, H, CK_EPI_F32, 1);
         mark(a);
         check_ck(ck_argmax_emit(logits_, R, m.vocab, D(o_s_rid), reinterpret_cast<const long long*>(D(o_s_out)),
-                                last_tok, out_tok, stream_),
+                                last_tok, out_tok, arg_ws_, arg_tickets_, stream_),
                  "argmax");
         ++launches;
         done(a, &stat_other, 0, 0);

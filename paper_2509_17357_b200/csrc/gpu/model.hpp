@@ -170,6 +170,9 @@ class Worker {
     float* logits_ = nullptr;
     float* attn_ws_ = nullptr;
     long long attn_ws_floats_ = 0;
+    int* attn_tickets_ = nullptr;  // split-merge tickets, [max_rows * n_kv_heads], self-resetting
+    float* arg_ws_ = nullptr;      // argmax slice winners [max_sample * 64]
+    int* arg_tickets_ = nullptr;   // [max_sample], self-resetting
     int* meta_dev_ = nullptr;
     long long meta_cap_ = 0;
     // pinned staging ring for per-pass metadata

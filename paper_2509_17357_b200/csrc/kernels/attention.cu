@@ -1,13 +1,8 @@
 // Paged attention over the block-major KV pool (see cronus_ck.h for the layout).
 //
-// Decode (one query token per sequence, HBM bound): split-KV "flash decoding".
-//   A CTA = 4 warps owns one (sequence, kv head, split) work item of up to
-//   `blocks_per_split` 16-token blocks; warps stride over the blocks, each warp
-//   consuming a whole 16-token block (4 KiB of K + 4 KiB of V, both contiguous)
-//   per step for all G query heads of the GQA group, keeping an online softmax in
-//   registers. Partials (m, l, acc) are merged across warps in smem and across
-//   splits by a combine kernel. Algorithmic bytes = sum kv_len * 512 B per
-//   (layer, kv head) — K and V each read exactly once.
+// Decode (one query token per sequence, HBM bound): split-KV "flash decoding" on
+//   mma.sync with a per-warp cp.async ring (see attn_decode_kernel). Algorithmic
+//   bytes = sum kv_len * 512 B per (layer, kv head) — K and V each read once.
 //
 // Prefill / chunk (tensor bound): FlashAttention-2 style with mma.sync
 //   m16n8k16 bf16 (a CTA = 64 query rows x 1 head; 64-key K/V tiles gathered
@@ -31,171 +26,6 @@ constexpr int kTile = kBlk * kHD;      // elements per (block, layer, K|V, head)
 __device__ __forceinline__ size_t tile_off(int block, int layer, int kv, int head, int n_layers, int nkv) {
     return ((static_cast<size_t>(block) * n_layers + layer) * 2 + kv) * static_cast<size_t>(nkv) * kTile +
            static_cast<size_t>(head) * kTile;
-}
-
-// ============================================================== decode
-template <int G>
-__global__ void __launch_bounds__(128)
-    attn_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ pool,
-                       const int* __restrict__ bt, const int* __restrict__ seq_row, const int* __restrict__ seq_len,
-                       const int* __restrict__ seq_bt, const int* __restrict__ work, int blocks_per_split,
-                       float* __restrict__ ws, int nq, int nkv, int layer, int n_layers, float qscale) {
-    // q for the group, split into the two 64-dim halves with a 4-float pad so the
-    // two half-warps read different banks.
-    __shared__ __align__(16) float qs[G][2][68];
-    __shared__ __align__(16) float ps[4][G][16];
-    __shared__ float wm[4][G], wl[4][G];
-    __shared__ __align__(16) float wacc[4][G][kHD];
-
-    const int item = blockIdx.x;
-    const int kvh = blockIdx.y;
-    const int w = work[item];
-    const int s = w >> 16, split = w & 0xffff;
-    const int len = seq_len[s];
-    const int nblk = (len + kBlk - 1) / kBlk;
-    const int b0 = split * blocks_per_split;
-    const int b1 = min(nblk, b0 + blocks_per_split);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int* table = bt + seq_bt[s];
-
-    const __nv_bfloat16* qrow = q + static_cast<size_t>(seq_row[s]) * nq * kHD + static_cast<size_t>(kvh) * G * kHD;
-    for (int i = threadIdx.x; i < G * kHD; i += blockDim.x) {
-        const int h = i / kHD, d = i % kHD;
-        qs[h][d >> 6][d & 63] = bf2f(qrow[i]) * qscale;
-    }
-    __syncthreads();
-
-    float m[G], l[G], acc[G][4];
-#pragma unroll
-    for (int h = 0; h < G; ++h) {
-        m[h] = -INFINITY;
-        l[h] = 0.f;
-        acc[h][0] = acc[h][1] = acc[h][2] = acc[h][3] = 0.f;
-    }
-    const int t = lane & 15, half = lane >> 4;
-
-    for (int b = b0 + warp; b < b1; b += 4) {
-        const int blk = table[b];
-        const __nv_bfloat16* kt = pool + tile_off(blk, layer, 0, kvh, n_layers, nkv);
-        const __nv_bfloat16* vt = kt + static_cast<size_t>(nkv) * kTile;
-        // ---- loads (K half-row for QK, V 4-dim column slice for PV)
-        uint4 kv4[8];
-        const uint4* kp = reinterpret_cast<const uint4*>(kt + t * kHD + half * 64);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) kv4[i] = __ldg(kp + i);
-        uint2 vv[16];
-        const uint2* vp = reinterpret_cast<const uint2*>(vt) + lane;  // dims 4*lane..4*lane+3
-        const int n_valid = min(kBlk, len - b * kBlk);  // slots past the sequence end hold stale data
-#pragma unroll
-        for (int j = 0; j < 16; ++j) vv[j] = j < n_valid ? __ldg(vp + j * (kHD / 4)) : make_uint2(0u, 0u);
-
-        // ---- scores
-        float sc[G];
-#pragma unroll
-        for (int h = 0; h < G; ++h) sc[h] = 0.f;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const float2 k01 = unpack_bf16x2(kv4[i].x), k23 = unpack_bf16x2(kv4[i].y), k45 = unpack_bf16x2(kv4[i].z),
-                         k67 = unpack_bf16x2(kv4[i].w);
-#pragma unroll
-            for (int h = 0; h < G; ++h) {
-                const float4 qa = *reinterpret_cast<const float4*>(&qs[h][half][i * 8]);
-                const float4 qb = *reinterpret_cast<const float4*>(&qs[h][half][i * 8 + 4]);
-                sc[h] += qa.x * k01.x + qa.y * k01.y + qa.z * k23.x + qa.w * k23.y + qb.x * k45.x + qb.y * k45.y +
-                         qb.z * k67.x + qb.w * k67.y;
-            }
-        }
-        const bool valid = b * kBlk + t < len;
-#pragma unroll
-        for (int h = 0; h < G; ++h) {
-            sc[h] += __shfl_xor_sync(0xffffffffu, sc[h], 16);
-            if (!valid) sc[h] = -INFINITY;
-            float mx = sc[h];
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-            const float mn = fmaxf(m[h], mx);
-            const float p = exp2f(sc[h] - mn);
-            float ps_sum = p;
-            ps_sum += __shfl_xor_sync(0xffffffffu, ps_sum, 8);
-            ps_sum += __shfl_xor_sync(0xffffffffu, ps_sum, 4);
-            ps_sum += __shfl_xor_sync(0xffffffffu, ps_sum, 2);
-            ps_sum += __shfl_xor_sync(0xffffffffu, ps_sum, 1);
-            const float corr = exp2f(m[h] - mn);
-            l[h] = l[h] * corr + ps_sum;
-            m[h] = mn;
-            acc[h][0] *= corr;
-            acc[h][1] *= corr;
-            acc[h][2] *= corr;
-            acc[h][3] *= corr;
-            if (half == 0) ps[warp][h][t] = p;
-        }
-        __syncwarp();
-        // ---- P x V
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const float2 v01 = unpack_bf16x2(vv[j].x), v23 = unpack_bf16x2(vv[j].y);
-#pragma unroll
-            for (int h = 0; h < G; ++h) {
-                const float p = ps[warp][h][j];
-                acc[h][0] += p * v01.x;
-                acc[h][1] += p * v01.y;
-                acc[h][2] += p * v23.x;
-                acc[h][3] += p * v23.y;
-            }
-        }
-        __syncwarp();
-    }
-
-    // ---- merge the 4 warps
-#pragma unroll
-    for (int h = 0; h < G; ++h) {
-        if (lane == 0) {
-            wm[warp][h] = m[h];
-            wl[warp][h] = l[h];
-        }
-        *reinterpret_cast<float4*>(&wacc[warp][h][lane * 4]) = make_float4(acc[h][0], acc[h][1], acc[h][2], acc[h][3]);
-    }
-    __syncthreads();
-    // partial layout per (item, q head): [m, l, acc[128]]
-    for (int i = threadIdx.x; i < G * kHD; i += blockDim.x) {
-        const int h = i / kHD, d = i % kHD;
-        float M = -INFINITY;
-#pragma unroll
-        for (int w2 = 0; w2 < 4; ++w2) M = fmaxf(M, wm[w2][h]);
-        float Lsum = 0.f, A = 0.f;
-#pragma unroll
-        for (int w2 = 0; w2 < 4; ++w2) {
-            const float f = wm[w2][h] == -INFINITY ? 0.f : exp2f(wm[w2][h] - M);
-            Lsum += wl[w2][h] * f;
-            A += wacc[w2][h][d] * f;
-        }
-        float* part = ws + (static_cast<size_t>(item) * nq + kvh * G + h) * (kHD + 2);
-        part[2 + d] = A;
-        if (d == 0) {
-            part[0] = M;
-            part[1] = Lsum;
-        }
-    }
-}
-
-// out[row(s), h, :] = sum_splits A * 2^(m - M) / sum_splits l * 2^(m - M)
-__global__ void attn_decode_combine_kernel(const float* __restrict__ ws, const int* __restrict__ seq_row,
-                                           const int* __restrict__ seq_item0, __nv_bfloat16* __restrict__ out,
-                                           int nq) {
-    const int s = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
-    const int i0 = seq_item0[s], i1 = seq_item0[s + 1];
-    float M = -INFINITY;
-    for (int i = i0; i < i1; ++i) M = fmaxf(M, ws[(static_cast<size_t>(i) * nq + h) * (kHD + 2)]);
-    float L = 0.f, A = 0.f;
-    for (int i = i0; i < i1; ++i) {
-        const float* part = ws + (static_cast<size_t>(i) * nq + h) * (kHD + 2);
-        const float f = part[0] == -INFINITY ? 0.f : exp2f(part[0] - M);
-        L += part[1] * f;
-        A += part[2 + d] * f;
-    }
-    out[static_cast<size_t>(seq_row[s]) * nq * kHD + h * kHD + d] = f2bf(L > 0.f ? A / L : 0.f);
 }
 
 // ============================================================== prefill (mma.sync)
@@ -248,6 +78,8 @@ __global__ void __launch_bounds__(128)
     attn_prefill_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ pool,
                         const int* __restrict__ table, int q_row0, int q_len, int pos0, __nv_bfloat16* __restrict__ out,
                         int nq, int nkv, int layer, int n_layers, float qk_scale_log2) {
+    pdl_wait();
+    pdl_launch();
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem_raw);
     __nv_bfloat16* sK = sQ + kPQ * kPad;          // [2][64][kPad]
@@ -410,39 +242,264 @@ __global__ void __launch_bounds__(128)
     }
 }
 
+
+// ============================================================== decode (split-KV, mma.sync)
+// One CTA = 4 warps owns one (sequence, kv head, split) work item. Each warp streams
+// every 4th 16-token block of the split through its own cp.async ring (kDecStages
+// deep, 128-B XOR-swizzled rows: conflict-free ldmatrix), and computes
+//   S[16 x 16] = Qpad[16 x 128] K^T   (G query heads padded to 16 MMA rows)
+//   O[16 x 128] += P[16 x 16] V       with an online softmax in registers,
+// i.e. 32 mma.sync per 8 KiB of K+V — the tensor pipe is idle most of the time and
+// the kernel is bound by HBM, as it should be. The warps merge in smem; the split
+// partials are merged by the last CTA of each (sequence, kv head) (atomic ticket),
+// so the whole op is one launch.
+constexpr int kDecStages = 3;
+constexpr int kDecTile = kBlk * kHD * 2;  // bytes of one K (or V) block tile
+
+__device__ __forceinline__ uint32_t swz(int row, int chunk) {  // byte offset in a [16][128] bf16 tile
+    return static_cast<uint32_t>(row * 256 + ((chunk ^ (row & 7)) << 4));
+}
+
+template <int G>
+__global__ void __launch_bounds__(128)
+    attn_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ pool,
+                       const int* __restrict__ bt, const int* __restrict__ seq_row, const int* __restrict__ seq_len,
+                       const int* __restrict__ seq_bt, const int* __restrict__ seq_item0,
+                       const int* __restrict__ work, int blocks_per_split, float* __restrict__ ws,
+                       int* __restrict__ tickets, __nv_bfloat16* __restrict__ out, int nq, int nkv, int layer,
+                       int n_layers, float qk_scale_log2) {
+    pdl_wait();
+    pdl_launch();
+    extern __shared__ __align__(128) uint8_t dsm[];
+    uint8_t* sQ = dsm;                                    // [16][128] bf16, swizzled
+    uint8_t* sKV = dsm + kDecTile;                        // [4 warps][stages][K|V] tiles
+    __shared__ float wm[4][16], wl[4][16];
+    __shared__ int s_last;
+
+    const int item = blockIdx.x, kvh = blockIdx.y;
+    const int wk = work[item];
+    const int s = wk >> 16, split = wk & 0xffff;
+    const int len = seq_len[s];
+    const int nblk = (len + kBlk - 1) / kBlk;
+    const int b0 = split * blocks_per_split, b1 = min(nblk, b0 + blocks_per_split);
+    const int nsplit = seq_item0[s + 1] - seq_item0[s];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, tq = lane & 3;
+    const int* table = bt + seq_bt[s];
+    const int row = seq_row[s];
+
+    // ---- Q (G rows, zero padded to 16)
+    {
+        const __nv_bfloat16* qrow = q + static_cast<size_t>(row) * nq * kHD + static_cast<size_t>(kvh) * G * kHD;
+        for (int c = threadIdx.x; c < 16 * 16; c += blockDim.x) {
+            const int r = c >> 4, ch = c & 15;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (r < G) v = *reinterpret_cast<const uint4*>(qrow + r * kHD + ch * 8);
+            *reinterpret_cast<uint4*>(sQ + swz(r, ch)) = v;
+        }
+    }
+    // ---- per-warp K/V ring
+    uint8_t* ring = sKV + static_cast<size_t>(warp) * kDecStages * 2 * kDecTile;
+    const int first = b0 + warp;
+    const int mine = first < b1 ? (b1 - first + 3) / 4 : 0;
+    auto load = [&](int i) {  // block #i of this warp -> stage i % kDecStages
+        const int b = first + 4 * i;
+        const int blk = table[b];
+        const __nv_bfloat16* kt = pool + tile_off(blk, layer, 0, kvh, n_layers, nkv);
+        const __nv_bfloat16* vt = kt + static_cast<size_t>(nkv) * kTile;
+        uint8_t* dK = ring + (i % kDecStages) * 2 * kDecTile;
+        uint8_t* dV = dK + kDecTile;
+        const int valid = min(kBlk, len - b * kBlk);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {  // 256 16-B chunks per tile, 8 per lane
+            const int c = lane + 32 * j;
+            const int r = c >> 4, ch = c & 15;
+            const bool ok = r < valid;  // slots past the sequence end may hold stale data: zero-fill
+            cp_async16(dK + swz(r, ch), kt + r * kHD + ch * 8, ok);
+            cp_async16(dV + swz(r, ch), vt + r * kHD + ch * 8, ok);
+        }
+    };
+#pragma unroll
+    for (int i = 0; i < kDecStages - 1; ++i) {
+        if (i < mine) load(i);
+        cp_commit();
+    }
+    __syncthreads();  // sQ visible
+    uint32_t qf[8][4];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+        const int r = lane & 15, ch = 2 * kk + (lane >> 4);
+        ldsm_x4(qf[kk], sQ + swz(r, ch));
+    }
+    float o[16][4];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float m_run = -INFINITY, l_run = 0.f;  // row g (query head g of the group)
+
+    for (int i = 0; i < mine; ++i) {
+        cp_wait<kDecStages - 2>();
+        __syncwarp();
+        const uint8_t* K = ring + (i % kDecStages) * 2 * kDecTile;
+        const uint8_t* V = K + kDecTile;
+        float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            uint32_t b[4];
+            const int r = (lane & 7) + ((lane >> 4) << 3), ch = 2 * kk + ((lane >> 3) & 1);
+            ldsm_x4(b, K + swz(r, ch));
+            mma16816(s0, qf[kk], b[0], b[1]);
+            mma16816(s1, qf[kk], b[2], b[3]);
+        }
+        const int tok0 = (first + 4 * i) * kBlk;
+        float sc[4];
+        sc[0] = tok0 + 2 * tq < len ? s0[0] * qk_scale_log2 : -INFINITY;
+        sc[1] = tok0 + 2 * tq + 1 < len ? s0[1] * qk_scale_log2 : -INFINITY;
+        sc[2] = tok0 + 8 + 2 * tq < len ? s1[0] * qk_scale_log2 : -INFINITY;
+        sc[3] = tok0 + 9 + 2 * tq < len ? s1[1] * qk_scale_log2 : -INFINITY;
+        float mx = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float mn = fmaxf(m_run, mx);  // finite: token 0 of every block is valid
+        const float corr = exp2f(m_run - mn);
+        float p[4], rs = 0.f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            p[e] = exp2f(sc[e] - mn);
+            rs += p[e];
+        }
+        rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+        rs += __shfl_xor_sync(0xffffffffu, rs, 2);
+        l_run = l_run * corr + rs;
+        m_run = mn;
+        uint32_t pf[4];
+        pf[0] = pack_bf16x2(p[0], p[1]);
+        pf[1] = 0u;  // padded rows 8..15
+        pf[2] = pack_bf16x2(p[2], p[3]);
+        pf[3] = 0u;
+#pragma unroll
+        for (int nd = 0; nd < 16; ++nd) {
+            o[nd][0] *= corr;
+            o[nd][1] *= corr;
+        }
+#pragma unroll
+        for (int nd = 0; nd < 16; nd += 2) {
+            uint32_t b[4];
+            const int r = (lane & 7) + (((lane >> 3) & 1) << 3), ch = nd + (lane >> 4);
+            ldsm_x4_t(b, V + swz(r, ch));
+            mma16816(o[nd], pf, b[0], b[1]);
+            mma16816(o[nd + 1], pf, b[2], b[3]);
+        }
+        __syncwarp();
+        const int nxt = i + kDecStages - 1;
+        if (nxt < mine) load(nxt);
+        cp_commit();
+    }
+    cp_wait<0>();
+
+    // ---- merge the 4 warps (reuse the ring as [4][16][128] fp32 scratch)
+    __syncthreads();
+    float* wo = reinterpret_cast<float*>(sKV);
+    if (tq == 0) {
+        wm[warp][g] = m_run;
+        wl[warp][g] = l_run;
+    }
+#pragma unroll
+    for (int nd = 0; nd < 16; ++nd) {
+        wo[(warp * 16 + g) * kHD + nd * 8 + 2 * tq] = o[nd][0];
+        wo[(warp * 16 + g) * kHD + nd * 8 + 2 * tq + 1] = o[nd][1];
+    }
+    __syncthreads();
+    const bool single = nsplit == 1;
+    for (int i = threadIdx.x; i < G * kHD; i += blockDim.x) {
+        const int h = i / kHD, d = i % kHD;
+        float M = -INFINITY;
+#pragma unroll
+        for (int w2 = 0; w2 < 4; ++w2) M = fmaxf(M, wm[w2][h]);
+        float Ls = 0.f, A = 0.f;
+#pragma unroll
+        for (int w2 = 0; w2 < 4; ++w2) {
+            const float f = wm[w2][h] == -INFINITY ? 0.f : exp2f(wm[w2][h] - M);
+            Ls += wl[w2][h] * f;
+            A += wo[(w2 * 16 + h) * kHD + d] * f;
+        }
+        if (single) {
+            out[static_cast<size_t>(row) * nq * kHD + (kvh * G + h) * kHD + d] = f2bf(Ls > 0.f ? A / Ls : 0.f);
+        } else {
+            float* part = ws + (static_cast<size_t>(item) * nq + kvh * G + h) * (kHD + 2);
+            part[2 + d] = A;
+            if (d == 0) {
+                part[0] = M;
+                part[1] = Ls;
+            }
+        }
+    }
+    if (single) return;
+    // ---- last CTA of this (sequence, kv head) merges the splits
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int prev = atomicAdd(&tickets[s * nkv + kvh], 1);
+        s_last = prev == nsplit - 1;
+        if (s_last) tickets[s * nkv + kvh] = 0;  // self-resetting for the next launch
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int i0 = seq_item0[s], i1 = seq_item0[s + 1];
+    for (int i = threadIdx.x; i < G * kHD; i += blockDim.x) {
+        const int h = i / kHD, d = i % kHD;
+        const int hq = kvh * G + h;
+        float M = -INFINITY;
+        for (int it = i0; it < i1; ++it) M = fmaxf(M, __ldcg(ws + (static_cast<size_t>(it) * nq + hq) * (kHD + 2)));
+        float Ls = 0.f, A = 0.f;
+        for (int it = i0; it < i1; ++it) {
+            const float* part = ws + (static_cast<size_t>(it) * nq + hq) * (kHD + 2);
+            const float pm = __ldcg(part);
+            const float f = pm == -INFINITY ? 0.f : exp2f(pm - M);
+            Ls += __ldcg(part + 1) * f;
+            A += __ldcg(part + 2 + d) * f;
+        }
+        out[static_cast<size_t>(row) * nq * kHD + hq * kHD + d] = f2bf(Ls > 0.f ? A / Ls : 0.f);
+    }
+}
+
 template <int G>
 int launch_decode(const void* q, const void* pool, const int* bt, const int* seq_row, const int* seq_len,
-                  const int* seq_bt, const int* work, int n_work, int bps, float* ws, int nq, int nkv, int layer,
-                  int n_layers, float qscale, cudaStream_t s) {
-    attn_decode_kernel<G><<<dim3(n_work, nkv), 128, 0, s>>>(
-        static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(pool), bt, seq_row, seq_len, seq_bt,
-        work, bps, ws, nq, nkv, layer, n_layers, qscale);
-    return static_cast<int>(cudaGetLastError());
+                  const int* seq_bt, const int* seq_item0, const int* work, int n_work, int bps, float* ws,
+                  int* tickets, void* out, int nq, int nkv, int layer, int n_layers, float qk, cudaStream_t st) {
+    constexpr int smem = kDecTile + 4 * kDecStages * 2 * kDecTile;
+    static_assert(4 * kDecStages * 2 * kDecTile >= 4 * 16 * kHD * 4, "merge scratch must fit in the ring");
+    static unsigned mask = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(mask & (1u << dev))) {
+        cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return static_cast<int>(e);
+        mask |= 1u << dev;
+    }
+    return launch_pdl(attn_decode_kernel<G>, dim3(n_work, nkv), dim3(128), smem, st,
+                      static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(pool), bt, seq_row,
+                      seq_len, seq_bt, seq_item0, work, bps, ws, tickets, static_cast<__nv_bfloat16*>(out), nq, nkv,
+                      layer, n_layers, qk);
 }
 
 }  // namespace
 
 extern "C" int ck_attn_decode(const void* q, const void* kv_pool, const int* bt, const int* seq_row,
                               const int* seq_len, const int* seq_bt, const int* seq_item0, const int* work,
-                              int n_work, int n_seq, int blocks_per_split, float* ws, void* out, int nq, int nkv,
-                              int layer, int n_layers, float scale, void* stream) {
+                              int n_work, int n_seq, int blocks_per_split, float* ws, int* tickets, void* out,
+                              int nq, int nkv, int layer, int n_layers, float scale, void* stream) {
     if (n_seq <= 0 || n_work <= 0) return 0;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const int G = nq / nkv;
-    const float qscale = scale * kLog2e;
-    int rc;
-    switch (G) {
-        case 1: rc = launch_decode<1>(q, kv_pool, bt, seq_row, seq_len, seq_bt, work, n_work, blocks_per_split, ws, nq, nkv, layer, n_layers, qscale, s); break;
-        case 2: rc = launch_decode<2>(q, kv_pool, bt, seq_row, seq_len, seq_bt, work, n_work, blocks_per_split, ws, nq, nkv, layer, n_layers, qscale, s); break;
-        case 4: rc = launch_decode<4>(q, kv_pool, bt, seq_row, seq_len, seq_bt, work, n_work, blocks_per_split, ws, nq, nkv, layer, n_layers, qscale, s); break;
-        case 7: rc = launch_decode<7>(q, kv_pool, bt, seq_row, seq_len, seq_bt, work, n_work, blocks_per_split, ws, nq, nkv, layer, n_layers, qscale, s); break;
-        case 8: rc = launch_decode<8>(q, kv_pool, bt, seq_row, seq_len, seq_bt, work, n_work, blocks_per_split, ws, nq, nkv, layer, n_layers, qscale, s); break;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const float qk = scale * kLog2e;
+    switch (nq / nkv) {
+        case 1: return launch_decode<1>(q, kv_pool, bt, seq_row, seq_len, seq_bt, seq_item0, work, n_work, blocks_per_split, ws, tickets, out, nq, nkv, layer, n_layers, qk, st);
+        case 2: return launch_decode<2>(q, kv_pool, bt, seq_row, seq_len, seq_bt, seq_item0, work, n_work, blocks_per_split, ws, tickets, out, nq, nkv, layer, n_layers, qk, st);
+        case 4: return launch_decode<4>(q, kv_pool, bt, seq_row, seq_len, seq_bt, seq_item0, work, n_work, blocks_per_split, ws, tickets, out, nq, nkv, layer, n_layers, qk, st);
+        case 7: return launch_decode<7>(q, kv_pool, bt, seq_row, seq_len, seq_bt, seq_item0, work, n_work, blocks_per_split, ws, tickets, out, nq, nkv, layer, n_layers, qk, st);
+        case 8: return launch_decode<8>(q, kv_pool, bt, seq_row, seq_len, seq_bt, seq_item0, work, n_work, blocks_per_split, ws, tickets, out, nq, nkv, layer, n_layers, qk, st);
         default: return static_cast<int>(cudaErrorInvalidValue);
     }
-    if (rc) return rc;
-    attn_decode_combine_kernel<<<dim3(n_seq, nq), kHD, 0, s>>>(ws, seq_row, seq_item0,
-                                                               static_cast<__nv_bfloat16*>(out), nq);
-    return static_cast<int>(cudaGetLastError());
 }
 
 extern "C" int ck_attn_prefill(const void* q, const void* kv_pool, const int* bt, int q_row0, int q_len, int pos0,
@@ -458,8 +515,7 @@ extern "C" int ck_attn_prefill(const void* q, const void* kv_pool, const int* bt
         attr_mask |= 1u << dev;
     }
     const dim3 grid((q_len + kPQ - 1) / kPQ, nq);
-    attn_prefill_kernel<<<grid, 128, smem, static_cast<cudaStream_t>(stream)>>>(
-        static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(kv_pool), bt, q_row0, q_len, pos0,
-        static_cast<__nv_bfloat16*>(out), nq, nkv, layer, n_layers, scale * kLog2e);
-    return static_cast<int>(cudaGetLastError());
+    return launch_pdl(attn_prefill_kernel, grid, dim3(128), smem, static_cast<cudaStream_t>(stream),
+                      static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(kv_pool), bt, q_row0,
+                      q_len, pos0, static_cast<__nv_bfloat16*>(out), nq, nkv, layer, n_layers, scale * kLog2e);
 }

@@ -182,6 +182,14 @@ __device__ __forceinline__ void red_add_f32(float* p, float v) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch: every kernel of the forward chain is launched with
+// programmatic stream serialization, waits for its producer grid at pdl_wait()
+// (after any prologue that touches no dependent data) and immediately lets its own
+// dependents launch, so launch latency and prologues overlap the previous kernel.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ int warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0); }
 
@@ -197,4 +205,36 @@ __device__ __forceinline__ bool elect_one() {
     return pred != 0;
 }
 
+}  // namespace ck
+
+#include <cstdlib>
+#include <utility>
+namespace ck {
+// Launch `kernel` on `stream` with programmatic stream serialization (PDL).
+// CRONUS_NO_PDL=1 launches without the attribute (griddepcontrol.* become no-ops):
+// required under Nsight Compute, whose kernel replay cannot coexist with dependents
+// already resident at griddepcontrol.wait.
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("CRONUS_NO_PDL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                      Args&&... args) {
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return static_cast<int>(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 }  // namespace ck

@@ -18,6 +18,8 @@ inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 // ---------------------------------------------------------------- init / tokens
 __global__ void init_uniform_kernel(__nv_bfloat16* out, long long n, uint64_t seed, uint64_t tid, float step,
                                     float offset) {
+    pdl_wait();
+    pdl_launch();
     const uint64_t base = seed * 0x9E3779B97F4A7C15ull + tid * 0xD1B54A32D192ED03ull;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -29,6 +31,8 @@ __global__ void init_uniform_kernel(__nv_bfloat16* out, long long n, uint64_t se
 }
 
 __global__ void prompt_tokens_kernel(int* out, const int* req, const int* pos, int n, uint64_t seed, int vocab) {
+    pdl_wait();
+    pdl_launch();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint64_t h = mix64(seed * 0x9E3779B97F4A7C15ull + static_cast<uint64_t>(static_cast<uint32_t>(req[i])) *
@@ -38,6 +42,8 @@ __global__ void prompt_tokens_kernel(int* out, const int* req, const int* pos, i
 }
 
 __global__ void rope_table_kernel(float* c, float* s, int max_pos, double theta) {
+    pdl_wait();
+    pdl_launch();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= max_pos * 64) return;
     const int p = i >> 6, f = i & 63;
@@ -52,6 +58,8 @@ __global__ void rope_table_kernel(float* c, float* s, int max_pos, double theta)
 __global__ void embed_kernel(float* __restrict__ x, const __nv_bfloat16* __restrict__ emb, const int* row_rid,
                              const int* row_pos, const int* row_dec, const int* prompt, const long long* prompt_off,
                              const int* last_tok, int H) {
+    pdl_wait();
+    pdl_launch();
     const int m = blockIdx.x;
     const int rid = row_rid[m];
     const int tok = row_dec[m] ? last_tok[rid] : prompt[prompt_off[rid] + row_pos[m]];
@@ -78,83 +86,99 @@ __device__ float block_sum(float v, float* red) {
     return t;
 }
 
-// y = bf16(x * rsqrt(mean(x^2) + eps) * gamma); fp32 math, one CTA per output row.
+// y = bf16(x * rsqrt(mean(x^2) + eps) * gamma); fp32 math, one CTA per output row, the
+// row held in registers (single pass over x: one L2 round trip on the critical path).
+constexpr int kRmsMaxVec = 8;  // float4 per thread: H <= 8 * 4 * blockDim
+
 __global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ gamma,
-                               __nv_bfloat16* __restrict__ out, const int* rows, int H, float eps) {
+                               __nv_bfloat16* __restrict__ out, const int* rows, int H, float eps,
+                               float* __restrict__ zero, int zero_cols) {
+    pdl_wait();
+    pdl_launch();
     __shared__ float red[32];
     const int r = blockIdx.x;
     const int src = rows ? rows[r] : r;
     const float4* xr = reinterpret_cast<const float4*>(x + static_cast<size_t>(src) * H);
+    const int n4 = H / 4;
+    float4 v[kRmsMaxVec];
     float ss = 0.f;
-    for (int i = threadIdx.x; i < H / 4; i += blockDim.x) {
-        const float4 v = xr[i];
-        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+#pragma unroll
+    for (int j = 0; j < kRmsMaxVec; ++j) {
+        const int i = threadIdx.x + j * blockDim.x;
+        v[j] = i < n4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        ss += v[j].x * v[j].x + v[j].y * v[j].y + v[j].z * v[j].z + v[j].w * v[j].w;
+    }
+    if (zero) {
+        float4* z = reinterpret_cast<float4*>(zero + static_cast<size_t>(r) * zero_cols);
+        for (int i = threadIdx.x; i < zero_cols / 4; i += blockDim.x) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     ss = block_sum(ss, red);
     const float inv = rsqrtf(ss / static_cast<float>(H) + eps);
     const uint2* g = reinterpret_cast<const uint2*>(gamma);
     uint2* o = reinterpret_cast<uint2*>(out + static_cast<size_t>(r) * H);
-    for (int i = threadIdx.x; i < H / 4; i += blockDim.x) {
-        const float4 v = xr[i];
-        const uint2 gg = g[i];
-        const float2 g0 = unpack_bf16x2(gg.x), g1 = unpack_bf16x2(gg.y);
-        o[i] = make_uint2(pack_bf16x2(v.x * inv * g0.x, v.y * inv * g0.y), pack_bf16x2(v.z * inv * g1.x, v.w * inv * g1.y));
+#pragma unroll
+    for (int j = 0; j < kRmsMaxVec; ++j) {
+        const int i = threadIdx.x + j * blockDim.x;
+        if (i < n4) {
+            const uint2 gg = g[i];
+            const float2 g0 = unpack_bf16x2(gg.x), g1 = unpack_bf16x2(gg.y);
+            o[i] = make_uint2(pack_bf16x2(v[j].x * inv * g0.x, v[j].y * inv * g0.y),
+                              pack_bf16x2(v[j].z * inv * g1.x, v[j].w * inv * g1.y));
+        }
     }
 }
 
 // ---------------------------------------------------------------- QKV post-processing
-// One CTA per row: (+bias) -> RoPE (rotate-half pairs (i, i+64)) -> q out (bf16) and
-// k, v into the row's paged KV slot.
+// grid (row, head): 64 threads per head. Rotary heads (q and k): thread i rotates the
+// pair (i, i + 64) (rotate-half RoPE); v heads: thread i moves dims (2i, 2i + 1).
+// q goes to q_out (bf16); k and v go to the row's slot of its paged KV block.
 __global__ void qkv_rope_append_kernel(const float* __restrict__ qkv, const __nv_bfloat16* __restrict__ bias,
                                        __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ pool,
                                        const int* __restrict__ bt, const int* __restrict__ row_bt,
                                        const int* __restrict__ row_pos, const float* __restrict__ cos_tab,
                                        const float* __restrict__ sin_tab, int nq, int nkv, int layer, int n_layers) {
-    const int m = blockIdx.x;
+    pdl_wait();
+    pdl_launch();
+    const int m = blockIdx.x, h = blockIdx.y, i = threadIdx.x;
     const int pos = row_pos[m];
-    const int width = (nq + 2 * nkv) * 128;
-    const float* row = qkv + static_cast<size_t>(m) * width;
-    const float* cs = cos_tab + static_cast<size_t>(pos) * 64;
-    const float* sn = sin_tab + static_cast<size_t>(pos) * 64;
-    const int block = bt[row_bt[m] + (pos >> 4)];
-    const int slot = pos & 15;
+    const float* row = qkv + static_cast<size_t>(m) * (nq + 2 * nkv) * 128 + h * 128;
+    const __nv_bfloat16* brow = bias ? bias + h * 128 : nullptr;
     const size_t head_stride = 16 * 128;
-    __nv_bfloat16* kbase =
-        pool + ((static_cast<size_t>(block) * n_layers + layer) * 2) * nkv * head_stride + slot * 128;
-    __nv_bfloat16* vbase = kbase + nkv * head_stride;
-    // rotary pairs: (nq + nkv) heads x 64 pairs
-    const int n_pairs = (nq + nkv) * 64;
-    for (int t = threadIdx.x; t < n_pairs; t += blockDim.x) {
-        const int h = t >> 6, i = t & 63;
-        const int c0 = h * 128 + i, c1 = c0 + 64;
-        float a = row[c0], b = row[c1];
-        if (bias) {
-            a += bf2f(bias[c0]);
-            b += bf2f(bias[c1]);
+    if (h < nq + nkv) {
+        float a = row[i], b = row[i + 64];
+        if (brow) {
+            a += bf2f(brow[i]);
+            b += bf2f(brow[i + 64]);
         }
-        const float ra = a * cs[i] - b * sn[i];
-        const float rb = b * cs[i] + a * sn[i];
+        const float c = cos_tab[static_cast<size_t>(pos) * 64 + i], sn = sin_tab[static_cast<size_t>(pos) * 64 + i];
+        const float ra = a * c - b * sn, rb = b * c + a * sn;
+        __nv_bfloat16* dst;
         if (h < nq) {
-            __nv_bfloat16* qo = q_out + static_cast<size_t>(m) * nq * 128 + h * 128;
-            qo[i] = f2bf(ra);
-            qo[i + 64] = f2bf(rb);
+            dst = q_out + static_cast<size_t>(m) * nq * 128 + h * 128;
         } else {
-            __nv_bfloat16* ko = kbase + (h - nq) * head_stride;
-            ko[i] = f2bf(ra);
-            ko[i + 64] = f2bf(rb);
+            const int block = bt[row_bt[m] + (pos >> 4)];
+            dst = pool + ((static_cast<size_t>(block) * n_layers + layer) * 2 * nkv + (h - nq)) * head_stride +
+                  (pos & 15) * 128;
         }
-    }
-    const int vcols = nkv * 128;
-    for (int t = threadIdx.x; t < vcols; t += blockDim.x) {
-        const int c = (nq + nkv) * 128 + t;
-        float v = row[c];
-        if (bias) v += bf2f(bias[c]);
-        vbase[(t >> 7) * head_stride + (t & 127)] = f2bf(v);
+        dst[i] = f2bf(ra);
+        dst[i + 64] = f2bf(rb);
+    } else {
+        float2 v = *reinterpret_cast<const float2*>(row + 2 * i);
+        if (brow) {
+            v.x += bf2f(brow[2 * i]);
+            v.y += bf2f(brow[2 * i + 1]);
+        }
+        const int block = bt[row_bt[m] + (pos >> 4)];
+        __nv_bfloat16* dst = pool + ((static_cast<size_t>(block) * n_layers + layer) * 2 * nkv + nkv +
+                                     (h - nq - nkv)) * head_stride + (pos & 15) * 128;
+        *reinterpret_cast<uint32_t*>(dst + 2 * i) = pack_bf16x2(v.x, v.y);
     }
 }
 
 // ---------------------------------------------------------------- SiLU * up
 __global__ void silu_mul_kernel(const float* __restrict__ gu, __nv_bfloat16* __restrict__ act, long long n_pairs4) {
+    pdl_wait();
+    pdl_launch();
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n_pairs4;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         // 4 (gate, up) pairs = 8 floats -> 4 bf16
@@ -169,31 +193,43 @@ __global__ void silu_mul_kernel(const float* __restrict__ gu, __nv_bfloat16* __r
 }
 
 // ---------------------------------------------------------------- greedy sampling
+// grid (row, kArgChunks): each CTA reduces a contiguous vocab slice with float4 loads;
+// the last CTA of a row (atomic ticket) reduces the slice winners and emits the token.
+// Order: larger value first, then the lower index (numpy argmax semantics).
+constexpr int kArgChunks = 32;
+
+__device__ __forceinline__ void arg_better(float& bv, int& bi, float v, int i) {
+    if (v > bv || (v == bv && i < bi)) {
+        bv = v;
+        bi = i;
+    }
+}
+
 __global__ void argmax_emit_kernel(const float* __restrict__ logits, int V, const int* rid, const long long* out_idx,
-                                   int* last_tok, int* out_tok) {
-    const int r = blockIdx.x;
-    const float* row = logits + static_cast<size_t>(r) * V;
-    float best = -INFINITY;
-    int bi = 0x7fffffff;
-    for (int v = threadIdx.x; v < V; v += blockDim.x) {
-        const float x = row[v];
-        if (x > best) {  // strictly greater: keeps the lowest index within a thread
-            best = x;
-            bi = v;
-        }
-    }
-    // (value desc, index asc) reduction
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) {
-            best = ob;
-            bi = oi;
-        }
-    }
+                                   int* last_tok, int* out_tok, float* __restrict__ pv, int* __restrict__ pi,
+                                   int* __restrict__ tickets) {
+    pdl_wait();
+    pdl_launch();
     __shared__ float sb[32];
     __shared__ int si[32];
+    __shared__ int s_last;
+    const int r = blockIdx.x, c = blockIdx.y;
+    const int n4 = V / 4;
+    const int lo = static_cast<int>(static_cast<long long>(c) * n4 / kArgChunks);
+    const int hi = static_cast<int>(static_cast<long long>(c + 1) * n4 / kArgChunks);
+    const float4* row = reinterpret_cast<const float4*>(logits + static_cast<size_t>(r) * V);
+    float best = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int v = lo + threadIdx.x; v < hi; v += blockDim.x) {
+        const float4 x = row[v];
+        arg_better(best, bi, x.x, 4 * v);
+        arg_better(best, bi, x.y, 4 * v + 1);
+        arg_better(best, bi, x.z, 4 * v + 2);
+        arg_better(best, bi, x.w, 4 * v + 3);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        arg_better(best, bi, __shfl_xor_sync(0xffffffffu, best, o), __shfl_xor_sync(0xffffffffu, bi, o));
     const int w = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0) {
         sb[w] = best;
@@ -201,15 +237,22 @@ __global__ void argmax_emit_kernel(const float* __restrict__ logits, int V, cons
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        const int nw = blockDim.x >> 5;
-        for (int i = 1; i < nw; ++i)
-            if (sb[i] > best || (sb[i] == best && si[i] < bi)) {
-                best = sb[i];
-                bi = si[i];
-            }
-        last_tok[rid[r]] = bi;
-        out_tok[out_idx[r]] = bi;
+        for (int i = 1; i < static_cast<int>(blockDim.x >> 5); ++i) arg_better(best, bi, sb[i], si[i]);
+        pv[r * kArgChunks + c] = best;
+        pi[r * kArgChunks + c] = bi;
+        __threadfence();
+        const int prev = atomicAdd(&tickets[r], 1);
+        s_last = prev == kArgChunks - 1;
     }
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    __threadfence();
+    float fb = -INFINITY;
+    int fi = 0x7fffffff;
+    for (int i = 0; i < kArgChunks; ++i) arg_better(fb, fi, __ldcg(pv + r * kArgChunks + i), __ldcg(pi + r * kArgChunks + i));
+    tickets[r] = 0;  // self-resetting
+    last_tok[rid[r]] = fi;
+    out_tok[out_idx[r]] = fi;
 }
 
 // ---------------------------------------------------------------- KV handoff
@@ -217,6 +260,8 @@ __global__ void argmax_emit_kernel(const float* __restrict__ logits, int V, cons
 // vectors, 4 in flight per thread.
 __global__ void kv_copy_kernel(const uint4* __restrict__ src, const int* __restrict__ src_ids, uint4* __restrict__ dst,
                                const int* __restrict__ dst_ids, long long block_vec, long long chunk_vec) {
+    pdl_wait();
+    pdl_launch();
     const long long b = blockIdx.x;
     const long long s0 = static_cast<long long>(src_ids[b]) * block_vec + blockIdx.y * chunk_vec;
     const long long d0 = static_cast<long long>(dst_ids[b]) * block_vec + blockIdx.y * chunk_vec;
@@ -234,6 +279,8 @@ __global__ void kv_copy_kernel(const uint4* __restrict__ src, const int* __restr
 }
 
 __global__ void smid_probe_kernel(int* hits) {
+    pdl_wait();
+    pdl_launch();
     uint32_t sm;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
     if (threadIdx.x == 0) atomicAdd(&hits[sm], 1);
@@ -244,6 +291,8 @@ __global__ void smid_probe_kernel(int* hits) {
 }
 
 __global__ void copy_token_kernel(const int* src, long long si, int* dst, long long di, int* dst2, long long di2) {
+    pdl_wait();
+    pdl_launch();
     const int v = src[si];
     dst[di] = v;
     if (dst2) dst2[di2] = v;
@@ -265,51 +314,47 @@ int ck_init_uniform(void* out, long long n, unsigned long long seed, unsigned lo
     if (n <= 0) return 0;
     const float step = scale * (1.0f / 8388608.0f);  // exact: power-of-two scaling
     const int grid = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 32));
-    init_uniform_kernel<<<grid, 256, 0, S(stream)>>>(static_cast<__nv_bfloat16*>(out), n, seed, tensor_id, step,
+    return launch_pdl(init_uniform_kernel, dim3(grid), dim3(256), 0, S(stream), static_cast<__nv_bfloat16*>(out), n, seed, tensor_id, step,
                                                      offset);
-    return ret();
 }
 
 int ck_prompt_tokens(int* out, const int* req_id, const int* pos, int n, unsigned long long seed, int vocab,
                      void* stream) {
     if (n <= 0) return 0;
-    prompt_tokens_kernel<<<(n + 255) / 256, 256, 0, S(stream)>>>(out, req_id, pos, n, seed, vocab);
-    return ret();
+    return launch_pdl(prompt_tokens_kernel, dim3((n + 255) / 256), dim3(256), 0, S(stream), out, req_id, pos, n, seed, vocab);
 }
 
 int ck_rope_table(float* c, float* s, int max_pos, double theta, void* stream) {
     const int n = max_pos * 64;
-    rope_table_kernel<<<(n + 255) / 256, 256, 0, S(stream)>>>(c, s, max_pos, theta);
-    return ret();
+    return launch_pdl(rope_table_kernel, dim3((n + 255) / 256), dim3(256), 0, S(stream), c, s, max_pos, theta);
 }
 
 int ck_embed(float* x, const void* emb, const int* row_rid, const int* row_pos, const int* row_dec, const int* prompt,
              const long long* prompt_off, const int* last_tok, int M, int H, void* stream) {
     if (M <= 0) return 0;
     if (H % 8) return static_cast<int>(cudaErrorInvalidValue);
-    embed_kernel<<<M, 128, 0, S(stream)>>>(x, static_cast<const __nv_bfloat16*>(emb), row_rid, row_pos, row_dec,
+    return launch_pdl(embed_kernel, dim3(M), dim3(128), 0, S(stream), x, static_cast<const __nv_bfloat16*>(emb), row_rid, row_pos, row_dec,
                                           prompt, prompt_off, last_tok, H);
-    return ret();
 }
 
-int ck_rmsnorm(const float* x, const void* gamma, void* out, const int* rows, int R, int H, float eps, void* stream) {
+int ck_rmsnorm(const float* x, const void* gamma, void* out, const int* rows, int R, int H, float eps, float* zero,
+               int zero_cols, void* stream) {
     if (R <= 0) return 0;
-    if (H % 4) return static_cast<int>(cudaErrorInvalidValue);
+    if (H % 4 || (zero && zero_cols % 4)) return static_cast<int>(cudaErrorInvalidValue);
     const int threads = H >= 1024 ? 256 : 64;
-    rmsnorm_kernel<<<R, threads, 0, S(stream)>>>(x, static_cast<const __nv_bfloat16*>(gamma),
-                                                 static_cast<__nv_bfloat16*>(out), rows, H, eps);
-    return ret();
+    if (H / 4 > kRmsMaxVec * threads) return static_cast<int>(cudaErrorInvalidValue);
+    return launch_pdl(rmsnorm_kernel, dim3(R), dim3(threads), 0, S(stream), x, static_cast<const __nv_bfloat16*>(gamma),
+                                                 static_cast<__nv_bfloat16*>(out), rows, H, eps, zero, zero_cols);
 }
 
 int ck_qkv_rope_append(const float* qkv, const void* bias, void* q_out, void* kv_pool, const int* bt,
                        const int* row_bt, const int* row_pos, const float* cos_tab, const float* sin_tab, int M,
                        int nq, int nkv, int layer, int n_layers, void* stream) {
     if (M <= 0) return 0;
-    qkv_rope_append_kernel<<<M, 256, 0, S(stream)>>>(qkv, static_cast<const __nv_bfloat16*>(bias),
+    return launch_pdl(qkv_rope_append_kernel, dim3(M, nq + 2 * nkv), dim3(64), 0, S(stream), qkv, static_cast<const __nv_bfloat16*>(bias),
                                                      static_cast<__nv_bfloat16*>(q_out),
                                                      static_cast<__nv_bfloat16*>(kv_pool), bt, row_bt, row_pos,
                                                      cos_tab, sin_tab, nq, nkv, layer, n_layers);
-    return ret();
 }
 
 int ck_silu_mul(const float* gu, void* act, int M, int F, void* stream) {
@@ -317,15 +362,17 @@ int ck_silu_mul(const float* gu, void* act, int M, int F, void* stream) {
     if (F % 4) return static_cast<int>(cudaErrorInvalidValue);
     const long long n4 = static_cast<long long>(M) * F / 4;
     const int grid = static_cast<int>(std::min<long long>((n4 + 255) / 256, 148LL * 16));
-    silu_mul_kernel<<<grid, 256, 0, S(stream)>>>(gu, static_cast<__nv_bfloat16*>(act), n4);
-    return ret();
+    return launch_pdl(silu_mul_kernel, dim3(grid), dim3(256), 0, S(stream), gu, static_cast<__nv_bfloat16*>(act), n4);
 }
 
 int ck_argmax_emit(const float* logits, int R, int V, const int* rid, const long long* out_idx, int* last_tok,
-                   int* out_tok, void* stream) {
+                   int* out_tok, float* ws, int* tickets, void* stream) {
     if (R <= 0) return 0;
-    argmax_emit_kernel<<<R, 1024, 0, S(stream)>>>(logits, V, rid, out_idx, last_tok, out_tok);
-    return ret();
+    if (V % 4) return static_cast<int>(cudaErrorInvalidValue);
+    float* pv = ws;
+    int* pi = reinterpret_cast<int*>(ws + static_cast<size_t>(R) * kArgChunks);
+    return launch_pdl(argmax_emit_kernel, dim3(R, kArgChunks), dim3(256), 0, S(stream), logits, V, rid, out_idx,
+                      last_tok, out_tok, pv, pi, tickets);
 }
 
 int ck_kv_copy(const void* src_pool, const int* src_ids, void* dst_pool, const int* dst_ids, int n_blocks,
@@ -335,19 +382,16 @@ int ck_kv_copy(const void* src_pool, const int* src_ids, void* dst_pool, const i
     const long long block_vec = block_bytes / 16;
     const long long chunk_vec = std::min<long long>(block_vec, 65536 / 16);
     const dim3 grid(n_blocks, static_cast<unsigned>((block_vec + chunk_vec - 1) / chunk_vec));
-    kv_copy_kernel<<<grid, 256, 0, S(stream)>>>(static_cast<const uint4*>(src_pool), src_ids,
+    return launch_pdl(kv_copy_kernel, dim3(grid), dim3(256), 0, S(stream), static_cast<const uint4*>(src_pool), src_ids,
                                                 static_cast<uint4*>(dst_pool), dst_ids, block_vec, chunk_vec);
-    return ret();
 }
 
 int ck_smid_probe(int* hits, int n_ctas, void* stream) {
-    smid_probe_kernel<<<n_ctas, 64, 0, S(stream)>>>(hits);
-    return ret();
+    return launch_pdl(smid_probe_kernel, dim3(n_ctas), dim3(64), 0, S(stream), hits);
 }
 
 int ck_copy_token(const int* src, long long si, int* dst, long long di, int* dst2, long long di2, void* stream) {
-    copy_token_kernel<<<1, 1, 0, S(stream)>>>(src, si, dst, di, dst2, di2);
-    return ret();
+    return launch_pdl(copy_token_kernel, dim3(1), dim3(1), 0, S(stream), src, si, dst, di, dst2, di2);
 }
 
 }  // extern "C"

@@ -38,10 +38,15 @@ constexpr int kTileK = 64;   // K per stage: one 128-byte swizzle row of bf16
 
 struct GemmParams {
     void* out;
-    const __nv_bfloat16* bias;  // [N] or null, added once (by split 0)
+    const __nv_bfloat16* bias;  // [N] or null, added once (by the unit that starts at k = 0)
     int M, N, K, ldo;
     int m_tiles, splits, kb_total, kb_per_split, units;
     int epi;
+    // stream-K (red.add epilogue only): CTA c owns global K-block iterations
+    // [c * iters / grid, (c + 1) * iters / grid) of the (tile, k-block) space, so every
+    // CTA streams the same number of weight bytes regardless of tile count.
+    int stream_k;
+    long long iters;
 };
 
 template <int BN>
@@ -49,7 +54,10 @@ struct Cfg {
     static constexpr int kABytes = kTileN * kTileK * 2;
     static constexpr int kBBytes = BN * kTileK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStages = (196 * 1024) / kStageBytes > 8 ? 8 : (196 * 1024) / kStageBytes;
+    // As many stages as fit in ~220 KB: the weight stream is latency bound (Little's
+    // law: bytes in flight per SM / loaded HBM latency), so small token tiles get a
+    // deeper ring (BN=32: 11 x 20 KB).
+    static constexpr int kStages = (220 * 1024) / kStageBytes > 12 ? 12 : (220 * 1024) / kStageBytes;
     static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
     static constexpr int kSmem = kStages * kStageBytes + 1024 /*align slack*/ + 256 /*barriers*/;
 };
@@ -62,6 +70,29 @@ __device__ __forceinline__ void decode_unit(const GemmParams& p, int u, int& nt,
     const int s = r - mt * p.splits;
     kb0 = s * p.kb_per_split;
     kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+}
+
+// Work iteration shared by the producer, MMA and epilogue roles (all three walk the
+// identical unit sequence). `pos` starts at first_unit().
+__device__ __forceinline__ long long first_unit(const GemmParams& p) {
+    return p.stream_k ? (static_cast<long long>(blockIdx.x) * p.iters) / gridDim.x : blockIdx.x;
+}
+__device__ __forceinline__ bool next_unit(const GemmParams& p, long long& pos, int& nt, int& mt, int& kb0, int& kb1) {
+    if (p.stream_k) {
+        const long long end = (static_cast<long long>(blockIdx.x + 1) * p.iters) / gridDim.x;
+        if (pos >= end) return false;
+        const int tile = static_cast<int>(pos / p.kb_total);
+        kb0 = static_cast<int>(pos - static_cast<long long>(tile) * p.kb_total);
+        kb1 = static_cast<int>(min(static_cast<long long>(p.kb_total), kb0 + (end - pos)));
+        nt = tile / p.m_tiles;
+        mt = tile - nt * p.m_tiles;
+        pos += kb1 - kb0;
+        return true;
+    }
+    if (pos >= p.units) return false;
+    decode_unit(p, static_cast<int>(pos), nt, mt, kb0, kb1);
+    pos += gridDim.x;
+    return true;
 }
 
 template <int BN>
@@ -103,22 +134,53 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // Everything above overlaps the previous kernel under PDL. Only the activations X
+    // and the output depend on it: the producer streams the first stages' WEIGHT tiles
+    // before griddepcontrol.wait, the epilogue waits before its first store, and the
+    // MMA warp only consumes shared memory.
+    pdl_launch();
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
         if (lane == 0) {
             const uint64_t keep = policy_evict_last();    // activations: reused by every weight tile
             const uint64_t stream = policy_evict_first();  // weights: streamed once per launch
+            // (1) weight prefetch: the first kStages k-blocks of this CTA's work (their
+            //     slots are free at kernel start), before the dependency wait
+            int pre_nt[C::kStages], pre_mt[C::kStages], pre_kb[C::kStages];
+            int n_pre = 0;
+            {
+                long long pos = first_unit(p);
+                int nt, mt, kb0, kb1;
+                while (n_pre < C::kStages && next_unit(p, pos, nt, mt, kb0, kb1))
+                    for (int kb = kb0; kb < kb1 && n_pre < C::kStages; ++kb) {
+                        mbar_arrive_expect_tx(&full[n_pre], C::kStageBytes);
+                        tma_load_2d_hint(sA + n_pre * C::kABytes, &tmW, &full[n_pre], kb * kTileK, nt * kTileN,
+                                         stream);
+                        pre_nt[n_pre] = nt, pre_mt[n_pre] = mt, pre_kb[n_pre] = kb;
+                        ++n_pre;
+                    }
+            }
+            pdl_wait();
+            // (2) the activation tiles of the prefetched stages
+            for (int i = 0; i < n_pre; ++i)
+                tma_load_2d_hint(sB + i * C::kBBytes, &tmX, &full[i], pre_kb[i] * kTileK, pre_mt[i] * BN, keep);
+            (void)pre_nt;
+            // (3) steady state
             int stage = 0;
             uint32_t phase = 0;
-            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-                int nt, mt, kb0, kb1;
-                decode_unit(p, u, nt, mt, kb0, kb1);
-                for (int kb = kb0; kb < kb1; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-                    tma_load_2d_hint(sA + stage * C::kABytes, &tmW, &full[stage], kb * kTileK, nt * kTileN, stream);
-                    tma_load_2d_hint(sB + stage * C::kBBytes, &tmX, &full[stage], kb * kTileK, mt * BN, keep);
+            int issued = 0;
+            long long pos = first_unit(p);
+            int nt, mt, kb0, kb1;
+            while (next_unit(p, pos, nt, mt, kb0, kb1)) {
+                for (int kb = kb0; kb < kb1; ++kb, ++issued) {
+                    if (issued >= n_pre) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+                        tma_load_2d_hint(sA + stage * C::kABytes, &tmW, &full[stage], kb * kTileK, nt * kTileN,
+                                         stream);
+                        tma_load_2d_hint(sB + stage * C::kBBytes, &tmX, &full[stage], kb * kTileK, mt * BN, keep);
+                    }
                     if (++stage == C::kStages) {
                         stage = 0;
                         phase ^= 1;
@@ -134,9 +196,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-                int nt, mt, kb0, kb1;
-                decode_unit(p, u, nt, mt, kb0, kb1);
+            long long pos = first_unit(p);
+            int nt, mt, kb0, kb1;
+            while (next_unit(p, pos, nt, mt, kb0, kb1)) {
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
@@ -162,13 +224,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         // ------------------------------------------------------------ epilogue
+        pdl_wait();  // `out` (residual / zeroed accumulator) is produced upstream
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         const int row = q * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-            int nt, mt, kb0, kb1;
-            decode_unit(p, u, nt, mt, kb0, kb1);
+        long long pos = first_unit(p);
+        int nt, mt, kb0, kb1;
+        while (next_unit(p, pos, nt, mt, kb0, kb1)) {
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int n = nt * kTileN + row;
@@ -298,9 +361,9 @@ int launch(const CUtensorMap& mw, const CUtensorMap& mx, GemmParams p, int max_c
         if (e != cudaSuccess) return static_cast<int>(e);
         attr_set_mask |= 1u << dev;
     }
-    const int grid = std::min(p.units, max_ctas > 0 ? max_ctas : num_sms());
-    gemm_tc_kernel<BN><<<grid, kThreads, C::kSmem, s>>>(mw, mx, p);
-    return static_cast<int>(cudaGetLastError());
+    const long long work = p.stream_k ? p.iters : p.units;
+    const int grid = static_cast<int>(std::min<long long>(work, max_ctas > 0 ? max_ctas : num_sms()));
+    return launch_pdl(gemm_tc_kernel<BN>, dim3(grid), dim3(kThreads), C::kSmem, s, mw, mx, p);
 }
 
 }  // namespace
@@ -323,15 +386,15 @@ extern "C" int ck_gemm(const void* W, const void* X, void* out, const void* bias
     p.m_tiles = (M + BN - 1) / BN;
     p.kb_total = K / kTileK;
     const int tiles = (N / kTileN) * p.m_tiles;
-    const int sms = max_ctas > 0 ? max_ctas : num_sms();
-    if (splits <= 0) {
-        // Auto split-K (only legal when partial sums can be combined by red.add):
-        // aim for >= one unit per SM while keeping >= 4 K-blocks per unit.
+    p.stream_k = 0;
+    p.iters = static_cast<long long>(tiles) * p.kb_total;
+    if (splits <= 0 && epi == CK_EPI_RED_F32) {
+        // Partial sums meet through red.add, so balance K-block iterations exactly
+        // across the persistent grid (stream-K) instead of quantizing to whole tiles.
+        p.stream_k = 1;
         splits = 1;
-        if (epi == CK_EPI_RED_F32 && tiles < sms) {
-            splits = (sms + tiles - 1) / tiles;
-            splits = std::min(splits, std::max(1, p.kb_total / 4));
-        }
+    } else if (splits <= 0) {
+        splits = 1;
     }
     if (splits > 1 && epi != CK_EPI_RED_F32) return static_cast<int>(cudaErrorInvalidValue);
     splits = std::min(splits, p.kb_total);

@@ -1,0 +1,53 @@
+"""Host-side logic of bench.py: pair sharding (static rid % pairs rule)
+and the max-over-ranks timing reduction, exercised with a world-size-2 gloo group."""
+import os
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+
+sys.path.insert(0, ROOT)
+
+
+def test_pair_sharding_partitions_the_trace():
+    import bench
+    from paper_2509_17357_b200 import engine as E
+    t = E.synth_trace(40, 1014, 247, E.ALL_AT_ZERO, 0, 1)
+    for pairs in (1, 2, 4):
+        parts = [bench.pair_trace(t, p, pairs) for p in range(pairs)]
+        ids = np.sort(np.concatenate([x.ids for x in parts]))
+        assert np.array_equal(ids, np.sort(t.ids))
+        for p, x in enumerate(parts):
+            assert (x.ids % pairs == p).all()
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    local = torch.tensor([10.0 + rank * 5.0, 20.0 - rank])  # per-step ms on this rank
+    dist.all_reduce(local, op=dist.ReduceOp.MAX)
+    done = torch.tensor([100.0 if rank % 2 == 0 else 0.0])  # only pair drivers count requests
+    dist.all_reduce(done)
+    if rank == 0:
+        out.put((local.tolist(), done.item()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_max_over_ranks_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(60)
+    assert all(p.exitcode == 0 for p in procs)
+    times, done = q.get(timeout=5)
+    assert times == [15.0, 20.0] and done == 100.0

@@ -108,7 +108,7 @@ def test_wall_clock_tiny():
         assert len(r["tbt_samples_ms"]) == t.output_len[r["id"]] - 1
         assert r["ttft_ms"] > 0
     st = res.extra["stats"]
-    assert st["cpi"]["decode_attn"]["launches"] > 0 and st["cpi"]["gemm"]["launches"] > 0
+    assert st["cpi"]["decode_attn"]["launches"] > 0 and st["cpi"]["gemm_stream"]["launches"] > 0
     splits = [r["partial_prefill_len"] for r in rep["records"]]
     total, exact = check_tokens(t, res.extra["tokens"], [0, 3, 31, 63], splits=splits)
     assert exact >= 0.95 * total

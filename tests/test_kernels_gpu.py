@@ -72,10 +72,12 @@ def test_rmsnorm(L):
         g = (1 + 0.1 * torch.randn(H, device="cuda")).bfloat16()
         rows = torch.tensor([2, 0] + list(range(3, R + 1)), dtype=torch.int32, device="cuda")
         out = torch.empty(R, H, dtype=torch.bfloat16, device="cuda")
-        ok(L.ck_rmsnorm(p(x), p(g), p(out), p(rows), R, H, 1e-5, stream()))
+        zero = torch.randn(R + 1, 512, device="cuda")
+        ok(L.ck_rmsnorm(p(x), p(g), p(out), p(rows), R, H, 1e-5, p(zero), 512, stream()))
         xs = x[rows.long()]
         ref = xs * torch.rsqrt(xs.pow(2).mean(-1, keepdim=True) + 1e-5) * g.float()
         assert torch.allclose(out.float(), ref, rtol=8e-3, atol=8e-3)
+        assert zero[:R].abs().sum() == 0 and zero[R].abs().sum() > 0
 
 
 def make_pool(n_blocks, layers, nkv, fill=float("nan")):
@@ -158,7 +160,7 @@ def attn_ref(q, k, v, qpos, scale):
     return torch.einsum("hnt,thd->nhd", s.softmax(-1), vv)
 
 
-@pytest.mark.parametrize("nq,nkv", [(2, 1), (32, 8), (28, 4)])
+@pytest.mark.parametrize("nq,nkv", [(2, 1), (32, 8), (28, 4), (4, 2)])
 def test_attn_decode(L, nq, nkv):
     gen = torch.Generator(device="cuda").manual_seed(nq)
     layers, layer = 2, 1
@@ -184,10 +186,12 @@ def test_attn_decode(L, nq, nkv):
         t_len, t_off, t_item0, t_work = (torch.tensor(a, dtype=torch.int32, device="cuda")
                                          for a in (lens, offs, item0, work))
         ws = torch.empty(len(work) * nq * 130, device="cuda")
+        tickets = torch.zeros(S * nkv, dtype=torch.int32, device="cuda")
         out = torch.zeros(M, nq * 128, dtype=torch.bfloat16, device="cuda")
         scale = 1 / math.sqrt(128)
         ok(L.ck_attn_decode(p(q), p(pool), p(bt), p(rows), p(t_len), p(t_off), p(t_item0), p(t_work),
-                            len(work), S, bps, p(ws), p(out), nq, nkv, layer, layers, scale, stream()))
+                            len(work), S, bps, p(ws), p(tickets), p(out), nq, nkv, layer, layers, scale, stream()))
+        assert tickets.abs().sum() == 0  # self-resetting
         for s_i, ln in enumerate(lens):
             r = int(rows[s_i])
             ref = attn_ref(q[r].view(1, nq, 128), ks[s_i], vs[s_i], torch.tensor([ln - 1], device="cuda"), scale)
@@ -232,7 +236,10 @@ def test_silu_mul_and_argmax(L):
     out_idx = torch.tensor([10, 11, 12, 13, 14], dtype=torch.int64, device="cuda")
     last = torch.full((5,), -1, dtype=torch.int32, device="cuda")
     out_tok = torch.full((20,), -1, dtype=torch.int32, device="cuda")
-    ok(L.ck_argmax_emit(p(logits), R, V, p(rid), p(out_idx), p(last), p(out_tok), stream()))
+    ws = torch.empty(64 * R, device="cuda")
+    tickets = torch.zeros(R, dtype=torch.int32, device="cuda")
+    ok(L.ck_argmax_emit(p(logits), R, V, p(rid), p(out_idx), p(last), p(out_tok), p(ws), p(tickets), stream()))
+    assert tickets.abs().sum() == 0
     want = logits.argmax(-1).int()
     assert int(want[1]) == 77
     assert torch.equal(out_tok[10:15], want)

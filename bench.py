@@ -285,6 +285,7 @@ def run_ours(args, rank, world):
                    "parallelism": "replicas of worker pairs" if pairs > 1 else "co-located pair"},
         "gpu_launches": int(st.get("gpu_launches", 0)),
         "cpi_iterations": st["cpi_iterations"], "violations": len(rep["violations"]),
+        "iteration_shapes_count_ms": st.get("iteration_shapes"),
         "clocks": clocks, "e2e": e2e, "roofline": roof, "kernels": classes[:8],
     }
     if not args.no_cpu_baseline and world == 1:

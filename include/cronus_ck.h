@@ -64,10 +64,11 @@ int ck_rmsnorm(const float* x, const void* gamma, void* out_bf16, const int* row
 
 /* qkv fp32 [M, (nq + 2 nkv) * 128] (+ bias) -> RoPE(q) bf16 [M, nq*128] and
  * RoPE(k), v appended to the paged pool at each row's position.
- * bt: flat block table; row_bt[M] = offset of the row's sequence in bt. */
-int ck_qkv_rope_append(const float* qkv, const void* bias, void* q_out, void* kv_pool, const int* bt,
-                       const int* row_bt, const int* row_pos, const float* cos_tab, const float* sin_tab, int M,
-                       int nq, int nkv, int layer, int n_layers, void* stream);
+ * bt: flat block table; row_bt[M] = offset of the row's sequence in bt.
+ * zero_after: clear the qkv rows after reading them (red.add accumulator reuse). */
+int ck_qkv_rope_append(float* qkv, const void* bias, void* q_out, void* kv_pool, const int* bt, const int* row_bt,
+                       const int* row_pos, const float* cos_tab, const float* sin_tab, int M, int nq, int nkv,
+                       int layer, int n_layers, int zero_after, void* stream);
 
 /* Decode attention over the paged pool for S single-token sequences (split-KV).
  * seq_row[S] (row of q/out), seq_len[S] (keys), seq_bt[S] (offset into bt),
@@ -85,8 +86,9 @@ int ck_attn_decode(const void* q, const void* kv_pool, const int* bt, const int*
 int ck_attn_prefill(const void* q, const void* kv_pool, const int* bt, int q_row0, int q_len, int pos0, void* out,
                     int nq, int nkv, int layer, int n_layers, float scale, void* stream);
 
-/* act[m, i] = silu(gu[m, 2i]) * gu[m, 2i+1]  (gate/up rows interleaved), fp32 in. */
-int ck_silu_mul(const float* gu, void* act_bf16, int M, int F, void* stream);
+/* act[m, i] = silu(gu[m, 2i]) * gu[m, 2i+1]  (gate/up rows interleaved), fp32 in;
+ * zero_after: clear gu after reading it. */
+int ck_silu_mul(float* gu, void* act_bf16, int M, int F, int zero_after, void* stream);
 
 /* Greedy sampling: token = argmax_v logits[r, v] (lowest index on ties), then
  * last_tok[rid[r]] = token, out_tok[out_idx[r]] = token. ws: 64 * R floats of

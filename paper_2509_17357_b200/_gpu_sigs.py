@@ -16,10 +16,10 @@ CK = {
     "ck_rope_table": [V, V, I, D, V],
     "ck_embed": [V, V, V, V, V, V, V, V, I, I, V],
     "ck_rmsnorm": [V, V, V, V, I, I, F, V, I, V],
-    "ck_qkv_rope_append": [V, V, V, V, V, V, V, V, V, I, I, I, I, I, V],
+    "ck_qkv_rope_append": [V, V, V, V, V, V, V, V, V, I, I, I, I, I, I, V],
     "ck_attn_decode": [V, V, V, V, V, V, V, V, I, I, I, V, V, V, I, I, I, I, F, V],
     "ck_attn_prefill": [V, V, V, I, I, I, V, I, I, I, I, F, V],
-    "ck_silu_mul": [V, V, I, I, V],
+    "ck_silu_mul": [V, V, I, I, I, V],
     "ck_argmax_emit": [V, I, I, V, V, V, V, V, V, V],
     "ck_kv_copy": [V, V, V, V, I, LL, V],
     "ck_copy_token": [V, LL, V, LL, V, LL, V],

@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstring>
 #include <deque>
+#include <map>
 #include <memory>
 #include <sstream>
 #include <stdexcept>
@@ -724,8 +725,35 @@ RunReport GpuEngine::run(const ClusterConfig& cfg, const Trace& trace, const Gpu
     ex.upload();
     sched::SchedulerHooks hooks;
     hooks.executor = &ex;
+    std::vector<sched::IterRecord> iters;
+    hooks.iterations = &iters;
     RunReport rep = sched::run_scheduler(cfg, trace, opts, hooks);
-    if (opts.stats_json) *opts.stats_json = ex.stats();
+    if (opts.stats_json) {
+        // iteration-shape histogram: (chunk?, decoders bucket) -> count, wall ms
+        struct Bin {
+            long long n = 0;
+            double ms = 0;
+        };
+        std::map<std::string, Bin> bins;
+        for (const auto& it : iters) {
+            const int d = it.n_decode;
+            const char* db = d == 0 ? "0" : d <= 16 ? "1-16" : d <= 64 ? "17-64" : d <= 128 ? "65-128" : ">128";
+            Bin& b = bins[std::string(it.chunk_len > 0 ? "chunk+" : "decode ") + db];
+            b.n++;
+            b.ms += it.t_end - it.t_start;
+        }
+        std::string js = ex.stats();
+        std::ostringstream h;
+        h << ", \"iteration_shapes\": {";
+        bool first = true;
+        for (const auto& [k, b] : bins) {
+            h << (first ? "" : ", ") << "\"" << k << "\": [" << b.n << ", " << b.ms << "]";
+            first = false;
+        }
+        h << "}}";
+        js.pop_back();  // '}'
+        *opts.stats_json = js + h.str();
+    }
     return rep;
 }
 

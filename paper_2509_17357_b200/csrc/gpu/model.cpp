@@ -230,6 +230,8 @@ Worker::Worker(const Weights& w, int max_rows, int max_sample, int max_blocks_pe
     check_cuda(cudaMalloc(&q_, R * m_.q_n() * 2), "alloc q");
     check_cuda(cudaMalloc(&attn_, R * m_.q_n() * 2), "alloc attn");
     check_cuda(cudaMalloc(&gu_, R * 2 * m_.ffn * 4), "alloc gu");
+    check_cuda(cudaMemset(qkv_, 0, R * m_.qkv_n() * 4), "zero qkv");
+    check_cuda(cudaMemset(gu_, 0, R * 2 * m_.ffn * 4), "zero gu");
     check_cuda(cudaMalloc(&act_, R * m_.ffn * 2), "alloc act");
     check_cuda(cudaMalloc(&hs_, static_cast<size_t>(max_sample) * H * 2), "alloc hs");
     check_cuda(cudaMalloc(&logits_, static_cast<size_t>(max_sample) * m_.vocab * 4), "alloc logits");
@@ -375,6 +377,16 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
     for (int len : b.d_len) dec_keys += len;
     const double kv_tok_layer = 2.0 * m.n_kv_heads * m.head_dim * 2;  // bytes per token per layer (K+V)
 
+    if (small) {  // red.add accumulators must start from zero
+        if (qkv_dirty_rows_ > 0)
+            check_cuda(cudaMemsetAsync(qkv_, 0, static_cast<size_t>(qkv_dirty_rows_) * Q * 4, stream_), "memset qkv");
+        if (gu_dirty_rows_ > 0)
+            check_cuda(cudaMemsetAsync(gu_, 0, static_cast<size_t>(gu_dirty_rows_) * 2 * F * 4, stream_), "memset gu");
+        qkv_dirty_rows_ = gu_dirty_rows_ = 0;
+    } else {
+        qkv_dirty_rows_ = std::max(qkv_dirty_rows_, M);
+        gu_dirty_rows_ = std::max(gu_dirty_rows_, M);
+    }
     cudaEvent_t a = nullptr;
     mark(a);
     check_ck(ck_embed(x_, w_.embed, row_rid, row_pos, row_dec, prompt, prompt_off, last_tok, M, H, stream_), "embed");
@@ -385,14 +397,13 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         mark(a);
         // weight-streaming regime (M <= 128): qkv accumulates with red.add (stream-K GEMM),
         // so the norm kernel clears it; tensor regime: plain fp32 tile stores
-        check_ck(ck_rmsnorm(x_, L.attn_norm, h_, nullptr, M, H, m.rms_eps, small ? qkv_ : nullptr, Q, stream_),
-                 "rmsnorm");
+        check_ck(ck_rmsnorm(x_, L.attn_norm, h_, nullptr, M, H, m.rms_eps, nullptr, 0, stream_), "rmsnorm");
         ++launches;
         done(a, &stat_other, 0, 0);
         gemm(L.wqkv, h_, qkv_, L.bqkv, M, Q, H, small ? CK_EPI_RED_F32 : CK_EPI_F32, small ? 0 : 1);
         mark(a);
         check_ck(ck_qkv_rope_append(qkv_, nullptr, q_, pool.base, bt, row_bt, row_pos, w_.cos_tab, w_.sin_tab, M,
-                                    m.n_heads, m.n_kv_heads, l, m.layers, stream_),
+                                    m.n_heads, m.n_kv_heads, l, m.layers, small ? 1 : 0, stream_),
                  "qkv_rope_append");
         ++launches;
         done(a, &stat_other, 0, 0);
@@ -416,13 +427,12 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         }
         gemm(L.wo, attn_, x_, nullptr, M, H, NQ, CK_EPI_RED_F32, 0);
         mark(a);
-        check_ck(ck_rmsnorm(x_, L.ffn_norm, h_, nullptr, M, H, m.rms_eps, small ? gu_ : nullptr, 2 * F, stream_),
-                 "rmsnorm");
+        check_ck(ck_rmsnorm(x_, L.ffn_norm, h_, nullptr, M, H, m.rms_eps, nullptr, 0, stream_), "rmsnorm");
         ++launches;
         done(a, &stat_other, 0, 0);
         gemm(L.wgu, h_, gu_, nullptr, M, 2 * F, H, small ? CK_EPI_RED_F32 : CK_EPI_F32, small ? 0 : 1);
         mark(a);
-        check_ck(ck_silu_mul(gu_, act_, M, F, stream_), "silu_mul");
+        check_ck(ck_silu_mul(gu_, act_, M, F, small ? 1 : 0, stream_), "silu_mul");
         ++launches;
         done(a, &stat_other, 0, 0);
         gemm(L.wd, act_, x_, nullptr, M, H, F, CK_EPI_RED_F32, 0);

@@ -171,6 +171,10 @@ class Worker {
     float* attn_ws_ = nullptr;
     long long attn_ws_floats_ = 0;
     int* attn_tickets_ = nullptr;  // split-merge tickets, [max_rows * n_kv_heads], self-resetting
+    // Leading rows of the qkv / gu fp32 accumulators that may be non-zero (left by a
+    // tensor-regime pass, which stores instead of red.adding); the weight-streaming
+    // regime needs them zero and its consumers re-zero what they read.
+    int qkv_dirty_rows_ = 0, gu_dirty_rows_ = 0;
     float* arg_ws_ = nullptr;      // argmax slice winners [max_sample * 64]
     int* arg_tickets_ = nullptr;   // [max_sample], self-resetting
     int* meta_dev_ = nullptr;

@@ -132,20 +132,28 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16*
 // grid (row, head): 64 threads per head. Rotary heads (q and k): thread i rotates the
 // pair (i, i + 64) (rotate-half RoPE); v heads: thread i moves dims (2i, 2i + 1).
 // q goes to q_out (bf16); k and v go to the row's slot of its paged KV block.
-__global__ void qkv_rope_append_kernel(const float* __restrict__ qkv, const __nv_bfloat16* __restrict__ bias,
+constexpr int kQkvHeadsPerCta = 4;
+
+__global__ void qkv_rope_append_kernel(float* __restrict__ qkv, const __nv_bfloat16* __restrict__ bias,
                                        __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ pool,
                                        const int* __restrict__ bt, const int* __restrict__ row_bt,
                                        const int* __restrict__ row_pos, const float* __restrict__ cos_tab,
-                                       const float* __restrict__ sin_tab, int nq, int nkv, int layer, int n_layers) {
+                                       const float* __restrict__ sin_tab, int nq, int nkv, int layer, int n_layers,
+                                       int zero_after) {
     pdl_wait();
     pdl_launch();
-    const int m = blockIdx.x, h = blockIdx.y, i = threadIdx.x;
+    const int m = blockIdx.x, h = blockIdx.y * kQkvHeadsPerCta + (threadIdx.x >> 6), i = threadIdx.x & 63;
+    if (h >= nq + 2 * nkv) return;
     const int pos = row_pos[m];
-    const float* row = qkv + static_cast<size_t>(m) * (nq + 2 * nkv) * 128 + h * 128;
+    float* row = qkv + static_cast<size_t>(m) * (nq + 2 * nkv) * 128 + h * 128;
     const __nv_bfloat16* brow = bias ? bias + h * 128 : nullptr;
     const size_t head_stride = 16 * 128;
     if (h < nq + nkv) {
         float a = row[i], b = row[i + 64];
+        if (zero_after) {  // leave the red.add accumulator clean for the next layer
+            row[i] = 0.f;
+            row[i + 64] = 0.f;
+        }
         if (brow) {
             a += bf2f(brow[i]);
             b += bf2f(brow[i + 64]);
@@ -164,6 +172,7 @@ __global__ void qkv_rope_append_kernel(const float* __restrict__ qkv, const __nv
         dst[i + 64] = f2bf(rb);
     } else {
         float2 v = *reinterpret_cast<const float2*>(row + 2 * i);
+        if (zero_after) *reinterpret_cast<float2*>(row + 2 * i) = make_float2(0.f, 0.f);
         if (brow) {
             v.x += bf2f(brow[2 * i]);
             v.y += bf2f(brow[2 * i + 1]);
@@ -176,7 +185,8 @@ __global__ void qkv_rope_append_kernel(const float* __restrict__ qkv, const __nv
 }
 
 // ---------------------------------------------------------------- SiLU * up
-__global__ void silu_mul_kernel(const float* __restrict__ gu, __nv_bfloat16* __restrict__ act, long long n_pairs4) {
+__global__ void silu_mul_kernel(float* __restrict__ gu, __nv_bfloat16* __restrict__ act, long long n_pairs4,
+                                int zero_after) {
     pdl_wait();
     pdl_launch();
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n_pairs4;
@@ -184,6 +194,10 @@ __global__ void silu_mul_kernel(const float* __restrict__ gu, __nv_bfloat16* __r
         // 4 (gate, up) pairs = 8 floats -> 4 bf16
         const float4 a = reinterpret_cast<const float4*>(gu)[2 * i];
         const float4 b = reinterpret_cast<const float4*>(gu)[2 * i + 1];
+        if (zero_after) {  // leave the red.add accumulator clean for the next layer
+            reinterpret_cast<float4*>(gu)[2 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            reinterpret_cast<float4*>(gu)[2 * i + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
         const float s0 = a.x / (1.f + __expf(-a.x)) * a.y;
         const float s1 = a.z / (1.f + __expf(-a.z)) * a.w;
         const float s2 = b.x / (1.f + __expf(-b.x)) * b.y;
@@ -347,22 +361,24 @@ int ck_rmsnorm(const float* x, const void* gamma, void* out, const int* rows, in
                                                  static_cast<__nv_bfloat16*>(out), rows, H, eps, zero, zero_cols);
 }
 
-int ck_qkv_rope_append(const float* qkv, const void* bias, void* q_out, void* kv_pool, const int* bt,
-                       const int* row_bt, const int* row_pos, const float* cos_tab, const float* sin_tab, int M,
-                       int nq, int nkv, int layer, int n_layers, void* stream) {
+int ck_qkv_rope_append(float* qkv, const void* bias, void* q_out, void* kv_pool, const int* bt, const int* row_bt,
+                       const int* row_pos, const float* cos_tab, const float* sin_tab, int M, int nq, int nkv,
+                       int layer, int n_layers, int zero_after, void* stream) {
     if (M <= 0) return 0;
-    return launch_pdl(qkv_rope_append_kernel, dim3(M, nq + 2 * nkv), dim3(64), 0, S(stream), qkv, static_cast<const __nv_bfloat16*>(bias),
+    const int nh = nq + 2 * nkv;
+    return launch_pdl(qkv_rope_append_kernel, dim3(M, (nh + kQkvHeadsPerCta - 1) / kQkvHeadsPerCta),
+                      dim3(64 * kQkvHeadsPerCta), 0, S(stream), qkv, static_cast<const __nv_bfloat16*>(bias),
                                                      static_cast<__nv_bfloat16*>(q_out),
                                                      static_cast<__nv_bfloat16*>(kv_pool), bt, row_bt, row_pos,
-                                                     cos_tab, sin_tab, nq, nkv, layer, n_layers);
+                                                     cos_tab, sin_tab, nq, nkv, layer, n_layers, zero_after);
 }
 
-int ck_silu_mul(const float* gu, void* act, int M, int F, void* stream) {
+int ck_silu_mul(float* gu, void* act, int M, int F, int zero_after, void* stream) {
     if (M <= 0) return 0;
     if (F % 4) return static_cast<int>(cudaErrorInvalidValue);
     const long long n4 = static_cast<long long>(M) * F / 4;
     const int grid = static_cast<int>(std::min<long long>((n4 + 255) / 256, 148LL * 16));
-    return launch_pdl(silu_mul_kernel, dim3(grid), dim3(256), 0, S(stream), gu, static_cast<__nv_bfloat16*>(act), n4);
+    return launch_pdl(silu_mul_kernel, dim3(grid), dim3(256), 0, S(stream), gu, static_cast<__nv_bfloat16*>(act), n4, zero_after);
 }
 
 int ck_argmax_emit(const float* logits, int R, int V, const int* rid, const long long* out_idx, int* last_tok,

@@ -256,10 +256,43 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int j = 0; j < 16; ++j)
                         if (j < mlim) o[static_cast<size_t>(j) * p.ldo] = __uint_as_float(v[j]) + bias;
                 } else {
-                    float* o = static_cast<float*>(p.out) + static_cast<size_t>(m_base + c) * p.ldo + n;
+                    // 4x4 register transposes inside each quad of lanes: lane 4g+t ends up
+                    // holding rows n0+4g..+3 of column 4b+t, so one 16-byte vector
+                    // reduction replaces four scalar atomics.
+                    float a[16];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        if (j < mlim) red_add_f32(o + static_cast<size_t>(j) * p.ldo, __uint_as_float(v[j]) + bias);
+                    for (int j = 0; j < 16; ++j) a[j] = __uint_as_float(v[j]) + bias;
+                    const int t = lane & 3;
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        float* r = a + 4 * b;
+                        float x0 = __shfl_xor_sync(0xffffffffu, (t & 1) ? r[0] : r[1], 1);
+                        float x1 = __shfl_xor_sync(0xffffffffu, (t & 1) ? r[2] : r[3], 1);
+                        if (t & 1) {
+                            r[0] = x0;
+                            r[2] = x1;
+                        } else {
+                            r[1] = x0;
+                            r[3] = x1;
+                        }
+                        x0 = __shfl_xor_sync(0xffffffffu, (t & 2) ? r[0] : r[2], 2);
+                        x1 = __shfl_xor_sync(0xffffffffu, (t & 2) ? r[1] : r[3], 2);
+                        if (t & 2) {
+                            r[0] = x0;
+                            r[1] = x1;
+                        } else {
+                            r[2] = x0;
+                            r[3] = x1;
+                        }
+                    }
+                    const int n4 = nt * kTileN + q * 32 + (lane & ~3);
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const int j = 4 * b + t;
+                        if (j < mlim)
+                            red_add_v4_f32(static_cast<float*>(p.out) + static_cast<size_t>(m_base + c + j) * p.ldo + n4,
+                                           a[4 * b], a[4 * b + 1], a[4 * b + 2], a[4 * b + 3]);
+                    }
                 }
             }
             tc_fence_before();

@@ -113,9 +113,11 @@ def test_qkv_rope_append(L, nq, nkv, bias):
     qout = torch.empty(M, nq * 128, dtype=torch.bfloat16, device="cuda")
     # use distinct positions to avoid two rows writing the same slot
     pos = torch.randperm(1000, device="cuda")[:M].int()
+    qkv_in = qkv.clone()
     ok(L.ck_qkv_rope_append(p(qkv), p(b), p(qout), p(pool), p(bt), p(row_bt), p(pos), p(c), p(s), M, nq, nkv, layer,
-                            layers, stream()))
-    x = qkv + (b.float() if bias else 0)
+                            layers, 1, stream()))
+    assert qkv.abs().sum() == 0  # zero_after
+    x = qkv_in + (b.float() if bias else 0)
     q = rope_ref(x[:, :nq * 128].view(M, nq, 128), pos, theta)
     k = rope_ref(x[:, nq * 128:(nq + nkv) * 128].view(M, nkv, 128), pos, theta)
     v = x[:, (nq + nkv) * 128:].view(M, nkv, 128)
@@ -224,8 +226,10 @@ def test_silu_mul_and_argmax(L):
     M, F = 9, 1024
     gu = torch.randn(M, 2 * F, device="cuda") * 3
     act = torch.empty(M, F, dtype=torch.bfloat16, device="cuda")
-    ok(L.ck_silu_mul(p(gu), p(act), M, F, stream()))
-    g, u = gu[:, 0::2], gu[:, 1::2]
+    gu_in = gu.clone()
+    ok(L.ck_silu_mul(p(gu), p(act), M, F, 1, stream()))
+    assert gu.abs().sum() == 0
+    g, u = gu_in[:, 0::2], gu_in[:, 1::2]
     assert torch.allclose(act.float(), torch.nn.functional.silu(g) * u, rtol=1e-2, atol=1e-2)
 
     R, V = 5, 128256

@@ -86,6 +86,14 @@ int ck_attn_decode(const void* q, const void* kv_pool, const int* bt, const int*
 int ck_attn_prefill(const void* q, const void* kv_pool, const int* bt, int q_row0, int q_len, int pos0, void* out,
                     int nq, int nkv, int layer, int n_layers, float scale, void* stream);
 
+/* Same op on the 5th-gen tensor cores (tcgen05 + TMEM + TMA): 128 query rows x 1 head
+ * per CTA. q_rows_total: rows of the q buffer (TMA bound); pool_blocks: blocks in the
+ * pool. Stale slots of a sequence's last block are read (and masked): the pool must hold
+ * finite values (the engine zero-fills it at allocation). */
+int ck_attn_prefill_tc(const void* q, int q_rows_total, const void* kv_pool, long long pool_blocks, const int* bt,
+                       int q_row0, int q_len, int pos0, void* out, int nq, int nkv, int layer, int n_layers,
+                       float scale, void* stream);
+
 /* act[m, i] = silu(gu[m, 2i]) * gu[m, 2i+1]  (gate/up rows interleaved), fp32 in;
  * zero_after: clear gu after reading it. */
 int ck_silu_mul(float* gu, void* act_bf16, int M, int F, int zero_after, void* stream);

@@ -125,6 +125,9 @@ Weights::~Weights() {
 KvPool::KvPool(int dev, long long n_blocks, long long bb) : device(dev), blocks(n_blocks), block_bytes(bb) {
     check_cuda(cudaSetDevice(dev), "cudaSetDevice");
     check_cuda(cudaMalloc(&base, static_cast<size_t>(n_blocks) * bb), "cudaMalloc(kv pool)");
+    // Never-written slots must hold finite values: the tensor-core attention reads whole
+    // 16-token blocks and masks the tail (0 * NaN would poison the P.V product).
+    check_cuda(cudaMemset(base, 0, static_cast<size_t>(n_blocks) * bb), "zero kv pool");
 }
 
 KvPool::~KvPool() {
@@ -418,9 +421,9 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         }
         if (b.p_len > 0) {
             mark(a);
-            check_ck(ck_attn_prefill(q_, pool.base, bt + b.p_bt, b.p_row0, b.p_len, b.p_pos0, attn_, m.n_heads,
-                                     m.n_kv_heads, l, m.layers, scale, stream_),
-                     "attn_prefill");
+            check_ck(ck_attn_prefill_tc(q_, max_rows_, pool.base, pool.blocks, bt + b.p_bt, b.p_row0, b.p_len,
+                                        b.p_pos0, attn_, m.n_heads, m.n_kv_heads, l, m.layers, scale, stream_),
+                     "attn_prefill_tc");
             ++launches;
             const double keys = static_cast<double>(b.p_len) * b.p_pos0 + 0.5 * b.p_len * (b.p_len + 1.0);
             done(a, &stat_prefill_attn, (b.p_pos0 + b.p_len) * kv_tok_layer, 4.0 * m.n_heads * m.head_dim * keys);

@@ -1,0 +1,403 @@
+// Causal prefill / chunk attention on the 5th-gen tensor cores (tcgen05 + TMEM + TMA).
+//
+// One CTA = 128 query rows of one head. Per 128-key tile j of the paged KV:
+//   S_j  = Q K_j^T              tcgen05.mma M=128 (queries) N=128 (keys) K=128 (dims) -> TMEM
+//   P_j  = exp2(S_j * scale - m) softmax warps: TMEM -> registers (one query row per
+//                               thread: row max / sum need no shuffles) -> bf16 P in smem
+//   O   += P_j V_j              tcgen05.mma M=128 N=128 (dims) K=128 (keys), V consumed
+//                               MN-major straight from its TMA tile -> TMEM accumulator
+// O is rescaled lazily (only when a row max grows by more than 2^8), so the common
+// case never touches the accumulator between MMAs.
+//
+// Shared-memory operands are in the canonical 128-byte-swizzled layouts TMA produces
+// (Swizzle<3,4,3>): K-major for Q, K and P (rows of 64 bf16), MN-major for V (64-dim
+// rows per key, 8-key atoms at SBO = 1 KiB, the second 64-dim half at LBO = 16 KiB).
+// K/V tiles are gathered from the paged pool with one 16-row TMA box per 16-token
+// block and 64-dim half (pool viewed as a [rows][128] bf16 matrix).
+//
+// Warp roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer (+ TMEM owner),
+// warps 2..5 softmax / correction / epilogue (TMEM lane quarter = warp % 4).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <cstdio>
+#include <string>
+#include <unordered_map>
+
+#include "common.cuh"
+#include "cronus_ck.h"
+
+namespace {
+
+using namespace ck;
+
+constexpr int kQ = 128;       // query rows per CTA
+constexpr int kKT = 128;      // keys per tile
+constexpr int kHalf = 16384;  // one 128-row x 64-col bf16 swizzled region
+constexpr int kTileBytes = 2 * kHalf;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+// smem map (offsets from a 1024-aligned base)
+constexpr int kOffQ = 0;
+constexpr int kOffK = kOffQ + kTileBytes;          // 2 stages
+constexpr int kOffV = kOffK + 2 * kTileBytes;      // 2 stages
+constexpr int kOffP = kOffV + 2 * kTileBytes;      // 1 buffer
+constexpr int kOffBar = kOffP + kTileBytes;
+constexpr int kSmemBytes = kOffBar + 256 + 1024;
+
+struct AttnParams {
+    int q_row0, q_len, pos0;
+    int nq, nkv, layer, n_layers;
+    int row_stride_blk;  // pool rows per block = n_layers * 2 * nkv * 16
+    float scale_log2;
+    __nv_bfloat16* out;
+    const int* table;
+};
+
+__device__ __forceinline__ uint64_t sdesc_mn_sw128(uint32_t addr) {
+    // MN-major, 128B swizzle: LBO = 16 KiB between the two 64-element MN halves,
+    // SBO = 1 KiB between 8-row (K) groups.
+    return (static_cast<uint64_t>((addr >> 4) & 0x3FFFu)) | (static_cast<uint64_t>(kHalf >> 4) << 16) |
+           (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+           (static_cast<uint64_t>(2) << 61);
+}
+
+__host__ __device__ constexpr uint32_t idesc_attn(bool b_mn_major) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) | (static_cast<uint32_t>(128 >> 3) << 17) |
+           (static_cast<uint32_t>(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%"
+        "19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__global__ void __launch_bounds__(192, 1)
+    attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
+                           AttnParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + kOffBar);
+    uint64_t* q_full = bar + 0;
+    uint64_t* kv_full = bar + 1;   // [2]
+    uint64_t* kv_empty = bar + 3;  // [2]
+    uint64_t* s_full = bar + 5;    // [2]
+    uint64_t* s_empty = bar + 7;   // [2]
+    uint64_t* p_full = bar + 9;
+    uint64_t* pv_done = bar + 10;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+
+    const int warp = warp_id(), lane = lane_id();
+    const int qt = blockIdx.x, h = blockIdx.y;
+    const int kvh = h / (p.nq / p.nkv);
+    const int r_begin = qt * kQ;
+    const int r_end = min(p.q_len, r_begin + kQ);
+    const int n_keys = p.pos0 + r_end;  // causal extent of this tile's last row
+    const int n_kt = (n_keys + kKT - 1) / kKT;
+
+    if (warp == 1) {
+        tmem_alloc(tmem_slot, 512);  // S[2] at cols 0 / 128, O at 256
+        tmem_relinquish();
+    } else if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmQ);
+        tma_prefetch_desc(&tmKV);
+        mbar_init(q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_empty[i], 4);
+        }
+        mbar_init(p_full, 4);
+        mbar_init(pv_done, 1);
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_wait();
+    pdl_launch();
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            const uint64_t keep = policy_evict_last();
+            mbar_arrive_expect_tx(q_full, kTileBytes);
+            const int qcol = h * 128;
+            const int qrow = p.q_row0 + r_begin;
+            tma_load_2d(sm + kOffQ, &tmQ, q_full, qcol, qrow);
+            tma_load_2d(sm + kOffQ + kHalf, &tmQ, q_full, qcol + 64, qrow);
+            const int n_tab = (n_keys + 15) / 16;
+            for (int j = 0; j < n_kt; ++j) {
+                const int s = j & 1;
+                mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(&kv_full[s], 2 * kTileBytes);
+                uint8_t* K = sm + kOffK + s * kTileBytes;
+                uint8_t* V = sm + kOffV + s * kTileBytes;
+                for (int b = 0; b < kKT / 16; ++b) {
+                    const int tb = j * (kKT / 16) + b;
+                    const int blk = p.table[tb < n_tab ? tb : 0];  // past the end: any finite block (masked)
+                    const int row_k = ((blk * p.n_layers + p.layer) * 2 + 0) * p.nkv * 16 + kvh * 16;
+                    const int row_v = row_k + p.nkv * 16;
+                    tma_load_2d_hint(K + b * 2048, &tmKV, &kv_full[s], 0, row_k, keep);
+                    tma_load_2d_hint(K + kHalf + b * 2048, &tmKV, &kv_full[s], 64, row_k, keep);
+                    tma_load_2d_hint(V + b * 2048, &tmKV, &kv_full[s], 0, row_v, keep);
+                    tma_load_2d_hint(V + kHalf + b * 2048, &tmKV, &kv_full[s], 64, row_v, keep);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t id_s = idesc_attn(false), id_o = idesc_attn(true);
+            const uint32_t q0 = smem_u32(sm + kOffQ);
+            const uint32_t pbase = smem_u32(sm + kOffP);
+            mbar_wait(q_full, 0);
+            auto issue_s = [&](int j) {
+                const int s = j & 1;
+                mbar_wait(&kv_full[s], (j >> 1) & 1);
+                mbar_wait(&s_empty[s], ((j >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t k0 = smem_u32(sm + kOffK + s * kTileBytes);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {  // 8 x K=16 over the 128 head dims
+                    const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
+                    tc_mma_bf16(tmem + s * 128, sdesc_sw128(q0 + off), sdesc_sw128(k0 + off), id_s, kk > 0);
+                }
+                tc_commit(&s_full[s]);
+            };
+            auto issue_pv = [&](int j) {
+                const int s = j & 1;
+                mbar_wait(p_full, j & 1);
+                tc_fence_after();
+                const uint32_t v0 = smem_u32(sm + kOffV + s * kTileBytes);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {  // 8 x K=16 over the 128 keys
+                    const uint32_t aoff = (kk >> 2) * kHalf + (kk & 3) * 32;
+                    tc_mma_bf16(tmem + 256, sdesc_sw128(pbase + aoff), sdesc_mn_sw128(v0 + kk * 2048), id_o,
+                                (j > 0 || kk > 0) ? 1u : 0u);
+                }
+                tc_commit(&kv_empty[s]);  // K/V stage reusable
+                tc_commit(pv_done);       // P buffer reusable / O stable
+            };
+            issue_s(0);
+            for (int j = 0; j < n_kt; ++j) {
+                if (j + 1 < n_kt) issue_s(j + 1);
+                issue_pv(j);
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ softmax / epilogue
+        const int qw = warp & 3;
+        const int row = qw * 32 + lane;       // query row within the tile = TMEM lane
+        const int qpos = p.pos0 + r_begin + row;
+        const uint32_t lane_base = static_cast<uint32_t>(qw * 32) << 16;
+        float m_ref = -INFINITY, l_sum = 0.f;
+        uint8_t* P = sm + kOffP;
+        for (int j = 0; j < n_kt; ++j) {
+            const int s = j & 1;
+            mbar_wait(&s_full[s], (j >> 1) & 1);
+            tc_fence_after();
+            uint32_t sv[4][32];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld32(tmem + lane_base + s * 128 + c * 32, sv[c]);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[s]);
+            // scale + causal mask (keys past this row's position, or past the sequence)
+            const int key0 = j * kKT;
+            float mx = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const int key = key0 + c * 32 + e;
+                    float v = __uint_as_float(sv[c][e]) * p.scale_log2;
+                    if (key > qpos) v = -INFINITY;
+                    sv[c][e] = __float_as_uint(v);
+                    mx = fmaxf(mx, v);
+                }
+            // previous PV must be done before P is overwritten (and before any O rescale)
+            if (j > 0) mbar_wait(pv_done, (j - 1) & 1);
+            // The decision is warp-uniform: tcgen05.ld/st are warp-collective. Lanes that
+            // did not need it rescale exactly (possibly by 1), which is always valid.
+            const bool need = __any_sync(0xffffffffu, mx > m_ref + kRescaleThreshold || m_ref == -INFINITY);
+            if (need) {
+                const float m_new = fmaxf(m_ref, mx);
+                const float corr = m_ref == -INFINITY ? 0.f : exp2f(m_ref - m_new);
+                l_sum *= corr;
+                m_ref = m_new;
+                if (j > 0) {  // rescale this warp's rows of the O accumulator in TMEM
+                    tc_fence_after();
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        uint32_t o[32];
+                        tmem_ld32(tmem + lane_base + 256 + c * 32, o);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+                        tmem_st32(tmem + lane_base + 256 + c * 32, o);
+                    }
+                    tmem_st_wait();
+                }
+            }
+            // P = exp2(S - m_ref) -> bf16, written in the K-major 128B-swizzled layout
+            float rs = 0.f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {  // 8 keys = one 16-byte chunk
+                    float pv[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        pv[e] = exp2f(__uint_as_float(sv[c][g * 8 + e]) - m_ref);
+                        rs += pv[e];
+                    }
+                    const int key = c * 32 + g * 8;  // within the tile
+                    const int half = key >> 6, chunk = (key & 63) >> 3;
+                    uint4 w;
+                    w.x = pack_bf16x2(pv[0], pv[1]);
+                    w.y = pack_bf16x2(pv[2], pv[3]);
+                    w.z = pack_bf16x2(pv[4], pv[5]);
+                    w.w = pack_bf16x2(pv[6], pv[7]);
+                    *reinterpret_cast<uint4*>(P + half * kHalf + row * 128 + ((chunk ^ (row & 7)) << 4)) = w;
+                }
+            }
+            l_sum += rs;
+            fence_async_smem();  // generic-proxy P writes -> visible to the tensor core
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(p_full);
+        }
+        // ---- epilogue: O / l -> bf16 rows
+        mbar_wait(pv_done, (n_kt - 1) & 1);
+        tc_fence_after();
+        const int grow = r_begin + row;
+        const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            tmem_ld32(tmem + lane_base + 256 + c * 32, o);
+            tmem_ld_wait();
+            if (grow < p.q_len) {
+                __nv_bfloat16* dst =
+                    p.out + static_cast<size_t>(p.q_row0 + grow) * p.nq * 128 + h * 128 + c * 32;
+#pragma unroll
+                for (int e = 0; e < 32; e += 8) {
+                    uint4 w;
+                    w.x = pack_bf16x2(__uint_as_float(o[e]) * inv, __uint_as_float(o[e + 1]) * inv);
+                    w.y = pack_bf16x2(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
+                    w.z = pack_bf16x2(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
+                    w.w = pack_bf16x2(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
+                    *reinterpret_cast<uint4*>(dst + e) = w;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// ------------------------------------------------------------------ host
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int make_map(const void* ptr, unsigned long long rows, unsigned long long cols, unsigned box_rows, CUtensorMap* m) {
+    static std::mutex mu;
+    static std::unordered_map<std::string, CUtensorMap> cache;
+    char key[96];
+    std::snprintf(key, sizeof key, "%p/%llu/%llu/%u", ptr, rows, cols, box_rows);
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) {
+            *m = it->second;
+            return 0;
+        }
+    }
+    static EncodeFn enc = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
+        return reinterpret_cast<EncodeFn>(f);
+    }();
+    if (!enc) return static_cast<int>(cudaErrorNotSupported);
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {64, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return static_cast<int>(cudaErrorInvalidValue);
+    std::lock_guard<std::mutex> g(mu);
+    if (cache.size() > 4096) cache.clear();
+    cache.emplace(key, *m);
+    return 0;
+}
+
+}  // namespace
+
+extern "C" int ck_attn_prefill_tc(const void* q, int q_rows_total, const void* kv_pool, long long pool_blocks,
+                                  const int* bt, int q_row0, int q_len, int pos0, void* out, int nq, int nkv, int layer,
+                                  int n_layers, float scale, void* stream) {
+    if (q_len <= 0) return 0;
+    CUtensorMap mq, mkv;
+    int rc = make_map(q, static_cast<unsigned long long>(q_rows_total), static_cast<unsigned long long>(nq) * 128,
+                      kQ, &mq);
+    if (rc) return rc;
+    const unsigned long long pool_rows = static_cast<unsigned long long>(pool_blocks) * n_layers * 2 * nkv * 16;
+    rc = make_map(kv_pool, pool_rows, 128, 16, &mkv);
+    if (rc) return rc;
+    static unsigned mask = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(mask & (1u << dev))) {
+        cudaError_t e =
+            cudaFuncSetAttribute(attn_prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        if (e != cudaSuccess) return static_cast<int>(e);
+        mask |= 1u << dev;
+    }
+    AttnParams prm;
+    prm.q_row0 = q_row0;
+    prm.q_len = q_len;
+    prm.pos0 = pos0;
+    prm.nq = nq;
+    prm.nkv = nkv;
+    prm.layer = layer;
+    prm.n_layers = n_layers;
+    prm.row_stride_blk = n_layers * 2 * nkv * 16;
+    prm.scale_log2 = scale * kLog2e;
+    prm.out = static_cast<__nv_bfloat16*>(out);
+    prm.table = bt;
+    const dim3 grid((q_len + kQ - 1) / kQ, nq);
+    return launch_pdl(attn_prefill_tc_kernel, grid, dim3(192), kSmemBytes, static_cast<cudaStream_t>(stream), mq, mkv,
+                      prm);
+}

@@ -8,6 +8,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "cronus kernels target sm_100a only"
@@ -78,9 +79,17 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
-// Spin (the hardware suspends inside try_wait) until phase `parity` completes.
+// Spin (the hardware suspends inside try_wait) until phase `parity` completes. A
+// watchdog turns a pipeline deadlock into a trapped kernel (an error the host sees)
+// instead of a hung GPU: ~2^30 failed polls is many seconds of wall time.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t spins = 0;
     while (!mbar_try_wait(bar, parity)) {
+        if (++spins == (1u << 26)) {
+            printf("[cronus watchdog] block (%d,%d) thread %d stuck on mbarrier smem+0x%x parity %u\n", blockIdx.x,
+                   blockIdx.y, threadIdx.x, smem_u32(bar) & 0xFFFFF, parity);
+            __trap();
+        }
     }
 }
 

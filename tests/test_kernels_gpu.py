@@ -201,20 +201,26 @@ def test_attn_decode(L, nq, nkv):
             assert torch.allclose(got, ref, rtol=2e-2, atol=2e-2), (bps, ln, (got - ref).abs().max().item())
 
 
+@pytest.mark.parametrize("impl", ["mma", "tc"])
 @pytest.mark.parametrize("nq,nkv", [(2, 1), (32, 8), (28, 4)])
-@pytest.mark.parametrize("pos0,qlen", [(0, 1), (0, 77), (0, 256), (300, 64), (1000, 212), (48, 512)])
-def test_attn_prefill(L, nq, nkv, pos0, qlen):
+@pytest.mark.parametrize("pos0,qlen", [(0, 1), (0, 77), (0, 256), (300, 64), (1000, 212), (48, 512), (2000, 700)])
+def test_attn_prefill(L, nq, nkv, pos0, qlen, impl):
     gen = torch.Generator(device="cuda").manual_seed(pos0 + qlen + nq)
     layers, layer = 2, 0
     T = pos0 + qlen
-    pool = make_pool((T + 15) // 16 + 5, layers, nkv)
+    # tc reads whole blocks (masked): stale slots must be finite -> large finite garbage
+    pool = make_pool((T + 15) // 16 + 5, layers, nkv, fill=float("nan") if impl == "mma" else 3e4)
     tables, ks, vs = fill_sequences(pool, layer, [T], nkv, gen)
     row0 = 3
     q = torch.randn(row0 + qlen + 2, nq * 128, device="cuda", generator=gen).bfloat16()
     out = torch.zeros_like(q)
     scale = 1 / math.sqrt(128)
-    ok(L.ck_attn_prefill(p(q), p(pool), p(tables[0]), row0, qlen, pos0, p(out), nq, nkv, layer, layers, scale,
-                         stream()))
+    if impl == "mma":
+        ok(L.ck_attn_prefill(p(q), p(pool), p(tables[0]), row0, qlen, pos0, p(out), nq, nkv, layer, layers, scale,
+                             stream()))
+    else:
+        ok(L.ck_attn_prefill_tc(p(q), q.shape[0], p(pool), pool.shape[0], p(tables[0]), row0, qlen, pos0, p(out), nq,
+                                nkv, layer, layers, scale, stream()))
     qpos = torch.arange(pos0, T, device="cuda")
     ref = attn_ref(q[row0:row0 + qlen].view(qlen, nq, 128), ks[0], vs[0], qpos, scale)
     got = out[row0:row0 + qlen].float().view(qlen, nq, 128)

@@ -36,6 +36,34 @@ enum { CK_EPI_BF16 = 0, CK_EPI_F32 = 1, CK_EPI_RED_F32 = 2 };
 int ck_gemm(const void* W, const void* X, void* out, const void* bias, int M, int N, int K, int ldo, int epi,
             int splits, int max_ctas, void* stream);
 
+/* Fused finalize of a GEMM output tile (128 output columns x BN tokens), run by the
+ * last CTA to complete the tile (per-tile ticket counting finished K-blocks):
+ *   CK_FUSE_QKV_ROPE: the tile is one 128-dim head of the fp32 qkv accumulator ->
+ *                     RoPE(q) -> q_out bf16, RoPE(k) / v -> paged KV slot of each row
+ *   CK_FUSE_SILU:     64 interleaved (gate, up) pairs -> act bf16 = silu(g) * u
+ * zero_after clears the accumulator tile after reading it (red.add reuse). tickets:
+ * one int per (n tile, m tile), zero before the first call, left zero. */
+enum { CK_FUSE_NONE = 0, CK_FUSE_QKV_ROPE = 1, CK_FUSE_SILU = 2 };
+typedef struct {
+    int kind;
+    int zero_after;
+    int* tickets;
+    /* QKV_ROPE */
+    void* q_out;
+    void* kv_pool;
+    const int* bt;
+    const int* row_bt;
+    const int* row_pos;
+    const float* cos_tab;
+    const float* sin_tab;
+    int nq, nkv, layer, n_layers;
+    /* SILU */
+    void* act;
+} ck_gemm_fuse;
+
+int ck_gemm_fused(const void* W, const void* X, void* out, const void* bias, int M, int N, int K, int epi,
+                  int splits, int max_ctas, const ck_gemm_fuse* fuse, void* stream);
+
 /* Deterministic uniform init: out[i] = bf16(offset + scale * u_i), u_i in [-1, 1)
  * from splitmix64(seed, tensor_id, i) (restated in oracle/numerics.py). */
 int ck_init_uniform(void* out_bf16, long long n, unsigned long long seed, unsigned long long tensor_id,

@@ -11,6 +11,7 @@ D = ctypes.c_double
 
 CK = {
     "ck_gemm": [V, V, V, V, I, I, I, I, I, I, I, V],
+    "ck_gemm_fused": [V, V, V, V, I, I, I, I, I, I, V, V],
     "ck_init_uniform": [V, LL, ULL, ULL, F, F, V],
     "ck_prompt_tokens": [V, V, V, I, ULL, I, V],
     "ck_rope_table": [V, V, I, D, V],

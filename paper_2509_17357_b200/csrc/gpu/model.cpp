@@ -242,6 +242,9 @@ Worker::Worker(const Weights& w, int max_rows, int max_sample, int max_blocks_pe
     check_cuda(cudaMalloc(&attn_ws_, attn_ws_floats_ * 4), "alloc attn ws");
     check_cuda(cudaMalloc(&attn_tickets_, R * m_.n_kv_heads * 4), "alloc attn tickets");
     check_cuda(cudaMemset(attn_tickets_, 0, R * m_.n_kv_heads * 4), "zero attn tickets");
+    const size_t n_tiles = static_cast<size_t>(std::max(2 * m_.ffn, m_.qkv_n()) / 128) * ((R + 31) / 32);
+    check_cuda(cudaMalloc(&tile_tickets_, n_tiles * 4), "alloc tile tickets");
+    check_cuda(cudaMemset(tile_tickets_, 0, n_tiles * 4), "zero tile tickets");
     check_cuda(cudaMalloc(&arg_ws_, static_cast<size_t>(max_sample) * 64 * 4), "alloc argmax ws");
     check_cuda(cudaMalloc(&arg_tickets_, static_cast<size_t>(max_sample) * 4), "alloc argmax tickets");
     check_cuda(cudaMemset(arg_tickets_, 0, static_cast<size_t>(max_sample) * 4), "zero argmax tickets");
@@ -257,7 +260,8 @@ Worker::~Worker() {
     cudaSetDevice(w_.device());
     for (void* p : {static_cast<void*>(x_), h_, static_cast<void*>(qkv_), q_, attn_, static_cast<void*>(gu_), act_, hs_,
                     static_cast<void*>(logits_), static_cast<void*>(attn_ws_), static_cast<void*>(meta_dev_),
-                    static_cast<void*>(attn_tickets_), static_cast<void*>(arg_ws_), static_cast<void*>(arg_tickets_)})
+                    static_cast<void*>(attn_tickets_), static_cast<void*>(arg_ws_), static_cast<void*>(arg_tickets_),
+                    static_cast<void*>(tile_tickets_)})
         if (p) cudaFree(p);
     for (int i = 0; i < kRing; ++i) {
         if (meta_host_[i]) cudaFreeHost(meta_host_[i]);
@@ -308,10 +312,10 @@ void Worker::collect_stats() {
 }
 
 void Worker::gemm(const void* W, const void* X, void* out, const void* bias, int M, int N, int K, int epi,
-                  int splits) {
+                  int splits, const ck_gemm_fuse* fuse) {
     cudaEvent_t a = nullptr;
     mark(a);
-    check_ck(ck_gemm(W, X, out, bias, M, N, K, N, epi, splits, max_ctas_, stream_), "gemm");
+    check_ck(ck_gemm_fused(W, X, out, bias, M, N, K, epi, splits, max_ctas_, fuse, stream_), "gemm");
     ++launches;
     // algorithmic bytes: weights + activations in + output (red.add counted once)
     done(a, M <= 128 ? &stat_gemm_stream : &stat_gemm_tc,
@@ -320,6 +324,17 @@ void Worker::gemm(const void* W, const void* X, void* out, const void* bias, int
 }
 
 namespace {
+// CRONUS_FUSE_EPILOGUE=1: RoPE/KV-append and SiLU*up run inside the QKV / gate_up GEMMs
+// (ticketed tile finalize). Measured slower than the separate kernels (the finalize
+// sits on the GEMM's critical tail), so off by default.
+bool fuse_epilogue() {
+    static const bool on = [] {
+        const char* e = std::getenv("CRONUS_FUSE_EPILOGUE");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 template <class T>
 T* carve(int*& cur, size_t n) {
     uintptr_t p = reinterpret_cast<uintptr_t>(cur);
@@ -403,13 +418,30 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         check_ck(ck_rmsnorm(x_, L.attn_norm, h_, nullptr, M, H, m.rms_eps, nullptr, 0, stream_), "rmsnorm");
         ++launches;
         done(a, &stat_other, 0, 0);
-        gemm(L.wqkv, h_, qkv_, L.bqkv, M, Q, H, small ? CK_EPI_RED_F32 : CK_EPI_F32, small ? 0 : 1);
-        mark(a);
-        check_ck(ck_qkv_rope_append(qkv_, nullptr, q_, pool.base, bt, row_bt, row_pos, w_.cos_tab, w_.sin_tab, M,
-                                    m.n_heads, m.n_kv_heads, l, m.layers, small ? 1 : 0, stream_),
-                 "qkv_rope_append");
-        ++launches;
-        done(a, &stat_other, 0, 0);
+        // QKV projection with RoPE + KV append fused into its tile finalize
+        ck_gemm_fuse fq{};
+        fq.kind = CK_FUSE_QKV_ROPE;
+        fq.zero_after = small ? 1 : 0;
+        fq.tickets = tile_tickets_;
+        fq.q_out = q_;
+        fq.kv_pool = pool.base;
+        fq.bt = bt;
+        fq.row_bt = row_bt;
+        fq.row_pos = row_pos;
+        fq.cos_tab = w_.cos_tab;
+        fq.sin_tab = w_.sin_tab;
+        fq.nq = m.n_heads, fq.nkv = m.n_kv_heads, fq.layer = l, fq.n_layers = m.layers;
+        if (fuse_epilogue()) {
+            gemm(L.wqkv, h_, qkv_, L.bqkv, M, Q, H, small ? CK_EPI_RED_F32 : CK_EPI_F32, small ? 0 : 1, &fq);
+        } else {
+            gemm(L.wqkv, h_, qkv_, L.bqkv, M, Q, H, small ? CK_EPI_RED_F32 : CK_EPI_F32, small ? 0 : 1);
+            mark(a);
+            check_ck(ck_qkv_rope_append(qkv_, nullptr, q_, pool.base, bt, row_bt, row_pos, w_.cos_tab, w_.sin_tab, M,
+                                        m.n_heads, m.n_kv_heads, l, m.layers, small ? 1 : 0, stream_),
+                     "qkv_rope_append");
+            ++launches;
+            done(a, &stat_other, 0, 0);
+        }
         if (n_dec > 0) {
             mark(a);
             check_ck(ck_attn_decode(q_, pool.base, bt, D(o_d_row), D(o_d_len), D(o_d_bt), D(o_d_item0), D(o_d_work),
@@ -433,11 +465,21 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         check_ck(ck_rmsnorm(x_, L.ffn_norm, h_, nullptr, M, H, m.rms_eps, nullptr, 0, stream_), "rmsnorm");
         ++launches;
         done(a, &stat_other, 0, 0);
-        gemm(L.wgu, h_, gu_, nullptr, M, 2 * F, H, small ? CK_EPI_RED_F32 : CK_EPI_F32, small ? 0 : 1);
-        mark(a);
-        check_ck(ck_silu_mul(gu_, act_, M, F, small ? 1 : 0, stream_), "silu_mul");
-        ++launches;
-        done(a, &stat_other, 0, 0);
+        // gate/up projection with SiLU(gate) * up fused into its tile finalize
+        ck_gemm_fuse fs{};
+        fs.kind = CK_FUSE_SILU;
+        fs.zero_after = small ? 1 : 0;
+        fs.tickets = tile_tickets_;
+        fs.act = act_;
+        if (fuse_epilogue()) {
+            gemm(L.wgu, h_, gu_, nullptr, M, 2 * F, H, small ? CK_EPI_RED_F32 : CK_EPI_F32, small ? 0 : 1, &fs);
+        } else {
+            gemm(L.wgu, h_, gu_, nullptr, M, 2 * F, H, small ? CK_EPI_RED_F32 : CK_EPI_F32, small ? 0 : 1);
+            mark(a);
+            check_ck(ck_silu_mul(gu_, act_, M, F, small ? 1 : 0, stream_), "silu_mul");
+            ++launches;
+            done(a, &stat_other, 0, 0);
+        }
         gemm(L.wd, act_, x_, nullptr, M, H, F, CK_EPI_RED_F32, 0);
     }
     if (R > 0) {

@@ -6,6 +6,8 @@
 
 #include <cuda_runtime.h>
 
+#include "cronus_ck.h"
+
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -175,6 +177,7 @@ class Worker {
     // tensor-regime pass, which stores instead of red.adding); the weight-streaming
     // regime needs them zero and its consumers re-zero what they read.
     int qkv_dirty_rows_ = 0, gu_dirty_rows_ = 0;
+    int* tile_tickets_ = nullptr;  // fused-epilogue tile tickets (self-resetting)
     float* arg_ws_ = nullptr;      // argmax slice winners [max_sample * 64]
     int* arg_tickets_ = nullptr;   // [max_sample], self-resetting
     int* meta_dev_ = nullptr;
@@ -196,7 +199,8 @@ class Worker {
     cudaEvent_t ev();
     void mark(cudaEvent_t& a);
     void done(cudaEvent_t a, KernelStat* into, double bytes, double flops);
-    void gemm(const void* W, const void* X, void* out, const void* bias, int M, int N, int K, int epi, int splits);
+    void gemm(const void* W, const void* X, void* out, const void* bias, int M, int N, int K, int epi, int splits,
+              const ck_gemm_fuse* fuse = nullptr);
 };
 
 void check_cuda(cudaError_t e, const char* what);

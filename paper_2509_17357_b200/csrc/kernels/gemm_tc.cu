@@ -47,7 +47,66 @@ struct GemmParams {
     // CTA streams the same number of weight bytes regardless of tile count.
     int stream_k;
     long long iters;
+    ck_gemm_fuse fuse;
 };
+
+// ------------------------------------------------------------------ fused tile finalize
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// Runs on the 128 epilogue threads (t = 0..127) of the CTA that completed tile (nt, mt).
+__device__ void finalize_tile(const GemmParams& p, int nt, int mt, int BN, int t) {
+    const ck_gemm_fuse& f = p.fuse;
+    float* acc = static_cast<float*>(p.out);
+    const int m0 = mt * BN, m1 = min(p.M, m0 + BN);
+    const int n0 = nt * kTileN;
+    if (f.kind == CK_FUSE_QKV_ROPE) {
+        const int h = nt;  // a 128-column tile is exactly one head
+        const int nrot = f.nq + f.nkv;
+        const size_t hs = 16 * 128;
+        __nv_bfloat16* pool = static_cast<__nv_bfloat16*>(f.kv_pool);
+        for (int m = m0; m < m1; ++m) {
+            float* row = acc + static_cast<size_t>(m) * p.ldo + n0;
+            const int pos = f.row_pos[m];
+            if (h < nrot) {
+                if (t < 64) {
+                    const float a = __ldcg(row + t), b = __ldcg(row + t + 64);
+                    if (f.zero_after) {
+                        row[t] = 0.f;
+                        row[t + 64] = 0.f;
+                    }
+                    const float c = f.cos_tab[static_cast<size_t>(pos) * 64 + t];
+                    const float sn = f.sin_tab[static_cast<size_t>(pos) * 64 + t];
+                    __nv_bfloat16* dst;
+                    if (h < f.nq) {
+                        dst = static_cast<__nv_bfloat16*>(f.q_out) + static_cast<size_t>(m) * f.nq * 128 + h * 128;
+                    } else {
+                        const int blk = f.bt[f.row_bt[m] + (pos >> 4)];
+                        dst = pool + ((static_cast<size_t>(blk) * f.n_layers + f.layer) * 2 * f.nkv + (h - f.nq)) * hs +
+                              (pos & 15) * 128;
+                    }
+                    dst[t] = f2bf(a * c - b * sn);
+                    dst[t + 64] = f2bf(b * c + a * sn);
+                }
+            } else {
+                const float v = __ldcg(row + t);
+                if (f.zero_after) row[t] = 0.f;
+                const int blk = f.bt[f.row_bt[m] + (pos >> 4)];
+                pool[((static_cast<size_t>(blk) * f.n_layers + f.layer) * 2 * f.nkv + f.nkv + (h - nrot)) * hs +
+                     (pos & 15) * 128 + t] = f2bf(v);
+            }
+        }
+    } else {  // CK_FUSE_SILU: 64 (gate, up) pairs; two rows in flight per pass
+        const int pair = t & 63;
+        __nv_bfloat16* act = static_cast<__nv_bfloat16*>(f.act);
+        const int F = p.N / 2;
+        for (int m = m0 + (t >> 6); m < m1; m += 2) {
+            float* row = acc + static_cast<size_t>(m) * p.ldo + n0;
+            const float2 gu = __ldcg(reinterpret_cast<const float2*>(row) + pair);
+            if (f.zero_after) reinterpret_cast<float2*>(row)[pair] = make_float2(0.f, 0.f);
+            act[static_cast<size_t>(m) * F + n0 / 2 + pair] = f2bf(gu.x / (1.f + __expf(-gu.x)) * gu.y);
+        }
+    }
+}
 
 template <int BN>
 struct Cfg {
@@ -300,6 +359,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) mbar_arrive(&tempty[acc]);
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
+            if (p.fuse.kind != CK_FUSE_NONE) {
+                // tile ticket: K-blocks finished so far; the CTA that completes the tile
+                // finalizes it (its own partial is made visible first)
+                __threadfence();
+                epi_bar();
+                const int t = (warp - 2) * 32 + lane;  // 0..127
+                int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
+                if (t == 0) {
+                    const int tile = nt * p.m_tiles + mt;
+                    const int done = atomicAdd(&p.fuse.tickets[tile], kb1 - kb0) + (kb1 - kb0);
+                    *s_last = done == p.kb_total;
+                    if (done == p.kb_total) p.fuse.tickets[tile] = 0;
+                }
+                epi_bar();
+                if (*s_last) {
+                    __threadfence();
+                    finalize_tile(p, nt, mt, BN, t);
+                }
+                epi_bar();
+            }
         }
     }
 
@@ -401,8 +480,26 @@ int launch(const CUtensorMap& mw, const CUtensorMap& mx, GemmParams p, int max_c
 
 }  // namespace
 
+namespace {
+int gemm_impl(const void* W, const void* X, void* out, const void* bias, int M, int N, int K, int ldo, int epi,
+              int splits, int max_ctas, const ck_gemm_fuse* fuse, void* stream);
+}
+
 extern "C" int ck_gemm(const void* W, const void* X, void* out, const void* bias, int M, int N, int K, int ldo,
                        int epi, int splits, int max_ctas, void* stream) {
+    return gemm_impl(W, X, out, bias, M, N, K, ldo, epi, splits, max_ctas, nullptr, stream);
+}
+
+extern "C" int ck_gemm_fused(const void* W, const void* X, void* out, const void* bias, int M, int N, int K, int epi,
+                             int splits, int max_ctas, const ck_gemm_fuse* fuse, void* stream) {
+    if (fuse && fuse->kind != CK_FUSE_NONE && (epi == CK_EPI_BF16 || !fuse->tickets))
+        return static_cast<int>(cudaErrorInvalidValue);  // finalize reads the fp32 tile back
+    return gemm_impl(W, X, out, bias, M, N, K, N, epi, splits, max_ctas, fuse, stream);
+}
+
+namespace {
+int gemm_impl(const void* W, const void* X, void* out, const void* bias, int M, int N, int K, int ldo, int epi,
+              int splits, int max_ctas, const ck_gemm_fuse* fuse, void* stream) {
     if (M <= 0) return 0;
     if (N % kTileN != 0 || K % kTileK != 0 || N <= 0 || K <= 0) return static_cast<int>(cudaErrorInvalidValue);
     if ((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(X)) & 15) return static_cast<int>(cudaErrorMisalignedAddress);
@@ -416,6 +513,7 @@ extern "C" int ck_gemm(const void* W, const void* X, void* out, const void* bias
     p.K = K;
     p.ldo = ldo > 0 ? ldo : N;
     p.epi = epi;
+    p.fuse = fuse ? *fuse : ck_gemm_fuse{};
     p.m_tiles = (M + BN - 1) / BN;
     p.kb_total = K / kTileK;
     const int tiles = (N / kTileN) * p.m_tiles;
@@ -448,3 +546,4 @@ extern "C" int ck_gemm(const void* W, const void* X, void* out, const void* bias
         default: return launch<256>(mw, mx, p, max_ctas, s);
     }
 }
+}  // namespace

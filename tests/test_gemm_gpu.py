@@ -95,3 +95,75 @@ def test_gemm_capped_grid(L):
     out = torch.empty(M, N, device="cuda", dtype=torch.float32)
     run_gemm(L, W, X, out, M, N, K, EPI_F32, max_ctas=5)
     check(out, ref, K, False)
+
+
+class Fuse(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("zero_after", ctypes.c_int), ("tickets", ctypes.c_void_p),
+                ("q_out", ctypes.c_void_p), ("kv_pool", ctypes.c_void_p), ("bt", ctypes.c_void_p),
+                ("row_bt", ctypes.c_void_p), ("row_pos", ctypes.c_void_p), ("cos_tab", ctypes.c_void_p),
+                ("sin_tab", ctypes.c_void_p), ("nq", ctypes.c_int), ("nkv", ctypes.c_int), ("layer", ctypes.c_int),
+                ("n_layers", ctypes.c_int), ("act", ctypes.c_void_p)]
+
+
+@pytest.mark.parametrize("M", [3, 32, 100, 300])
+def test_gemm_fused_silu_matches_unfused(L, M):
+    """gate_up GEMM + SiLU*up finalized by the last CTA of each tile (tickets)."""
+    F, K = 512, 1024
+    W = (torch.randn(2 * F, K, device="cuda") * 0.05).bfloat16()
+    X = torch.randn(M, K, device="cuda").bfloat16()
+    small = M <= 128
+    acc = torch.zeros(M, 2 * F, device="cuda")
+    act = torch.empty(M, F, dtype=torch.bfloat16, device="cuda")
+    tickets = torch.zeros(4096, dtype=torch.int32, device="cuda")
+    f = Fuse(kind=2, zero_after=1 if small else 0, tickets=tickets.data_ptr(), act=act.data_ptr())
+    s = torch.cuda.current_stream().cuda_stream
+    rc = L.ck_gemm_fused(p(W), p(X), p(acc), None, M, 2 * F, K, EPI_RED if small else EPI_F32, 0 if small else 1, 0,
+                         ctypes.byref(f), ctypes.c_void_p(s))
+    assert rc == 0
+    torch.cuda.synchronize()
+    gu = X.float() @ W.float().t()
+    ref = torch.nn.functional.silu(gu[:, 0::2]) * gu[:, 1::2]
+    assert torch.allclose(act.float(), ref, rtol=2e-2, atol=2e-2)
+    assert tickets.abs().sum() == 0
+    if small:
+        assert acc.abs().sum() == 0  # accumulator cleared for reuse
+
+
+@pytest.mark.parametrize("M", [5, 64, 200])
+def test_gemm_fused_qkv_rope_matches_unfused(L, M):
+    nq, nkv, H, layers, layer = 4, 2, 512, 2, 1
+    Q = (nq + 2 * nkv) * 128
+    g = torch.Generator(device="cuda").manual_seed(M)
+    W = (torch.randn(Q, H, device="cuda", generator=g) * 0.05).bfloat16()
+    X = torch.randn(M, H, device="cuda", generator=g).bfloat16()
+    bias = (0.1 * torch.randn(Q, device="cuda", generator=g)).bfloat16()
+    small = M <= 128
+    nb = 64
+    pos = torch.randperm(1000, device="cuda", generator=g)[:M].int()
+    perm = torch.randperm(nb, device="cuda", generator=g).int()
+    bt = perm.repeat(M)
+    row_bt = torch.arange(M, device="cuda", dtype=torch.int32) * nb
+    c = torch.empty(2048 * 64, device="cuda"); sn = torch.empty(2048 * 64, device="cuda")
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert L.ck_rope_table(p(c), p(sn), 2048, 10000.0, st) == 0
+    outs = []
+    for fused in (False, True):
+        pool = torch.zeros(nb, layers, 2, nkv, 16, 128, dtype=torch.bfloat16, device="cuda")
+        acc = torch.zeros(M, Q, device="cuda")
+        q_out = torch.empty(M, nq * 128, dtype=torch.bfloat16, device="cuda")
+        epi = EPI_RED if small else EPI_F32
+        if fused:
+            tickets = torch.zeros(4096, dtype=torch.int32, device="cuda")
+            f = Fuse(kind=1, zero_after=1 if small else 0, tickets=tickets.data_ptr(), q_out=q_out.data_ptr(),
+                     kv_pool=pool.data_ptr(), bt=bt.data_ptr(), row_bt=row_bt.data_ptr(), row_pos=pos.data_ptr(),
+                     cos_tab=c.data_ptr(), sin_tab=sn.data_ptr(), nq=nq, nkv=nkv, layer=layer, n_layers=layers)
+            assert L.ck_gemm_fused(p(W), p(X), p(acc), p(bias), M, Q, H, epi, 0 if small else 1, 0, ctypes.byref(f),
+                                   st) == 0
+        else:
+            assert L.ck_gemm(p(W), p(X), p(acc), p(bias), M, Q, H, Q, epi, 0 if small else 1, 0, st) == 0
+            assert L.ck_qkv_rope_append(p(acc), None, p(q_out), p(pool), p(bt), p(row_bt), p(pos), p(c), p(sn), M,
+                                        nq, nkv, layer, layers, 1 if small else 0, st) == 0
+        torch.cuda.synchronize()
+        outs.append((q_out.float(), pool.float()))
+    assert torch.allclose(outs[0][0], outs[1][0], rtol=1e-2, atol=1e-2)
+    assert torch.allclose(outs[0][1], outs[1][1], rtol=1e-2, atol=1e-2)

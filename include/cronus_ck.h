@@ -151,6 +151,33 @@ int ck_smid_probe(int* hits, int n_ctas, void* stream);
  * cp.async.bulk 16 KiB chunks. Time it with events on `stream`. */
 int ck_bw_probe(const void* buf, long long bytes, int mode, int ctas, void* stream);
 
+/* Persistent decode forward: one cooperative launch runs a whole decode-only pass
+ * (embed -> L layers -> final norm -> LM head -> greedy argmax) for M <= 64 rows.
+ * A plan holds the weight tensor maps (built once) and the activation buffers the
+ * per-M activation maps point at. Activation / accumulator buffers follow the
+ * separate-kernel path's conventions: qkv and gu are red.add accumulators that must be
+ * zero on entry and are left zero. */
+typedef struct ck_mega_args {
+    int M, H, NQKV, NQ, F, V, nq, nkv, grid;
+    float eps, scale;
+    float* x; void* h; float* qkv; void* q; void* attn; float* gu; void* act; void* hs; float* logits;
+    const void* embed; const void* final_norm; const float* cos_tab; const float* sin_tab;
+    const int* row_rid; const int* row_pos; const int* bt;
+    const int* d_row; const int* d_len; const int* d_bt; const int* d_item0; const int* d_work;
+    int n_work, blocks_per_split;
+    float* attn_ws; int* attn_tickets; void* pool;
+    const long long* s_out; int* last_tok; int* out_tok; float* arg_ws; int* arg_tickets;
+} ck_mega_args;
+
+int ck_mega_plan_create(void** plan, int L, const void* const* w_qkv, const void* const* w_o,
+                        const void* const* w_gu, const void* const* w_d, const void* lm_head,
+                        const void* const* attn_norm, const void* const* ffn_norm, const void* const* bqkv, int H,
+                        int NQKV, int NQ, int F, int V, const void* h_buf, const void* attn_buf,
+                        const void* act_buf, const void* hs_buf);
+void ck_mega_plan_destroy(void* plan);
+int ck_mega_max_rows(void);
+int ck_mega_decode(void* plan, const ck_mega_args* args, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -14,6 +14,7 @@
 // still execute exactly the scheduled work, and in wall-clock mode the copy
 // stream overlaps CPI compute.
 #include <algorithm>
+#include <cstdio>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -46,6 +47,10 @@ struct EngineOptions {
     long long cpi_pool_blocks = 0, ppi_pool_blocks = 0;
     uint64_t seed = 1234, prompt_seed = 99;
     bool profile = false;
+    // decode-only CPI passes: "layered" (one kernel per op, PDL-chained) or "persistent"
+    // (ck_mega_decode: one cooperative launch per pass; measured slower on B200, kept
+    // selectable for experiments — see DESIGN.md)
+    bool persistent_decode = false;
 };
 
 EngineOptions parse_engine_options(const std::string& text) {
@@ -79,7 +84,11 @@ EngineOptions parse_engine_options(const std::string& text) {
         else if (k == "seed") o.seed = std::stoull(v);
         else if (k == "prompt_seed") o.prompt_seed = std::stoull(v);
         else if (k == "profile") o.profile = v == "1" || v == "true";
-        else throw std::invalid_argument("engine options: unknown key " + k);
+        else if (k == "decode_forward") {
+            if (v != "layered" && v != "persistent")
+                throw std::invalid_argument("engine options: decode_forward = layered | persistent");
+            o.persistent_decode = v == "persistent";
+        } else throw std::invalid_argument("engine options: unknown key " + k);
     }
     if (o.ppi_chunk < 16 || o.ppi_chunk % 16) throw std::invalid_argument("engine options: ppi_chunk % 16 != 0");
     return o;
@@ -252,6 +261,7 @@ struct GpuEngine::Impl {
             cpi.reset();
             check_cuda(cudaSetDevice(opt.cpi_device), "cudaSetDevice");
             cpi = std::make_unique<gpu::Worker>(*w_cpi, B, B, static_cast<int>(pool_cpi->blocks) + B, s_cpi, cpi_ctas);
+            cpi->set_persistent_decode(opt.persistent_decode);
             cpi_rows = B;
         }
         if (!ppi) {
@@ -569,6 +579,7 @@ class PairExecutor : public sched::Executor {
         ks("gemm_stream", E.cpi->stat_gemm_stream);
         ks("gemm_tc", E.cpi->stat_gemm_tc);
         ks("other", E.cpi->stat_other);
+        ks("mega_decode", E.cpi->stat_mega);
         ks("forward", E.cpi->stat_forward, false);
         s << "}, \"ppi\": {";
         ks("prefill_attn", E.ppi->stat_prefill_attn);
@@ -698,6 +709,27 @@ double GpuEngine::time_pass(const ClusterConfig& cfg, int worker, int n_dec, int
     }
     cudaEventDestroy(a);
     cudaEventDestroy(b);
+    if (const char* e = std::getenv("CRONUS_PASS_STATS"); e && e[0] == '1') {  // dev: per-kernel-class split
+        W.reset_stats();
+        W.set_profiling(true);
+        W.forward(batch, pool, static_cast<int*>(tb.prompt.p), static_cast<long long*>(tb.prompt_off.p),
+                  static_cast<int*>(tb.last_tok.p), static_cast<int*>(tb.out_tok.p));
+        W.collect_stats();
+        W.set_profiling(false);
+        auto pr = [](const char* n, const gpu::KernelStat& k) {
+            if (k.launches)
+                std::fprintf(stderr, " %s: n=%lld ms=%.3f GB/s=%.0f", n, k.launches, k.ms, k.bytes / std::max(k.ms, 1e-9) / 1e6);
+        };
+        std::fprintf(stderr, "[pass stats n_dec=%d ctx=%d chunk=%d]", n_dec, dec_ctx, chunk_len);
+        pr("decode_attn", W.stat_decode_attn);
+        pr("prefill_attn", W.stat_prefill_attn);
+        pr("gemm_stream", W.stat_gemm_stream);
+        pr("gemm_tc", W.stat_gemm_tc);
+        pr("other", W.stat_other);
+        pr("mega", W.stat_mega);
+        pr("forward", W.stat_forward);
+        std::fprintf(stderr, "\n");
+    }
     std::sort(t.begin(), t.end());
     return t[t.size() / 2];
 }

@@ -258,6 +258,7 @@ Worker::Worker(const Weights& w, int max_rows, int max_sample, int max_blocks_pe
 
 Worker::~Worker() {
     cudaSetDevice(w_.device());
+    if (mega_) ck_mega_plan_destroy(mega_);
     for (void* p : {static_cast<void*>(x_), h_, static_cast<void*>(qkv_), q_, attn_, static_cast<void*>(gu_), act_, hs_,
                     static_cast<void*>(logits_), static_cast<void*>(attn_ws_), static_cast<void*>(meta_dev_),
                     static_cast<void*>(attn_tickets_), static_cast<void*>(arg_ws_), static_cast<void*>(arg_tickets_),
@@ -390,6 +391,14 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
 
     const int H = m.hidden, Q = m.qkv_n(), NQ = m.q_n(), F = m.ffn;
     const bool small = M <= 128;  // weight-streaming regime
+    if (b.p_len == 0 && n_dec == M && R == M && persistent_ && mega_ok_ && M <= ck_mega_max_rows()) {
+        const PassMeta pm{row_rid,       row_pos,          bt,         D(o_d_row), D(o_d_len), D(o_d_bt), D(o_d_item0),
+                          D(o_d_work), reinterpret_cast<const long long*>(D(o_s_out))};
+        if (forward_mega(b, pool, pm, last_tok, out_tok)) {
+            done(pass0, &stat_forward, 0, 0);
+            return;
+        }
+    }
     const float scale = 1.0f / std::sqrt(static_cast<float>(m.head_dim));
     long long dec_keys = 0;
     for (int len : b.d_len) dec_keys += len;
@@ -496,6 +505,60 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         done(a, &stat_other, 0, 0);
     }
     done(pass0, &stat_forward, 0, 0);
+}
+
+bool Worker::forward_mega(const Batch& b, const KvPool& pool, const PassMeta& pm, int* last_tok, int* out_tok) {
+    const ModelSpec& m = m_;
+    const int M = b.rows();
+    for (int i = 0; i < M; ++i)  // decode rows in order, each sampled into its own slot
+        if (b.d_row[i] != i || b.s_row[i] != i) return false;
+    if (!mega_) {
+        std::vector<const void*> wq, wo, wgu, wd, an, fn, bq;
+        bool bias = false;
+        for (const LayerWeights& L : w_.layer) {
+            wq.push_back(L.wqkv), wo.push_back(L.wo), wgu.push_back(L.wgu), wd.push_back(L.wd);
+            an.push_back(L.attn_norm), fn.push_back(L.ffn_norm), bq.push_back(L.bqkv);
+            bias = bias || L.bqkv;
+        }
+        check_ck(ck_mega_plan_create(&mega_, m.layers, wq.data(), wo.data(), wgu.data(), wd.data(), w_.lm_head,
+                                     an.data(), fn.data(), bias ? bq.data() : nullptr, m.hidden, m.qkv_n(), m.q_n(),
+                                     m.ffn, m.vocab, h_, attn_, act_, hs_),
+                 "mega plan");
+    }
+    if (qkv_dirty_rows_ > 0)
+        check_cuda(cudaMemsetAsync(qkv_, 0, static_cast<size_t>(qkv_dirty_rows_) * m.qkv_n() * 4, stream_), "memset qkv");
+    if (gu_dirty_rows_ > 0)
+        check_cuda(cudaMemsetAsync(gu_, 0, static_cast<size_t>(gu_dirty_rows_) * 2 * m.ffn * 4, stream_), "memset gu");
+    qkv_dirty_rows_ = gu_dirty_rows_ = 0;
+    ck_mega_args a{};
+    a.M = M, a.H = m.hidden, a.NQKV = m.qkv_n(), a.NQ = m.q_n(), a.F = m.ffn, a.V = m.vocab;
+    a.nq = m.n_heads, a.nkv = m.n_kv_heads, a.grid = max_ctas_ > 0 ? max_ctas_ : ck_device_sms();
+    a.eps = m.rms_eps, a.scale = 1.0f / std::sqrt(static_cast<float>(m.head_dim));
+    a.x = x_, a.h = h_, a.qkv = qkv_, a.q = q_, a.attn = attn_, a.gu = gu_, a.act = act_, a.hs = hs_, a.logits = logits_;
+    a.embed = w_.embed, a.final_norm = w_.final_norm, a.cos_tab = w_.cos_tab, a.sin_tab = w_.sin_tab;
+    a.row_rid = pm.row_rid, a.row_pos = pm.row_pos, a.bt = pm.bt, a.d_row = pm.d_row, a.d_len = pm.d_len;
+    a.d_bt = pm.d_bt, a.d_item0 = pm.d_item0, a.d_work = pm.d_work;
+    a.n_work = static_cast<int>(b.d_work.size()), a.blocks_per_split = b.blocks_per_split;
+    a.attn_ws = attn_ws_, a.attn_tickets = attn_tickets_, a.pool = pool.base;
+    a.s_out = pm.s_out, a.last_tok = last_tok, a.out_tok = out_tok, a.arg_ws = arg_ws_, a.arg_tickets = arg_tickets_;
+    cudaEvent_t ev0 = nullptr;
+    mark(ev0);
+    const int rc = ck_mega_decode(mega_, &a, stream_);
+    if (rc == static_cast<int>(cudaErrorCooperativeLaunchTooLarge)) {
+        (void)cudaGetLastError();
+        mega_ok_ = false;
+        return false;
+    }
+    check_ck(rc, "mega_decode");
+    ++launches;
+    long long keys = 0;
+    for (int len : b.d_len) keys += len;
+    const double wbytes = 2.0 * (static_cast<double>(m.layers) *
+                                     (static_cast<double>(m.qkv_n()) * m.hidden + static_cast<double>(m.hidden) * m.q_n() +
+                                      3.0 * m.hidden * m.ffn) +
+                                 static_cast<double>(m.vocab) * m.hidden);
+    done(ev0, &stat_mega, wbytes + keys * m.layers * 4.0 * m.n_kv_heads * m.head_dim, 0);
+    return true;
 }
 
 }  // namespace gpu

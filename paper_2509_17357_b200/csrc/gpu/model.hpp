@@ -146,12 +146,15 @@ class Worker {
     int max_rows() const { return max_rows_; }
     cudaStream_t stream() const { return stream_; }
     void set_profiling(bool on) { profile_ = on; }
+    void set_persistent_decode(bool on) { persistent_ = on; }
     void collect_stats();  // fold finished profiling events into stats (synchronizes)
     void reset_stats() {
         stat_decode_attn = stat_prefill_attn = stat_gemm_stream = stat_gemm_tc = stat_other = stat_forward = {};
+        stat_mega = {};
     }
     // gemm_stream: M <= 128 (weight-streaming, HBM bound); gemm_tc: M > 128 (tensor bound)
     KernelStat stat_decode_attn, stat_prefill_attn, stat_gemm_stream, stat_gemm_tc, stat_other, stat_forward;
+    KernelStat stat_mega;  // persistent decode forward (one launch per decode-only pass)
     long long launches = 0;  // our kernels launched (always counted)
 
   private:
@@ -199,6 +202,16 @@ class Worker {
     cudaEvent_t ev();
     void mark(cudaEvent_t& a);
     void done(cudaEvent_t a, KernelStat* into, double bytes, double flops);
+    // persistent decode forward (ck_mega_decode): plan built on first use; disabled for
+    // good if the cooperative launch is refused (e.g. grid larger than co-residency)
+    void* mega_ = nullptr;
+    bool persistent_ = false;
+    bool mega_ok_ = true;
+    struct PassMeta {
+        const int *row_rid, *row_pos, *bt, *d_row, *d_len, *d_bt, *d_item0, *d_work;
+        const long long* s_out;
+    };
+    bool forward_mega(const Batch& b, const KvPool& pool, const PassMeta& pm, int* last_tok, int* out_tok);
     void gemm(const void* W, const void* X, void* out, const void* bias, int M, int N, int K, int epi, int splits,
               const ck_gemm_fuse* fuse = nullptr);
 };

@@ -13,6 +13,7 @@
 
 #include "common.cuh"
 #include "cronus_ck.h"
+#include "decode_attn.cuh"
 
 namespace {
 
@@ -32,33 +33,6 @@ __device__ __forceinline__ size_t tile_off(int block, int layer, int kv, int hea
 constexpr int kPQ = 64;        // query rows per CTA
 constexpr int kPK = 64;        // keys per tile
 constexpr int kPad = 136;      // padded smem row (bf16 elements): 272 B, conflict-free ldmatrix
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
-    const int sz = pred ? 16 : 0;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(sz) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(smem_u32(p)));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(smem_u32(p)));
-}
-__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-        "{%0,%1,%2,%3};"
-        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
 
 // Gather a 64-key K or V tile of (layer, kvh) into padded smem rows.
 __device__ __forceinline__ void load_kv_tile(__nv_bfloat16* dst, const __nv_bfloat16* pool, const int* table,
@@ -254,213 +228,16 @@ __global__ void __launch_bounds__(128)
 // partials are merged by the last CTA of each (sequence, kv head) (atomic ticket),
 // so the whole op is one launch.
 constexpr int kDecStages = 3;
-constexpr int kDecTile = kBlk * kHD * 2;  // bytes of one K (or V) block tile
-
-__device__ __forceinline__ uint32_t swz(int row, int chunk) {  // byte offset in a [16][128] bf16 tile
-    return static_cast<uint32_t>(row * 256 + ((chunk ^ (row & 7)) << 4));
-}
+constexpr int kDecTile = kDTileBytes;
 
 template <int G>
 __global__ void __launch_bounds__(128)
-    attn_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ pool,
-                       const int* __restrict__ bt, const int* __restrict__ seq_row, const int* __restrict__ seq_len,
-                       const int* __restrict__ seq_bt, const int* __restrict__ seq_item0,
-                       const int* __restrict__ work, int blocks_per_split, float* __restrict__ ws,
-                       int* __restrict__ tickets, __nv_bfloat16* __restrict__ out, int nq, int nkv, int layer,
-                       int n_layers, float qk_scale_log2) {
+    attn_decode_kernel(DecodeAttnArgs a) {
     pdl_wait();
     pdl_launch();
-    extern __shared__ __align__(128) uint8_t dsm[];
-    uint8_t* sQ = dsm;                                    // [16][128] bf16, swizzled
-    uint8_t* sKV = dsm + kDecTile;                        // [4 warps][stages][K|V] tiles
-    __shared__ float wm[4][16], wl[4][16];
-    __shared__ int s_last;
-
-    const int item = blockIdx.x, kvh = blockIdx.y;
-    const int wk = work[item];
-    const int s = wk >> 16, split = wk & 0xffff;
-    const int len = seq_len[s];
-    const int nblk = (len + kBlk - 1) / kBlk;
-    const int b0 = split * blocks_per_split, b1 = min(nblk, b0 + blocks_per_split);
-    const int nsplit = seq_item0[s + 1] - seq_item0[s];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = lane >> 2, tq = lane & 3;
-    const int* table = bt + seq_bt[s];
-    const int row = seq_row[s];
-
-    // ---- Q (G rows, zero padded to 16)
-    {
-        const __nv_bfloat16* qrow = q + static_cast<size_t>(row) * nq * kHD + static_cast<size_t>(kvh) * G * kHD;
-        for (int c = threadIdx.x; c < 16 * 16; c += blockDim.x) {
-            const int r = c >> 4, ch = c & 15;
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (r < G) v = *reinterpret_cast<const uint4*>(qrow + r * kHD + ch * 8);
-            *reinterpret_cast<uint4*>(sQ + swz(r, ch)) = v;
-        }
-    }
-    // ---- per-warp K/V ring
-    uint8_t* ring = sKV + static_cast<size_t>(warp) * kDecStages * 2 * kDecTile;
-    const int first = b0 + warp;
-    const int mine = first < b1 ? (b1 - first + 3) / 4 : 0;
-    auto load = [&](int i) {  // block #i of this warp -> stage i % kDecStages
-        const int b = first + 4 * i;
-        const int blk = table[b];
-        const __nv_bfloat16* kt = pool + tile_off(blk, layer, 0, kvh, n_layers, nkv);
-        const __nv_bfloat16* vt = kt + static_cast<size_t>(nkv) * kTile;
-        uint8_t* dK = ring + (i % kDecStages) * 2 * kDecTile;
-        uint8_t* dV = dK + kDecTile;
-        const int valid = min(kBlk, len - b * kBlk);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {  // 256 16-B chunks per tile, 8 per lane
-            const int c = lane + 32 * j;
-            const int r = c >> 4, ch = c & 15;
-            const bool ok = r < valid;  // slots past the sequence end may hold stale data: zero-fill
-            cp_async16(dK + swz(r, ch), kt + r * kHD + ch * 8, ok);
-            cp_async16(dV + swz(r, ch), vt + r * kHD + ch * 8, ok);
-        }
-    };
-#pragma unroll
-    for (int i = 0; i < kDecStages - 1; ++i) {
-        if (i < mine) load(i);
-        cp_commit();
-    }
-    __syncthreads();  // sQ visible
-    uint32_t qf[8][4];
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-        const int r = lane & 15, ch = 2 * kk + (lane >> 4);
-        ldsm_x4(qf[kk], sQ + swz(r, ch));
-    }
-    float o[16][4];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-    float m_run = -INFINITY, l_run = 0.f;  // row g (query head g of the group)
-
-    for (int i = 0; i < mine; ++i) {
-        cp_wait<kDecStages - 2>();
-        __syncwarp();
-        const uint8_t* K = ring + (i % kDecStages) * 2 * kDecTile;
-        const uint8_t* V = K + kDecTile;
-        float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-            uint32_t b[4];
-            const int r = (lane & 7) + ((lane >> 4) << 3), ch = 2 * kk + ((lane >> 3) & 1);
-            ldsm_x4(b, K + swz(r, ch));
-            mma16816(s0, qf[kk], b[0], b[1]);
-            mma16816(s1, qf[kk], b[2], b[3]);
-        }
-        const int tok0 = (first + 4 * i) * kBlk;
-        float sc[4];
-        sc[0] = tok0 + 2 * tq < len ? s0[0] * qk_scale_log2 : -INFINITY;
-        sc[1] = tok0 + 2 * tq + 1 < len ? s0[1] * qk_scale_log2 : -INFINITY;
-        sc[2] = tok0 + 8 + 2 * tq < len ? s1[0] * qk_scale_log2 : -INFINITY;
-        sc[3] = tok0 + 9 + 2 * tq < len ? s1[1] * qk_scale_log2 : -INFINITY;
-        float mx = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        const float mn = fmaxf(m_run, mx);  // finite: token 0 of every block is valid
-        const float corr = exp2f(m_run - mn);
-        float p[4], rs = 0.f;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            p[e] = exp2f(sc[e] - mn);
-            rs += p[e];
-        }
-        rs += __shfl_xor_sync(0xffffffffu, rs, 1);
-        rs += __shfl_xor_sync(0xffffffffu, rs, 2);
-        l_run = l_run * corr + rs;
-        m_run = mn;
-        uint32_t pf[4];
-        pf[0] = pack_bf16x2(p[0], p[1]);
-        pf[1] = 0u;  // padded rows 8..15
-        pf[2] = pack_bf16x2(p[2], p[3]);
-        pf[3] = 0u;
-#pragma unroll
-        for (int nd = 0; nd < 16; ++nd) {
-            o[nd][0] *= corr;
-            o[nd][1] *= corr;
-        }
-#pragma unroll
-        for (int nd = 0; nd < 16; nd += 2) {
-            uint32_t b[4];
-            const int r = (lane & 7) + (((lane >> 3) & 1) << 3), ch = nd + (lane >> 4);
-            ldsm_x4_t(b, V + swz(r, ch));
-            mma16816(o[nd], pf, b[0], b[1]);
-            mma16816(o[nd + 1], pf, b[2], b[3]);
-        }
-        __syncwarp();
-        const int nxt = i + kDecStages - 1;
-        if (nxt < mine) load(nxt);
-        cp_commit();
-    }
-    cp_wait<0>();
-
-    // ---- merge the 4 warps (reuse the ring as [4][16][128] fp32 scratch)
-    __syncthreads();
-    float* wo = reinterpret_cast<float*>(sKV);
-    if (tq == 0) {
-        wm[warp][g] = m_run;
-        wl[warp][g] = l_run;
-    }
-#pragma unroll
-    for (int nd = 0; nd < 16; ++nd) {
-        wo[(warp * 16 + g) * kHD + nd * 8 + 2 * tq] = o[nd][0];
-        wo[(warp * 16 + g) * kHD + nd * 8 + 2 * tq + 1] = o[nd][1];
-    }
-    __syncthreads();
-    const bool single = nsplit == 1;
-    for (int i = threadIdx.x; i < G * kHD; i += blockDim.x) {
-        const int h = i / kHD, d = i % kHD;
-        float M = -INFINITY;
-#pragma unroll
-        for (int w2 = 0; w2 < 4; ++w2) M = fmaxf(M, wm[w2][h]);
-        float Ls = 0.f, A = 0.f;
-#pragma unroll
-        for (int w2 = 0; w2 < 4; ++w2) {
-            const float f = wm[w2][h] == -INFINITY ? 0.f : exp2f(wm[w2][h] - M);
-            Ls += wl[w2][h] * f;
-            A += wo[(w2 * 16 + h) * kHD + d] * f;
-        }
-        if (single) {
-            out[static_cast<size_t>(row) * nq * kHD + (kvh * G + h) * kHD + d] = f2bf(Ls > 0.f ? A / Ls : 0.f);
-        } else {
-            float* part = ws + (static_cast<size_t>(item) * nq + kvh * G + h) * (kHD + 2);
-            part[2 + d] = A;
-            if (d == 0) {
-                part[0] = M;
-                part[1] = Ls;
-            }
-        }
-    }
-    if (single) return;
-    // ---- last CTA of this (sequence, kv head) merges the splits
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const int prev = atomicAdd(&tickets[s * nkv + kvh], 1);
-        s_last = prev == nsplit - 1;
-        if (s_last) tickets[s * nkv + kvh] = 0;  // self-resetting for the next launch
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    const int i0 = seq_item0[s], i1 = seq_item0[s + 1];
-    for (int i = threadIdx.x; i < G * kHD; i += blockDim.x) {
-        const int h = i / kHD, d = i % kHD;
-        const int hq = kvh * G + h;
-        float M = -INFINITY;
-        for (int it = i0; it < i1; ++it) M = fmaxf(M, __ldcg(ws + (static_cast<size_t>(it) * nq + hq) * (kHD + 2)));
-        float Ls = 0.f, A = 0.f;
-        for (int it = i0; it < i1; ++it) {
-            const float* part = ws + (static_cast<size_t>(it) * nq + hq) * (kHD + 2);
-            const float pm = __ldcg(part);
-            const float f = pm == -INFINITY ? 0.f : exp2f(pm - M);
-            Ls += __ldcg(part + 1) * f;
-            A += __ldcg(part + 2 + d) * f;
-        }
-        out[static_cast<size_t>(row) * nq * kHD + hq * kHD + d] = f2bf(Ls > 0.f ? A / Ls : 0.f);
-    }
+    extern __shared__ __align__(1024) uint8_t dsm[];
+    __shared__ float small[2 * 64 + 4];
+    decode_attn_item<G, kDecStages>(a, blockIdx.x, blockIdx.y, dsm, dsm + kDecTile, small, threadIdx.x, 1);
 }
 
 template <int G>
@@ -477,10 +254,10 @@ int launch_decode(const void* q, const void* pool, const int* bt, const int* seq
         if (e != cudaSuccess) return static_cast<int>(e);
         mask |= 1u << dev;
     }
-    return launch_pdl(attn_decode_kernel<G>, dim3(n_work, nkv), dim3(128), smem, st,
-                      static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(pool), bt, seq_row,
-                      seq_len, seq_bt, seq_item0, work, bps, ws, tickets, static_cast<__nv_bfloat16*>(out), nq, nkv,
-                      layer, n_layers, qk);
+    DecodeAttnArgs a{static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(pool), bt, seq_row, seq_len,
+                     seq_bt, seq_item0, work, bps, ws, tickets, static_cast<__nv_bfloat16*>(out), nq, nkv, layer,
+                     n_layers, qk};
+    return launch_pdl(attn_decode_kernel<G>, dim3(n_work, nkv), dim3(128), smem, st, a);
 }
 
 }  // namespace

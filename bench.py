@@ -285,7 +285,9 @@ def run_ours(args, rank, world):
                    "parallelism": "replicas of worker pairs" if pairs > 1 else "co-located pair"},
         "gpu_launches": int(st.get("gpu_launches", 0)),
         "cpi_iterations": st["cpi_iterations"], "violations": len(rep["violations"]),
-        "iteration_shapes_count_ms": st.get("iteration_shapes"),
+        "cpi_busy_ms": round(st.get("cpi_busy_ms", 0.0), 2),
+        "cpi_lent_iterations": st.get("cpi_lent_iterations"),
+        "iteration_shapes_count_ms_rows_ctx": st.get("iteration_shapes"),
         "clocks": clocks, "e2e": e2e, "roofline": roof, "kernels": classes[:8],
     }
     if not args.no_cpu_baseline and world == 1:

@@ -146,6 +146,9 @@ int ck_device_sms(void);
  * verify the SM partition of co-located workers. */
 int ck_smid_probe(int* hits, int n_ctas, void* stream);
 
+/* Diagnostic: occupy `stream` for `us` microseconds (one warp spinning on the timer). */
+int ck_spin(int us, void* stream);
+
 /* Diagnostic: stream `bytes` of `buf` with `ctas` CTAs; mode 0 = LDG.128, 1 = TMA
  * 128x64 bf16 boxes over a [rows][4096] matrix (the GEMM's weight pattern), 2 =
  * cp.async.bulk 16 KiB chunks. Time it with events on `stream`. */

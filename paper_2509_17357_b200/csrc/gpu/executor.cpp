@@ -51,6 +51,10 @@ struct EngineOptions {
     // (ck_mega_decode: one cooperative launch per pass; measured slower on B200, kept
     // selectable for experiments — see DESIGN.md)
     bool persistent_decode = false;
+    // co-located pair with a green-context split: CPI iterations launched while the PPI
+    // has nothing in flight run on all SMs (the PPI's share is idle); PPI work issued
+    // behind such an iteration waits for it, so the two never contend for SMs
+    bool sm_lending = true;
 };
 
 EngineOptions parse_engine_options(const std::string& text) {
@@ -84,6 +88,7 @@ EngineOptions parse_engine_options(const std::string& text) {
         else if (k == "seed") o.seed = std::stoull(v);
         else if (k == "prompt_seed") o.prompt_seed = std::stoull(v);
         else if (k == "profile") o.profile = v == "1" || v == "true";
+        else if (k == "sm_lending") o.sm_lending = v == "1" || v == "true";
         else if (k == "decode_forward") {
             if (v != "layered" && v != "persistent")
                 throw std::invalid_argument("engine options: decode_forward = layered | persistent");
@@ -131,6 +136,7 @@ struct GpuEngine::Impl {
     std::shared_ptr<gpu::Weights> w_ppi, w_cpi;
     std::unique_ptr<gpu::KvPool> pool_ppi, pool_cpi;
     cudaStream_t s_ppi = nullptr, s_cpi = nullptr, s_copy = nullptr;
+    cudaStream_t s_cpi_full = nullptr;  // primary-context stream for lent (all-SM) CPI iterations
     std::unique_ptr<gpu::Worker> ppi, cpi;
     std::unique_ptr<gpu::SmPartition> part;
     std::string partition_mode = "none";
@@ -170,6 +176,8 @@ struct GpuEngine::Impl {
                 ppi_ctas = part->ppi_sms;
                 cpi_ctas = part->cpi_sms;
                 partition_mode = "green-context";
+                if (opt.sm_lending)
+                    check_cuda(cudaStreamCreateWithPriority(&s_cpi_full, cudaStreamNonBlocking, hi), "stream");
             } else {
                 ppi_ctas = opt.ppi_sms;  // fallback: only the PPI's GEMM grid is capped
                 partition_mode = "grid-cap";
@@ -203,6 +211,7 @@ struct GpuEngine::Impl {
         }
         ppi.reset();
         cpi.reset();
+        if (s_cpi_full) cudaStreamDestroy(s_cpi_full);
         if (part) {
             part.reset();  // owns the green-context streams
         } else {
@@ -217,7 +226,8 @@ struct GpuEngine::Impl {
     std::string describe(bool probe) {
         std::ostringstream o;
         o << "{\"mode\": \"" << partition_mode << "\", \"device_sms\": " << sms << ", \"ppi_sms\": "
-          << (ppi_ctas ? ppi_ctas : sms) << ", \"cpi_sms\": " << cpi_sm_count();
+          << (ppi_ctas ? ppi_ctas : sms) << ", \"cpi_sms\": " << cpi_sm_count()
+          << ", \"sm_lending\": " << (s_cpi_full ? "true" : "false");
         if (probe) {
             auto seen = [&](int dev, cudaStream_t st) {
                 check_cuda(cudaSetDevice(dev), "cudaSetDevice");
@@ -380,6 +390,10 @@ class PairExecutor : public sched::Executor {
             check_cuda(cudaStreamWaitEvent(E.s_ppi, ppi_fence, 0), "wait fence");
             ppi_fence = nullptr;
         }
+        if (last_lent && last_cpi) {  // the in-flight CPI iteration holds the PPI's SMs too
+            check_cuda(cudaStreamWaitEvent(E.s_ppi, last_cpi, 0), "wait lent iteration");
+            last_lent = false;
+        }
         TokenBufs& tb = ppi_tok();
         const Request& r = trace.requests[w.rid];
         for (long long start = 0; start < w.tokens; start += E.opt.ppi_chunk) {
@@ -434,9 +448,17 @@ class PairExecutor : public sched::Executor {
 
     uint64_t iteration(const sched::IterWork& w) override {
         check_cuda(cudaSetDevice(E.opt.cpi_device), "cudaSetDevice");
+        // SM lending: nothing in flight on the PPI -> this iteration may use every SM
+        const bool lend = E.opt.wall && E.s_cpi_full && done_q[0].empty();
+        cudaStream_t cur = lend ? E.s_cpi_full : E.s_cpi;
+        if (cur != cpi_stream) {  // keep CPI iterations in order across the two streams
+            if (last_cpi) check_cuda(cudaStreamWaitEvent(cur, last_cpi, 0), "wait previous iteration");
+            cpi_stream = cur;
+            E.cpi->set_launch(cur, lend ? 0 : E.cpi_ctas);
+        }
         auto need = [&](int rid) {
             if (xfer_pending[rid]) {
-                check_cuda(cudaStreamWaitEvent(E.s_cpi, xfer_ev[rid], 0), "wait handoff");
+                check_cuda(cudaStreamWaitEvent(cur, xfer_ev[rid], 0), "wait handoff");
                 xfer_pending[rid] = 0;
             }
         };
@@ -452,17 +474,24 @@ class PairExecutor : public sched::Executor {
                               out_off[w.chunk_rid]);
         }
         for (int rid : w.finishers) need(rid);
-        if (!batch.d_len.empty()) batch.plan_decode_splits(E.spec.n_kv_heads, 2 * E.cpi_sm_count());
+        if (!batch.d_len.empty())
+            batch.plan_decode_splits(E.spec.n_kv_heads, 2 * (lend ? E.sms : E.cpi_sm_count()));
+        if (E.opt.wall) {  // device-side start of this iteration (busy time = end - start)
+            iter_start = take_event();
+            check_cuda(cudaEventRecord(iter_start, cur), "event record");
+        }
         E.cpi->forward(batch, *E.pool_cpi, static_cast<int*>(E.tok_cpi.prompt.p),
                        static_cast<long long*>(E.tok_cpi.prompt_off.p), static_cast<int*>(E.tok_cpi.last_tok.p),
                        static_cast<int*>(E.tok_cpi.out_tok.p));
         iters++;
+        lent_iters += lend ? 1 : 0;
+        last_lent = lend;
         iter_rows += batch.rows();
         decode_rows += static_cast<long long>(w.decoders.size());
         for (const sched::DecodeRow& d : w.decoders) decode_keys += d.ctx;
         chunk_rows += w.chunk_len;
-        last_cpi = record(E.s_cpi, last_cpi);
-        return complete(E.s_cpi, 2);
+        last_cpi = record(cur, last_cpi);
+        return complete(cur, 2);
     }
 
     void release(int instance, int rid) override {
@@ -478,6 +507,8 @@ class PairExecutor : public sched::Executor {
     bool wall_clock() const override { return E.opt.wall; }
 
     void start() override {
+        E.cpi->set_launch(E.s_cpi, E.cpi_ctas);
+        cpi_stream = E.s_cpi;
         launches0_cpi = E.cpi->launches;
         launches0_ppi = E.ppi->launches;
         check_cuda(cudaSetDevice(E.opt.cpi_device), "cudaSetDevice");
@@ -510,6 +541,13 @@ class PairExecutor : public sched::Executor {
                 check_cuda(cudaEventElapsedTime(&ms, q == 0 ? t0_ppi : t0_cpi, t.ev), "elapsed");
                 t.t = ms;
                 t.done = true;
+                if (t.start) {
+                    float busy = 0.f;
+                    check_cuda(cudaEventElapsedTime(&busy, t.start, t.ev), "elapsed");
+                    cpi_busy_ms += busy;
+                    spare.push_back(t.start);
+                    t.start = nullptr;
+                }
             }
             if (best < 0 || t.t < best_t) {
                 best = q;
@@ -541,14 +579,16 @@ class PairExecutor : public sched::Executor {
         check_cuda(cudaSetDevice(E.opt.cpi_device), "cudaSetDevice");
         check_cuda(cudaStreamSynchronize(E.s_copy), "sync copy");
         check_cuda(cudaStreamSynchronize(E.s_cpi), "sync cpi");
+        if (E.s_cpi_full) check_cuda(cudaStreamSynchronize(E.s_cpi_full), "sync cpi (lent)");
         float ms = 0.f;
         cudaEvent_t end;
         check_cuda(cudaEventCreate(&end), "event");
-        check_cuda(cudaEventRecord(end, E.s_cpi), "event");
+        check_cuda(cudaEventRecord(end, cpi_stream ? cpi_stream : E.s_cpi), "event");
         check_cuda(cudaEventSynchronize(end), "sync");
         check_cuda(cudaEventElapsedTime(&ms, t0_cpi, end), "elapsed");
         cudaEventDestroy(end);
         gpu_ms = ms;
+        E.cpi->set_launch(E.s_cpi, E.cpi_ctas);
         if (opts.host_tokens) {
             check_cuda(cudaMemcpy(opts.host_tokens, E.tok_cpi.out_tok.p, static_cast<size_t>(total_out) * 4,
                                   cudaMemcpyDeviceToHost),
@@ -566,7 +606,7 @@ class PairExecutor : public sched::Executor {
               << ", \"bytes\": " << k.bytes << ", \"flops\": " << k.flops << "}" << (comma ? ", " : "");
         };
         s.precision(10);
-        s << "{\"gpu_ms\": " << gpu_ms << ", \"cpi_iterations\": " << iters << ", \"iter_rows\": " << iter_rows
+        s << "{\"gpu_ms\": " << gpu_ms << ", \"cpi_busy_ms\": " << cpi_busy_ms << ", \"cpi_iterations\": " << iters << ", \"cpi_lent_iterations\": " << lent_iters << ", \"iter_rows\": " << iter_rows
           << ", \"decode_rows\": " << decode_rows << ", \"decode_keys\": " << decode_keys
           << ", \"chunk_rows\": " << chunk_rows << ", \"prefill_tokens\": " << prefill_tokens
           << ", \"handoffs\": " << handoffs << ", \"handoff_bytes\": " << handoff_bytes
@@ -607,7 +647,12 @@ class PairExecutor : public sched::Executor {
         cudaEvent_t ev;
         bool done;
         double t;
+        cudaEvent_t start;  // CPI iterations: event recorded before the first kernel
     };
+    cudaEvent_t iter_start = nullptr;
+    cudaStream_t cpi_stream = nullptr;  // stream the latest CPI iteration went to
+    bool last_lent = false;
+    long long lent_iters = 0;
     std::deque<Tick> done_q[3];
     std::vector<cudaEvent_t> spare;
     uint64_t next_ticket = 1;
@@ -616,7 +661,7 @@ class PairExecutor : public sched::Executor {
 
   public:
     long long launches0_cpi = 0, launches0_ppi = 0, copy_launches = 0;
-    double gpu_ms = 0;
+    double gpu_ms = 0, cpi_busy_ms = 0;
     long long iters = 0, iter_rows = 0, decode_rows = 0, decode_keys = 0, chunk_rows = 0, prefill_tokens = 0;
     long long handoffs = 0;
     double handoff_bytes = 0, h2d_bytes = 0, d2h_bytes = 0;
@@ -631,6 +676,13 @@ class PairExecutor : public sched::Executor {
     uint64_t complete(cudaStream_t s, int q) {
         const uint64_t t = next_ticket++;
         if (!E.opt.wall) return t;  // virtual clock: completions come from the cost model
+        cudaEvent_t ev = take_event();
+        check_cuda(cudaEventRecord(ev, s), "event record");
+        done_q[q].push_back(Tick{t, ev, false, 0.0, q == 2 ? iter_start : nullptr});
+        if (q == 2) iter_start = nullptr;
+        return t;
+    }
+    cudaEvent_t take_event() {
         cudaEvent_t ev;
         if (!spare.empty()) {
             ev = spare.back();
@@ -638,9 +690,7 @@ class PairExecutor : public sched::Executor {
         } else {
             check_cuda(cudaEventCreate(&ev), "event");
         }
-        check_cuda(cudaEventRecord(ev, s), "event record");
-        done_q[q].push_back(Tick{t, ev, false, 0.0});
-        return t;
+        return ev;
     }
 };
 
@@ -697,7 +747,12 @@ double GpuEngine::time_pass(const ClusterConfig& cfg, int worker, int n_dec, int
     check_cuda(cudaEventCreate(&a), "event");
     check_cuda(cudaEventCreate(&b), "event");
     std::vector<float> t;
+    // CRONUS_PASS_PRELOAD=1: hold the stream while the host enqueues the pass, so the
+    // measurement excludes host launch throughput (compare with the default).
+    const char* pre = std::getenv("CRONUS_PASS_PRELOAD");
+    const bool preload = pre && pre[0] == '1';
     for (int r = 0; r < reps + 1; ++r) {
+        if (preload) check_ck(ck_spin(20000, st), "spin");
         check_cuda(cudaEventRecord(a, st), "event");
         W.forward(batch, pool, static_cast<int*>(tb.prompt.p), static_cast<long long*>(tb.prompt_off.p),
                   static_cast<int*>(tb.last_tok.p), static_cast<int*>(tb.out_tok.p));
@@ -765,6 +820,7 @@ RunReport GpuEngine::run(const ClusterConfig& cfg, const Trace& trace, const Gpu
         struct Bin {
             long long n = 0;
             double ms = 0;
+            long long rows = 0, ctx = 0;
         };
         std::map<std::string, Bin> bins;
         for (const auto& it : iters) {
@@ -773,13 +829,18 @@ RunReport GpuEngine::run(const ClusterConfig& cfg, const Trace& trace, const Gpu
             Bin& b = bins[std::string(it.chunk_len > 0 ? "chunk+" : "decode ") + db];
             b.n++;
             b.ms += it.t_end - it.t_start;
+            b.rows += it.n_decode;
+            b.ctx += it.decode_ctx_sum;
         }
         std::string js = ex.stats();
         std::ostringstream h;
         h << ", \"iteration_shapes\": {";
         bool first = true;
         for (const auto& [k, b] : bins) {
-            h << (first ? "" : ", ") << "\"" << k << "\": [" << b.n << ", " << b.ms << "]";
+            // [iterations, wall ms, mean decoders per iteration, mean decode context]
+            h << (first ? "" : ", ") << "\"" << k << "\": [" << b.n << ", " << b.ms << ", "
+              << static_cast<double>(b.rows) / std::max<long long>(1, b.n) << ", "
+              << static_cast<double>(b.ctx) / std::max<long long>(1, b.rows) << "]";
             first = false;
         }
         h << "}}";

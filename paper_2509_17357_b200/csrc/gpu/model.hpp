@@ -147,6 +147,12 @@ class Worker {
     cudaStream_t stream() const { return stream_; }
     void set_profiling(bool on) { profile_ = on; }
     void set_persistent_decode(bool on) { persistent_ = on; }
+    // Switch the stream / persistent-grid cap later passes launch on (SM lending). The
+    // caller orders the streams.
+    void set_launch(cudaStream_t s, int max_ctas) {
+        stream_ = s;
+        max_ctas_ = max_ctas;
+    }
     void collect_stats();  // fold finished profiling events into stats (synchronizes)
     void reset_stats() {
         stat_decode_attn = stat_prefill_attn = stat_gemm_stream = stat_gemm_tc = stat_other = stat_forward = {};

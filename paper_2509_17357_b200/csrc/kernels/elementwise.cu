@@ -292,6 +292,15 @@ __global__ void kv_copy_kernel(const uint4* __restrict__ src, const int* __restr
     for (; i < n; i += blockDim.x) dst[d0 + i] = src[s0 + i];
 }
 
+// Diagnostic: hold the stream for `ns` nanoseconds (lets the host enqueue ahead).
+__global__ void spin_kernel(unsigned long long ns) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+    do {
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    } while (t - t0 < ns);
+}
+
 __global__ void smid_probe_kernel(int* hits) {
     pdl_wait();
     pdl_launch();
@@ -400,6 +409,11 @@ int ck_kv_copy(const void* src_pool, const int* src_ids, void* dst_pool, const i
     const dim3 grid(n_blocks, static_cast<unsigned>((block_vec + chunk_vec - 1) / chunk_vec));
     return launch_pdl(kv_copy_kernel, dim3(grid), dim3(256), 0, S(stream), static_cast<const uint4*>(src_pool), src_ids,
                                                 static_cast<uint4*>(dst_pool), dst_ids, block_vec, chunk_vec);
+}
+
+int ck_spin(int us, void* stream) {
+    spin_kernel<<<1, 32, 0, S(stream)>>>(static_cast<unsigned long long>(us) * 1000ull);
+    return static_cast<int>(cudaGetLastError());
 }
 
 int ck_smid_probe(int* hits, int n_ctas, void* stream) {

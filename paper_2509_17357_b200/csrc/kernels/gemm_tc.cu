@@ -22,7 +22,11 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
+#include <vector>
 #include <unordered_map>
 
 #include "common.cuh"
@@ -48,7 +52,16 @@ struct GemmParams {
     int stream_k;
     long long iters;
     ck_gemm_fuse fuse;
+    unsigned long long* probe;  // dev (CRONUS_GEMM_PROBE=1): per-CTA timeline stamps, else null
 };
+
+__device__ __forceinline__ void probe_stamp(const GemmParams& p, int slot) {
+    if (p.probe != nullptr) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        p.probe[blockIdx.x * 6 + slot] = t;
+    }
+}
 
 // ------------------------------------------------------------------ fused tile finalize
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
@@ -193,6 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) probe_stamp(p, 0);
     // Everything above overlaps the previous kernel under PDL. Only the activations X
     // and the output depend on it: the producer streams the first stages' WEIGHT tiles
     // before griddepcontrol.wait, the epilogue waits before its first store, and the
@@ -221,6 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
             }
             pdl_wait();
+            probe_stamp(p, 1);
             // (2) the activation tiles of the prefetched stages
             for (int i = 0; i < n_pre; ++i)
                 tma_load_2d_hint(sB + i * C::kBBytes, &tmX, &full[i], pre_kb[i] * kTileK, pre_mt[i] * BN, keep);
@@ -264,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
+                    if (p.probe != nullptr && p.probe[blockIdx.x * 6 + 2] == 0) probe_stamp(p, 2);
                     const uint32_t a0 = smem_u32(sA + stage * C::kABytes);
                     const uint32_t b0 = smem_u32(sB + stage * C::kBBytes);
 #pragma unroll
@@ -280,6 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }
+            probe_stamp(p, 3);
         }
     } else {
         // ------------------------------------------------------------ epilogue
@@ -380,6 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 epi_bar();
             }
         }
+        if (warp == 2 && lane == 0) probe_stamp(p, 4);
     }
 
     tc_fence_before();
@@ -475,7 +493,35 @@ int launch(const CUtensorMap& mw, const CUtensorMap& mx, GemmParams p, int max_c
     }
     const long long work = p.stream_k ? p.iters : p.units;
     const int grid = static_cast<int>(std::min<long long>(work, max_ctas > 0 ? max_ctas : num_sms()));
-    return launch_pdl(gemm_tc_kernel<BN>, dim3(grid), dim3(kThreads), C::kSmem, s, mw, mx, p);
+    static const bool probe = [] {
+        const char* e = std::getenv("CRONUS_GEMM_PROBE");
+        return e && e[0] == '1';
+    }();
+    if (!probe) return launch_pdl(gemm_tc_kernel<BN>, dim3(grid), dim3(kThreads), C::kSmem, s, mw, mx, p);
+    // dev: per-CTA timeline (entry, after dependency wait, first stage ready, last MMA
+    // issued, epilogue done), printed relative to the earliest CTA entry
+    static unsigned long long* buf = nullptr;
+    if (!buf) cudaMalloc(&buf, 1024 * 6 * sizeof(unsigned long long));
+    cudaMemsetAsync(buf, 0, grid * 6 * sizeof(unsigned long long), s);
+    p.probe = buf;
+    const int rc = launch_pdl(gemm_tc_kernel<BN>, dim3(grid), dim3(kThreads), C::kSmem, s, mw, mx, p);
+    std::vector<unsigned long long> h(grid * 6);
+    cudaMemcpyAsync(h.data(), buf, h.size() * 8, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    unsigned long long t0 = ~0ull;
+    for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[c * 6]);
+    std::fprintf(stderr, "[gemm probe] M=%d N=%d K=%d BN=%d grid=%d sk=%d:", p.M, p.N, p.K, BN, grid, p.stream_k);
+    const char* names[5] = {"entry", "dep_ok", "first_full", "last_mma", "epi_done"};
+    for (int k = 0; k < 5; ++k) {
+        std::vector<double> v;
+        for (int c = 0; c < grid; ++c)
+            if (h[c * 6 + k]) v.push_back((h[c * 6 + k] - t0) * 1e-3);
+        std::sort(v.begin(), v.end());
+        if (!v.empty())
+            std::fprintf(stderr, " %s=%.1f/%.1f/%.1f", names[k], v.front(), v[v.size() / 2], v.back());
+    }
+    std::fprintf(stderr, " us\n");
+    return rc;
 }
 
 }  // namespace
@@ -504,7 +550,7 @@ int gemm_impl(const void* W, const void* X, void* out, const void* bias, int M, 
     if (N % kTileN != 0 || K % kTileK != 0 || N <= 0 || K <= 0) return static_cast<int>(cudaErrorInvalidValue);
     if ((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(X)) & 15) return static_cast<int>(cudaErrorMisalignedAddress);
     if (epi < CK_EPI_BF16 || epi > CK_EPI_RED_F32) return static_cast<int>(cudaErrorInvalidValue);
-    const int BN = M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
+    const int BN = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
     GemmParams p{};
     p.out = out;
     p.bias = static_cast<const __nv_bfloat16*>(bias);
@@ -540,6 +586,7 @@ int gemm_impl(const void* W, const void* X, void* out, const void* bias, int M, 
     if (rc) return rc;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     switch (BN) {
+        case 16: return launch<16>(mw, mx, p, max_ctas, s);
         case 32: return launch<32>(mw, mx, p, max_ctas, s);
         case 64: return launch<64>(mw, mx, p, max_ctas, s);
         case 128: return launch<128>(mw, mx, p, max_ctas, s);

@@ -149,3 +149,26 @@ def test_persistent_decode_forward(model, cfg_name):
     total, exact = check_tokens(t, res.extra["tokens"], [0, 5, 11, 23], model=model, splits=splits)
     assert exact >= 0.95 * total
     eng.close()
+
+
+def test_wall_clock_sm_lending():
+    """Green-context pair: CPI iterations issued while the PPI is idle run on every SM
+    (primary-context stream); tokens and invariants are unaffected."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2509_17357_b200.serving import GpuEngine
+    eng = GpuEngine(model="tiny", clock="wall", ppi_sms=40)
+    if eng.describe()["mode"] != "green-context":
+        eng.close()
+        pytest.skip("no green-context partition on this device")
+    cfg = load_cfg("a100_a10_llama8b")
+    t = c1_trace()
+    res = eng.serve(cfg, t, want_tokens=True)
+    rep = json.loads(res.json)
+    assert rep["violations"] == [] and rep["completed"] == len(t)
+    st = res.extra["stats"]
+    assert 0 < st["cpi_lent_iterations"] <= st["cpi_iterations"]
+    splits = [r["partial_prefill_len"] for r in rep["records"]]
+    total, exact = check_tokens(t, res.extra["tokens"], [0, 7, 40, 63], splits=splits)
+    assert exact >= 0.95 * total
+    eng.close()

@@ -8,7 +8,7 @@ from paper_2509_17357_b200.serving import GpuEngine
 cfg = open("tests/golden/configs/b200_llama8b_coloc.cfg").read()
 model = sys.argv[1] if len(sys.argv) > 1 else "llama3-8b"
 shapes = sys.argv[2:] or [f"{n}x{c}" for c in (512, 2048) for n in (1, 8, 16, 32, 48, 64)]
-eng = GpuEngine(model=model, clock="wall", ppi_sms=40,
+eng = GpuEngine(model=model, clock="wall", ppi_sms=int(os.environ.get("PPI_SMS", "40")),
                 decode_forward="persistent" if os.environ.get("CRONUS_MEGA") == "1" else "layered")
 out = {}
 for sh in shapes:

@@ -109,6 +109,19 @@ int ck_attn_decode(const void* q, const void* kv_pool, const int* bt, const int*
                    int blocks_per_split, float* ws, int* tickets, void* out, int nq, int nkv, int layer,
                    int n_layers, float scale, void* stream);
 
+/* Same op, production path: K/V rings filled by TMA (2-D map over the pool viewed as
+ * [pool_blocks * n_layers * 2 * nkv * 16 rows][128]) and each work item served by a
+ * thread-block CLUSTER of `cluster` CTAs (1..16) that split the item's blocks and merge
+ * through distributed shared memory. work[i] = seq << 16 | part; a sequence's parts
+ * (seq_item0) are evened out to ceil(nblocks / nparts) blocks; parts of one sequence
+ * merge through ws / tickets as in ck_attn_decode. Partially filled last blocks are
+ * read whole and masked, so never-written slots must hold finite values (the engine
+ * zero-fills its pools). pool rows must be < 2^31. */
+int ck_attn_decode_tma(const void* q, const void* kv_pool, long long pool_blocks, const int* bt, const int* seq_row,
+                       const int* seq_len, const int* seq_bt, const int* seq_item0, const int* work, int n_work,
+                       int n_seq, int cluster, float* ws, int* tickets, void* out, int nq, int nkv, int layer,
+                       int n_layers, float scale, void* stream);
+
 /* Prefill/chunk attention, causal: query rows [q_row0, q_row0+q_len) sit at
  * positions [pos0, pos0+q_len); keys [0, pos0+q_len) from the paged pool via bt. */
 int ck_attn_prefill(const void* q, const void* kv_pool, const int* bt, int q_row0, int q_len, int pos0, void* out,

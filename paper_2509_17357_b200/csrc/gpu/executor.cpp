@@ -475,7 +475,8 @@ class PairExecutor : public sched::Executor {
         }
         for (int rid : w.finishers) need(rid);
         if (!batch.d_len.empty())
-            batch.plan_decode_splits(E.spec.n_kv_heads, 2 * (lend ? E.sms : E.cpi_sm_count()));
+            batch.plan_decode(E.spec.n_kv_heads, 2 * (lend ? E.sms : E.cpi_sm_count()),
+                              !E.opt.persistent_decode && gpu::decode_cluster_kernel());
         if (E.opt.wall) {  // device-side start of this iteration (busy time = end - start)
             iter_start = take_event();
             check_cuda(cudaEventRecord(iter_start, cur), "event record");
@@ -741,8 +742,9 @@ double GpuEngine::time_pass(const ClusterConfig& cfg, int worker, int n_dec, int
         tables.push_back(blocks_for(chunk_pos0 + chunk_len));
         batch.add_prefill(0, chunk_pos0, chunk_len, tables.back(), true, 0);
     }
-    if (n_dec > 0) batch.plan_decode_splits(E.spec.n_kv_heads, 2 * (worker == 0 ? (E.ppi_ctas ? E.ppi_ctas : E.sms)
-                                                                             : E.cpi_sm_count()));
+    if (n_dec > 0)
+        batch.plan_decode(E.spec.n_kv_heads, 2 * (worker == 0 ? (E.ppi_ctas ? E.ppi_ctas : E.sms) : E.cpi_sm_count()),
+                          !E.opt.persistent_decode && gpu::decode_cluster_kernel());
     cudaEvent_t a, b;
     check_cuda(cudaEventCreate(&a), "event");
     check_cuda(cudaEventCreate(&b), "event");

@@ -209,6 +209,7 @@ void Batch::plan_decode_splits(int n_kv_heads, int slots) {
         bps *= 2;
     }
     blocks_per_split = bps;
+    decode_cluster = 0;
     d_item0.clear();
     d_work.clear();
     for (size_t s = 0; s < d_len.size(); ++s) {
@@ -218,6 +219,40 @@ void Batch::plan_decode_splits(int n_kv_heads, int slots) {
         for (int i = 0; i < ns; ++i) d_work.push_back(static_cast<int>(s << 16) | i);
     }
     d_item0.push_back(static_cast<int>(d_work.size()));
+}
+
+void Batch::plan_decode_clusters(int n_kv_heads, int slots) {
+    // One wave of `slots` resident CTAs: every (sequence, kv head) pair gets a cluster of
+    // C CTAs (C = power of two <= 16, as large as the wave allows while each CTA keeps
+    // >= 4 blocks, one per warp); a sequence more than ~2x longer than its fair share
+    // per cluster is cut into parts (merged through the global ticket path).
+    const long long n = static_cast<long long>(d_len.size());
+    long long total = 0;
+    for (int len : d_len) total += (len + 15) / 16;
+    const long long pairs = n * n_kv_heads;
+    int C = 1;
+    while (C < 16 && pairs * C * 2 <= slots && total * n_kv_heads >= pairs * C * 2 * 4) C *= 2;
+    const long long share = std::max<long long>(8, (total * n_kv_heads + slots - 1) / std::max(1, slots));
+    const long long cap = 2 * share * C;  // blocks one cluster may take before a sequence is cut
+    decode_cluster = C;
+    d_item0.clear();
+    d_work.clear();
+    for (size_t s = 0; s < d_len.size(); ++s) {
+        d_item0.push_back(static_cast<int>(d_work.size()));
+        const long long nblk = (d_len[s] + 15) / 16;
+        const long long parts = std::max<long long>(1, (nblk + cap - 1) / cap);
+        for (long long i = 0; i < parts; ++i) d_work.push_back(static_cast<int>(s << 16) | static_cast<int>(i));
+    }
+    d_item0.push_back(static_cast<int>(d_work.size()));
+    blocks_per_split = static_cast<int>(cap);
+}
+
+bool decode_cluster_kernel() {
+    static const bool on = [] {
+        const char* e = std::getenv("CRONUS_DECODE_CPASYNC");
+        return !(e && e[0] == '1');
+    }();
+    return on;
 }
 
 // ------------------------------------------------------------------ Worker
@@ -391,7 +426,8 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
 
     const int H = m.hidden, Q = m.qkv_n(), NQ = m.q_n(), F = m.ffn;
     const bool small = M <= 128;  // weight-streaming regime
-    if (b.p_len == 0 && n_dec == M && R == M && persistent_ && mega_ok_ && M <= ck_mega_max_rows()) {
+    if (b.p_len == 0 && n_dec == M && R == M && persistent_ && mega_ok_ && M <= ck_mega_max_rows() &&
+        b.decode_cluster == 0) {
         const PassMeta pm{row_rid,       row_pos,          bt,         D(o_d_row), D(o_d_len), D(o_d_bt), D(o_d_item0),
                           D(o_d_work), reinterpret_cast<const long long*>(D(o_s_out))};
         if (forward_mega(b, pool, pm, last_tok, out_tok)) {
@@ -453,10 +489,17 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         }
         if (n_dec > 0) {
             mark(a);
-            check_ck(ck_attn_decode(q_, pool.base, bt, D(o_d_row), D(o_d_len), D(o_d_bt), D(o_d_item0), D(o_d_work),
-                                    n_work, n_dec, b.blocks_per_split, attn_ws_, attn_tickets_, attn_, m.n_heads,
-                                    m.n_kv_heads, l, m.layers, scale, stream_),
-                     "attn_decode");
+            if (b.decode_cluster == 0)  // split plan (plan_decode_splits): cp.async kernel
+                check_ck(ck_attn_decode(q_, pool.base, bt, D(o_d_row), D(o_d_len), D(o_d_bt), D(o_d_item0),
+                                        D(o_d_work), n_work, n_dec, b.blocks_per_split, attn_ws_, attn_tickets_, attn_,
+                                        m.n_heads, m.n_kv_heads, l, m.layers, scale, stream_),
+                         "attn_decode");
+            else
+                check_ck(ck_attn_decode_tma(q_, pool.base, pool.blocks, bt, D(o_d_row), D(o_d_len), D(o_d_bt),
+                                            D(o_d_item0), D(o_d_work), n_work, n_dec, b.decode_cluster, attn_ws_,
+                                            attn_tickets_, attn_, m.n_heads, m.n_kv_heads, l, m.layers, scale,
+                                            stream_),
+                         "attn_decode_tma");
             ++launches;
             done(a, &stat_decode_attn, dec_keys * kv_tok_layer, 4.0 * m.n_heads * m.head_dim * dec_keys);
         }

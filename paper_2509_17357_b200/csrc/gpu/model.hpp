@@ -102,6 +102,9 @@ struct Batch {
     // decode sequences
     std::vector<int> d_row, d_len, d_bt, d_item0, d_work;
     int blocks_per_split = 16;
+    // 0: split plan (plan_decode_splits) for ck_attn_decode / the persistent pass;
+    // C >= 1: cluster plan (plan_decode_clusters) for ck_attn_decode_tma
+    int decode_cluster = 0;
     // one prefill sequence: rows [p_row0, p_row0 + p_len) at positions [p_pos0, ...)
     int p_row0 = 0, p_len = 0, p_pos0 = 0, p_bt = 0;
     // flat block table (all sequences)
@@ -118,6 +121,11 @@ struct Batch {
     void add_prefill(int rid, long long pos0, long long len, const std::vector<int32_t>& blocks, bool sample,
                      long long out_index);
     void plan_decode_splits(int n_kv_heads, int target_ctas);
+    void plan_decode_clusters(int n_kv_heads, int slots);
+    void plan_decode(int n_kv_heads, int slots, bool clusters) {
+        if (clusters) plan_decode_clusters(n_kv_heads, slots);
+        else plan_decode_splits(n_kv_heads, slots);
+    }
 };
 
 // Kernel-time accounting (CUDA events around selected launches, on the launching stream).
@@ -221,6 +229,10 @@ class Worker {
     void gemm(const void* W, const void* X, void* out, const void* bias, int M, int N, int K, int epi, int splits,
               const ck_gemm_fuse* fuse = nullptr);
 };
+
+// Decode attention kernel family: TMA + cluster (default) or the cp.async split kernel
+// (CRONUS_DECODE_CPASYNC=1).
+bool decode_cluster_kernel();
 
 void check_cuda(cudaError_t e, const char* what);
 void check_ck(int rc, const char* what);

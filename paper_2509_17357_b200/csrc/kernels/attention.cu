@@ -1,7 +1,8 @@
 // Paged attention over the block-major KV pool (see cronus_ck.h for the layout).
 //
 // Decode (one query token per sequence, HBM bound): split-KV "flash decoding" on
-//   mma.sync with a per-warp cp.async ring (see attn_decode_kernel). Algorithmic
+//   mma.sync with a per-warp K/V ring filled by TMA (attn_decode_tma_kernel; the
+//   cp.async-ring attn_decode_kernel is kept as ck_attn_decode for comparison). Algorithmic
 //   bytes = sum kv_len * 512 B per (layer, kv head) — K and V each read once.
 //
 // Prefill / chunk (tensor bound): FlashAttention-2 style with mma.sync
@@ -11,6 +12,10 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <cstdlib>
+
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "cronus_ck.h"
 #include "decode_attn.cuh"
@@ -18,6 +23,7 @@
 namespace {
 
 using namespace ck;
+namespace cg = cooperative_groups;
 
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kHD = 128;               // head dim
@@ -52,8 +58,8 @@ __global__ void __launch_bounds__(128)
     attn_prefill_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ pool,
                         const int* __restrict__ table, int q_row0, int q_len, int pos0, __nv_bfloat16* __restrict__ out,
                         int nq, int nkv, int layer, int n_layers, float qk_scale_log2) {
-    pdl_wait();
     pdl_launch();
+    pdl_wait();
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem_raw);
     __nv_bfloat16* sK = sQ + kPQ * kPad;          // [2][64][kPad]
@@ -233,8 +239,8 @@ constexpr int kDecTile = kDTileBytes;
 template <int G>
 __global__ void __launch_bounds__(128)
     attn_decode_kernel(DecodeAttnArgs a) {
-    pdl_wait();
     pdl_launch();
+    pdl_wait();
     extern __shared__ __align__(1024) uint8_t dsm[];
     __shared__ float small[2 * 64 + 4];
     decode_attn_item<G, kDecStages>(a, blockIdx.x, blockIdx.y, dsm, dsm + kDecTile, small, threadIdx.x, 1);
@@ -260,6 +266,244 @@ int launch_decode(const void* q, const void* pool, const int* bt, const int* seq
     return launch_pdl(attn_decode_kernel<G>, dim3(n_work, nkv), dim3(128), smem, st, a);
 }
 
+
+// ------------------------------------------------ decode, TMA + cluster variant (default)
+// Same math as attn_decode_kernel. Differences:
+//  * each warp's K/V ring is filled by TMA: lane 0 issues four 64x16 SWIZZLE_128B boxes
+//    (K and V halves, 8 KiB) per block on the slot's mbarrier, STAGES blocks in flight;
+//  * a work item (sequence, part) is served by a CLUSTER of C CTAs, each streaming 1/C
+//    of the item's blocks; the C partial results meet in rank 0's registers through
+//    distributed shared memory (one cluster barrier, no global round trip), so small
+//    batches can spread over many SMs without the split-merge tail. Only sequences too
+//    long for one cluster are cut into several parts, merged through the ticketed
+//    global path of dec_store;
+//  * PDL: every block except the sequence's last (the one the previous kernel appends
+//    the new token to) is requested before griddepcontrol.wait.
+// Requires finite stale slots in partially filled blocks (read, then masked): the
+// engine zero-fills its pools at allocation.
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cluster_size() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+
+template <int G, int STAGES>
+__global__ void __launch_bounds__(128)
+    attn_decode_tma_kernel(const __grid_constant__ CUtensorMap tm, DecodeAttnArgs a) {
+    extern __shared__ __align__(1024) uint8_t dsm[];
+    __shared__ float small[2 * 64 + 4];
+    __shared__ __align__(8) uint64_t bars[4][STAGES];
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const uint32_t C = cluster_size(), rank = cluster_rank();
+    const int item = blockIdx.x / C, kvh = blockIdx.y;
+    // per-pass metadata comes from host copies ordered before the pass: safe pre-wait
+    const int wk = a.work[item];
+    const int s = wk >> 16, part = wk & 0xffff;
+    const int len = a.seq_len[s];
+    const int nblk = (len + kDBlk - 1) / kDBlk;
+    const int nparts = a.seq_item0[s + 1] - a.seq_item0[s];
+    const int bpp = (nblk + nparts - 1) / nparts;  // blocks per part (parts evened out)
+    const int p0 = part * bpp, p1 = min(nblk, p0 + bpp);
+    const int bpc = (p1 - p0 + static_cast<int>(C) - 1) / static_cast<int>(C);  // blocks per cluster CTA
+    const int b0 = min(p1, p0 + static_cast<int>(rank) * bpc), b1 = min(p1, b0 + bpc);
+    const int first = b0 + warp;
+    const int mine = first < b1 ? (b1 - first + 3) / 4 : 0;
+    const int* table = a.bt + a.seq_bt[s];
+    uint8_t* sQ = dsm;
+    uint8_t* ring_all = dsm + kDTileBytes;
+    uint8_t* ring = ring_all + static_cast<size_t>(warp) * STAGES * 2 * kDTileBytes;
+    uint64_t* bar = bars[warp];
+    const int v_rows = a.nkv * kDBlk;  // pool rows from a head's K tile to its V tile
+    int issued = 0;
+    auto load = [&](int i) {  // lane 0
+        const int row = ((table[first + 4 * i] * a.n_layers + a.layer) * 2 * a.nkv + kvh) * kDBlk;
+        uint8_t* dK = ring + (i % STAGES) * 2 * kDTileBytes;
+        uint64_t* bb = &bar[i % STAGES];
+        mbar_arrive_expect_tx(bb, 2 * kDTileBytes);
+        tma_load_2d(dK, &tm, bb, 0, row);
+        tma_load_2d(dK + kDTileBytes / 2, &tm, bb, 64, row);
+        tma_load_2d(dK + kDTileBytes, &tm, bb, 0, row + v_rows);
+        tma_load_2d(dK + kDTileBytes + kDTileBytes / 2, &tm, bb, 64, row + v_rows);
+    };
+    const int pre = min(mine, STAGES);
+    pdl_launch();
+    if (lane == 0) {
+        tma_prefetch_desc(&tm);
+#pragma unroll
+        for (int i = 0; i < STAGES; ++i) mbar_init(&bar[i], 1);
+        fence_mbar_init();
+        while (issued < pre && first + 4 * issued != nblk - 1) load(issued++);
+    }
+    pdl_wait();
+    if (lane == 0)
+        while (issued < pre) load(issued++);
+    {  // Q (G rows, zero padded to 16) — written by the previous kernel
+        const __nv_bfloat16* qrow =
+            a.q + static_cast<size_t>(a.seq_row[s]) * a.nq * kDHD + static_cast<size_t>(kvh) * G * kDHD;
+        for (int c = t; c < 16 * 16; c += 128) {
+            const int r = c >> 4, ch = c & 15;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (r < G) v = *reinterpret_cast<const uint4*>(qrow + r * kDHD + ch * 8);
+            *reinterpret_cast<uint4*>(sQ + swz(r, ch)) = v;
+        }
+    }
+    __syncthreads();
+    uint32_t qf[8][4];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) ldsm_x4(qf[kk], sQ + swz(lane & 15, 2 * kk + (lane >> 4)));
+    float o[16][4];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int i = 0; i < mine; ++i) {
+        mbar_wait(&bar[i % STAGES], (i / STAGES) & 1);
+        const uint8_t* K = ring + (i % STAGES) * 2 * kDTileBytes;
+        dec_block<SwzTma128>(K, K + kDTileBytes, qf, o, m_run, l_run, (first + 4 * i) * kDBlk, len,
+                             a.qk_scale_log2, lane);
+        __syncwarp();
+        if (lane == 0 && issued < mine) load(issued++);  // refill the slot just consumed
+    }
+    float* res = reinterpret_cast<float*>(ring_all + kDResOff);
+    dec_merge_warps<G>(ring_all, small, o, m_run, l_run, t, 1, res);
+    if (C == 1) {
+        dec_store<G>(a, item, kvh, res, small, t, 1);
+        return;
+    }
+    // ---- cluster merge over distributed shared memory: CTA r folds the C per-CTA
+    // results for its 1/C slice of the G x 128 outputs (3C independent DSMEM loads
+    // per element, pipelined), then writes that slice of the output (or the part's
+    // partial, whose ticket rank 0 takes once every slice is written).
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();  // every CTA's res is complete
+    const int n_el = G * kDHD;
+    const int per = (n_el + static_cast<int>(C) - 1) / static_cast<int>(C);
+    const int e_end = min(n_el, (static_cast<int>(rank) + 1) * per);
+    const int row = a.seq_row[s];
+    const bool single = nparts == 1;
+    for (int e = static_cast<int>(rank) * per + t; e < e_end; e += 128) {
+        const int h = e / kDHD, d = e % kDHD;
+        float pm[16], pl[16], pa[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+            if (r < static_cast<int>(C)) {
+                const float* peer = cl.map_shared_rank(res, r);
+                pm[r] = peer[h * kDRes];
+                pl[r] = peer[h * kDRes + 1];
+                pa[r] = peer[h * kDRes + 2 + d];
+            }
+        float M = -INFINITY;
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+            if (r < static_cast<int>(C)) M = fmaxf(M, pm[r]);
+        float Ls = 0.f, A = 0.f;
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+            if (r < static_cast<int>(C)) {
+                const float f = pm[r] == -INFINITY ? 0.f : exp2f(pm[r] - M);
+                Ls += pl[r] * f;
+                A += pa[r] * f;
+            }
+        if (single) {
+            a.out[static_cast<size_t>(row) * a.nq * kDHD + (kvh * G + h) * kDHD + d] = f2bf(Ls > 0.f ? A / Ls : 0.f);
+        } else {
+            float* prt = a.ws + (static_cast<size_t>(item) * a.nq + kvh * G + h) * kDRes;
+            prt[2 + d] = A;
+            if (d == 0) {
+                prt[0] = M;
+                prt[1] = Ls;
+            }
+        }
+    }
+    if (!single) __threadfence();
+    cl.sync();  // peers' shared memory may be released after this; part's partial complete
+    if (single || rank != 0) return;
+    // several parts of one sequence: the last part to finish merges all partials
+    int* s_last = reinterpret_cast<int*>(small + 128);
+    if (t == 0) {
+        const int prev = atomicAdd(&a.tickets[s * a.nkv + kvh], 1);
+        *s_last = prev == nparts - 1;
+        if (*s_last) a.tickets[s * a.nkv + kvh] = 0;  // self-resetting
+    }
+    __syncthreads();
+    if (*s_last) {
+        __threadfence();
+        const int i0 = a.seq_item0[s], i1 = a.seq_item0[s + 1];
+        for (int i = t; i < n_el; i += 128) {
+            const int h = i / kDHD, d = i % kDHD;
+            const int hq = kvh * G + h;
+            float M = -INFINITY;
+            for (int it = i0; it < i1; ++it) M = fmaxf(M, __ldcg(a.ws + (static_cast<size_t>(it) * a.nq + hq) * kDRes));
+            float Ls = 0.f, A = 0.f;
+            for (int it = i0; it < i1; ++it) {
+                const float* prt = a.ws + (static_cast<size_t>(it) * a.nq + hq) * kDRes;
+                const float pmv = __ldcg(prt);
+                const float f = pmv == -INFINITY ? 0.f : exp2f(pmv - M);
+                Ls += __ldcg(prt + 1) * f;
+                A += __ldcg(prt + 2 + d) * f;
+            }
+            a.out[static_cast<size_t>(row) * a.nq * kDHD + hq * kDHD + d] = f2bf(Ls > 0.f ? A / Ls : 0.f);
+        }
+    }
+}
+
+template <int G, int STAGES>
+int launch_decode_tma(const CUtensorMap& tm, const DecodeAttnArgs& a, int n_work, int cluster, cudaStream_t st) {
+    constexpr int smem = kDTileBytes + 4 * STAGES * 2 * kDTileBytes;
+    static_assert(4 * STAGES * 2 * kDTileBytes >= kDResOff + 8 * kDRes * 4, "merge scratch must fit in the ring");
+    static unsigned mask = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(mask & (1u << dev))) {
+        cudaError_t e =
+            cudaFuncSetAttribute(attn_decode_tma_kernel<G, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return static_cast<int>(e);
+        e = cudaFuncSetAttribute(attn_decode_tma_kernel<G, STAGES>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return static_cast<int>(e);
+        mask |= 1u << dev;
+    }
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = cluster;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(n_work * cluster, a.nkv);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    // attribute 0 (PDL) is dropped under CRONUS_NO_PDL, like every other launch
+    cfg.attrs = pdl_enabled() ? attr : attr + 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    return static_cast<int>(cudaLaunchKernelEx(&cfg, attn_decode_tma_kernel<G, STAGES>, tm, a));
+}
+
+// Ring depth per warp: 3 (100 KiB per CTA, 2 CTAs per SM) unless CRONUS_DEC_STAGES says otherwise.
+int dec_stages() {
+    static const int v = [] {
+        const char* e = std::getenv("CRONUS_DEC_STAGES");
+        const int x = e ? std::atoi(e) : 3;
+        return (x == 2 || x == 4 || x == 6) ? x : 3;
+    }();
+    return v;
+}
+
+template <int G>
+int launch_decode_tma_g(const CUtensorMap& tm, const DecodeAttnArgs& a, int n_work, int cluster, cudaStream_t st) {
+    switch (dec_stages()) {
+        case 2: return launch_decode_tma<G, 2>(tm, a, n_work, cluster, st);
+        case 4: return launch_decode_tma<G, 4>(tm, a, n_work, cluster, st);
+        case 6: return launch_decode_tma<G, 6>(tm, a, n_work, cluster, st);
+        default: return launch_decode_tma<G, 3>(tm, a, n_work, cluster, st);
+    }
+}
+
 }  // namespace
 
 extern "C" int ck_attn_decode(const void* q, const void* kv_pool, const int* bt, const int* seq_row,
@@ -275,6 +519,31 @@ extern "C" int ck_attn_decode(const void* q, const void* kv_pool, const int* bt,
         case 4: return launch_decode<4>(q, kv_pool, bt, seq_row, seq_len, seq_bt, seq_item0, work, n_work, blocks_per_split, ws, tickets, out, nq, nkv, layer, n_layers, qk, st);
         case 7: return launch_decode<7>(q, kv_pool, bt, seq_row, seq_len, seq_bt, seq_item0, work, n_work, blocks_per_split, ws, tickets, out, nq, nkv, layer, n_layers, qk, st);
         case 8: return launch_decode<8>(q, kv_pool, bt, seq_row, seq_len, seq_bt, seq_item0, work, n_work, blocks_per_split, ws, tickets, out, nq, nkv, layer, n_layers, qk, st);
+        default: return static_cast<int>(cudaErrorInvalidValue);
+    }
+}
+
+extern "C" int ck_attn_decode_tma(const void* q, const void* kv_pool, long long pool_blocks, const int* bt,
+                                  const int* seq_row, const int* seq_len, const int* seq_bt, const int* seq_item0,
+                                  const int* work, int n_work, int n_seq, int cluster, float* ws, int* tickets,
+                                  void* out, int nq, int nkv, int layer, int n_layers, float scale, void* stream) {
+    if (n_seq <= 0 || n_work <= 0) return 0;
+    if (cluster < 1 || cluster > 16) return static_cast<int>(cudaErrorInvalidValue);
+    CUtensorMap tm;
+    const unsigned long long pool_rows = static_cast<unsigned long long>(pool_blocks) * n_layers * 2 * nkv * kBlk;
+    if (pool_rows >= (1ull << 31)) return static_cast<int>(cudaErrorInvalidValue);  // int32 TMA row coordinate
+    int rc = make_map_2d(kv_pool, pool_rows, kHD, kBlk, &tm);
+    if (rc) return rc;
+    const DecodeAttnArgs a{static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(kv_pool), bt,
+                           seq_row, seq_len, seq_bt, seq_item0, work, 0, ws, tickets,
+                           static_cast<__nv_bfloat16*>(out), nq, nkv, layer, n_layers, scale * kLog2e};
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    switch (nq / nkv) {
+        case 1: return launch_decode_tma_g<1>(tm, a, n_work, cluster, st);
+        case 2: return launch_decode_tma_g<2>(tm, a, n_work, cluster, st);
+        case 4: return launch_decode_tma_g<4>(tm, a, n_work, cluster, st);
+        case 7: return launch_decode_tma_g<7>(tm, a, n_work, cluster, st);
+        case 8: return launch_decode_tma_g<8>(tm, a, n_work, cluster, st);
         default: return static_cast<int>(cudaErrorInvalidValue);
     }
 }

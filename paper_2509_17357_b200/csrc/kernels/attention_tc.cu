@@ -136,8 +136,8 @@ __global__ void __launch_bounds__(192, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    pdl_wait();
     pdl_launch();
+    pdl_wait();
 
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
@@ -324,12 +324,16 @@ __global__ void __launch_bounds__(192, 1)
     }
 }
 
+
+}  // namespace
+
+namespace ck {
 // ------------------------------------------------------------------ host
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-int make_map(const void* ptr, unsigned long long rows, unsigned long long cols, unsigned box_rows, CUtensorMap* m) {
+int make_map_2d(const void* ptr, unsigned long long rows, unsigned long long cols, unsigned box_rows, CUtensorMap* m) {
     static std::mutex mu;
     static std::unordered_map<std::string, CUtensorMap> cache;
     char key[96];
@@ -363,18 +367,18 @@ int make_map(const void* ptr, unsigned long long rows, unsigned long long cols, 
     return 0;
 }
 
-}  // namespace
+}  // namespace ck
 
 extern "C" int ck_attn_prefill_tc(const void* q, int q_rows_total, const void* kv_pool, long long pool_blocks,
                                   const int* bt, int q_row0, int q_len, int pos0, void* out, int nq, int nkv, int layer,
                                   int n_layers, float scale, void* stream) {
     if (q_len <= 0) return 0;
     CUtensorMap mq, mkv;
-    int rc = make_map(q, static_cast<unsigned long long>(q_rows_total), static_cast<unsigned long long>(nq) * 128,
+    int rc = make_map_2d(q, static_cast<unsigned long long>(q_rows_total), static_cast<unsigned long long>(nq) * 128,
                       kQ, &mq);
     if (rc) return rc;
     const unsigned long long pool_rows = static_cast<unsigned long long>(pool_blocks) * n_layers * 2 * nkv * 16;
-    rc = make_map(kv_pool, pool_rows, 128, 16, &mkv);
+    rc = make_map_2d(kv_pool, pool_rows, 128, 16, &mkv);
     if (rc) return rc;
     static unsigned mask = 0;
     int dev = 0;

@@ -198,9 +198,13 @@ __device__ __forceinline__ void red_add_v4_f32(float* p, float a, float b, float
 
 // ---------------------------------------------------------------- PDL
 // Programmatic dependent launch: every kernel of the forward chain is launched with
-// programmatic stream serialization, waits for its producer grid at pdl_wait()
-// (after any prologue that touches no dependent data) and immediately lets its own
-// dependents launch, so launch latency and prologues overlap the previous kernel.
+// programmatic stream serialization and lets its dependents launch at entry
+// (pdl_launch before pdl_wait), then waits for its producer grid at pdl_wait() before
+// touching dependent data. A dependent grid is only scheduled once EVERY CTA of its
+// primary has triggered (so it can never starve the primary of SMs), and its own
+// pdl_wait covers the primary's completion, which in turn covered its primary's: the
+// next weight-streaming GEMM therefore takes each SM the moment the previous GEMM's CTA
+// leaves it and streams its weights while the small kernel in between still waits.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
@@ -228,6 +232,10 @@ namespace ck {
 // CRONUS_NO_PDL=1 launches without the attribute (griddepcontrol.* become no-ops):
 // required under Nsight Compute, whose kernel replay cannot coexist with dependents
 // already resident at griddepcontrol.wait.
+// Host: 2-D bf16 tensor map [rows][cols] (row-major), box = 64 columns x box_rows rows,
+// 128-B swizzle; cached per (ptr, shape, box). Defined in attention_tc.cu.
+int make_map_2d(const void* ptr, unsigned long long rows, unsigned long long cols, unsigned box_rows, CUtensorMap* m);
+
 inline bool pdl_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("CRONUS_NO_PDL");

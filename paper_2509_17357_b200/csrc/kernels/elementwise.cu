@@ -18,8 +18,8 @@ inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 // ---------------------------------------------------------------- init / tokens
 __global__ void init_uniform_kernel(__nv_bfloat16* out, long long n, uint64_t seed, uint64_t tid, float step,
                                     float offset) {
-    pdl_wait();
     pdl_launch();
+    pdl_wait();
     const uint64_t base = seed * 0x9E3779B97F4A7C15ull + tid * 0xD1B54A32D192ED03ull;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -31,8 +31,8 @@ __global__ void init_uniform_kernel(__nv_bfloat16* out, long long n, uint64_t se
 }
 
 __global__ void prompt_tokens_kernel(int* out, const int* req, const int* pos, int n, uint64_t seed, int vocab) {
-    pdl_wait();
     pdl_launch();
+    pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint64_t h = mix64(seed * 0x9E3779B97F4A7C15ull + static_cast<uint64_t>(static_cast<uint32_t>(req[i])) *
@@ -42,8 +42,8 @@ __global__ void prompt_tokens_kernel(int* out, const int* req, const int* pos, i
 }
 
 __global__ void rope_table_kernel(float* c, float* s, int max_pos, double theta) {
-    pdl_wait();
     pdl_launch();
+    pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= max_pos * 64) return;
     const int p = i >> 6, f = i & 63;
@@ -58,8 +58,8 @@ __global__ void rope_table_kernel(float* c, float* s, int max_pos, double theta)
 __global__ void embed_kernel(float* __restrict__ x, const __nv_bfloat16* __restrict__ emb, const int* row_rid,
                              const int* row_pos, const int* row_dec, const int* prompt, const long long* prompt_off,
                              const int* last_tok, int H) {
-    pdl_wait();
     pdl_launch();
+    pdl_wait();
     const int m = blockIdx.x;
     const int rid = row_rid[m];
     const int tok = row_dec[m] ? last_tok[rid] : prompt[prompt_off[rid] + row_pos[m]];
@@ -93,8 +93,8 @@ constexpr int kRmsMaxVec = 8;  // float4 per thread: H <= 8 * 4 * blockDim
 __global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ gamma,
                                __nv_bfloat16* __restrict__ out, const int* rows, int H, float eps,
                                float* __restrict__ zero, int zero_cols) {
-    pdl_wait();
     pdl_launch();
+    pdl_wait();
     __shared__ float red[32];
     const int r = blockIdx.x;
     const int src = rows ? rows[r] : r;
@@ -140,8 +140,8 @@ __global__ void qkv_rope_append_kernel(float* __restrict__ qkv, const __nv_bfloa
                                        const int* __restrict__ row_pos, const float* __restrict__ cos_tab,
                                        const float* __restrict__ sin_tab, int nq, int nkv, int layer, int n_layers,
                                        int zero_after) {
-    pdl_wait();
     pdl_launch();
+    pdl_wait();
     const int m = blockIdx.x, h = blockIdx.y * kQkvHeadsPerCta + (threadIdx.x >> 6), i = threadIdx.x & 63;
     if (h >= nq + 2 * nkv) return;
     const int pos = row_pos[m];
@@ -187,8 +187,8 @@ __global__ void qkv_rope_append_kernel(float* __restrict__ qkv, const __nv_bfloa
 // ---------------------------------------------------------------- SiLU * up
 __global__ void silu_mul_kernel(float* __restrict__ gu, __nv_bfloat16* __restrict__ act, long long n_pairs4,
                                 int zero_after) {
-    pdl_wait();
     pdl_launch();
+    pdl_wait();
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n_pairs4;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         // 4 (gate, up) pairs = 8 floats -> 4 bf16
@@ -222,8 +222,8 @@ __device__ __forceinline__ void arg_better(float& bv, int& bi, float v, int i) {
 __global__ void argmax_emit_kernel(const float* __restrict__ logits, int V, const int* rid, const long long* out_idx,
                                    int* last_tok, int* out_tok, float* __restrict__ pv, int* __restrict__ pi,
                                    int* __restrict__ tickets) {
-    pdl_wait();
     pdl_launch();
+    pdl_wait();
     __shared__ float sb[32];
     __shared__ int si[32];
     __shared__ int s_last;
@@ -274,8 +274,8 @@ __global__ void argmax_emit_kernel(const float* __restrict__ logits, int V, cons
 // vectors, 4 in flight per thread.
 __global__ void kv_copy_kernel(const uint4* __restrict__ src, const int* __restrict__ src_ids, uint4* __restrict__ dst,
                                const int* __restrict__ dst_ids, long long block_vec, long long chunk_vec) {
-    pdl_wait();
     pdl_launch();
+    pdl_wait();
     const long long b = blockIdx.x;
     const long long s0 = static_cast<long long>(src_ids[b]) * block_vec + blockIdx.y * chunk_vec;
     const long long d0 = static_cast<long long>(dst_ids[b]) * block_vec + blockIdx.y * chunk_vec;
@@ -302,8 +302,8 @@ __global__ void spin_kernel(unsigned long long ns) {
 }
 
 __global__ void smid_probe_kernel(int* hits) {
-    pdl_wait();
     pdl_launch();
+    pdl_wait();
     uint32_t sm;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
     if (threadIdx.x == 0) atomicAdd(&hits[sm], 1);
@@ -314,8 +314,8 @@ __global__ void smid_probe_kernel(int* hits) {
 }
 
 __global__ void copy_token_kernel(const int* src, long long si, int* dst, long long di, int* dst2, long long di2) {
-    pdl_wait();
     pdl_launch();
+    pdl_wait();
     const int v = src[si];
     dst[di] = v;
     if (dst2) dst2[di2] = v;

@@ -162,12 +162,16 @@ def attn_ref(q, k, v, qpos, scale):
     return torch.einsum("hnt,thd->nhd", s.softmax(-1), vv)
 
 
+@pytest.mark.parametrize("impl", ["tma", "cp_async"])
 @pytest.mark.parametrize("nq,nkv", [(2, 1), (32, 8), (28, 4), (4, 2)])
-def test_attn_decode(L, nq, nkv):
+def test_attn_decode(L, nq, nkv, impl):
     gen = torch.Generator(device="cuda").manual_seed(nq)
     layers, layer = 2, 1
     lens = [1, 15, 16, 17, 100, 333, 1024, 2049]
-    pool = make_pool(sum((l + 15) // 16 for l in lens) + 3, layers, nkv)
+    # cp.async zero-fills past the end (NaN garbage must not leak); TMA reads whole
+    # blocks and masks, so stale slots hold large finite garbage instead
+    pool = make_pool(sum((l + 15) // 16 for l in lens) + 3, layers, nkv,
+                     fill=float("nan") if impl == "cp_async" else 3e4)
     tables, ks, vs = fill_sequences(pool, layer, lens, nkv, gen)
     S = len(lens)
     rows = torch.arange(S, dtype=torch.int32, device="cuda") * 2 + 1  # non-trivial row mapping
@@ -175,7 +179,9 @@ def test_attn_decode(L, nq, nkv):
     q = torch.randn(M, nq * 128, device="cuda", generator=gen).bfloat16()
     bt = torch.cat(tables)
     offs = np.concatenate([[0], np.cumsum([len(t) for t in tables])[:-1]]).astype(np.int32)
-    for bps in (1, 3, 64):
+    # cp_async: blocks per split; tma: (blocks per part, cluster CTAs per part)
+    cases = [(1, 1), (3, 1), (64, 1)] if impl == "cp_async" else [(64, 1), (3, 1), (64, 2), (5, 4), (64, 8), (1000, 16)]
+    for bps, cluster in cases:
         work, item0 = [], []
         for s_i, ln in enumerate(lens):
             item0.append(len(work))
@@ -191,14 +197,20 @@ def test_attn_decode(L, nq, nkv):
         tickets = torch.zeros(S * nkv, dtype=torch.int32, device="cuda")
         out = torch.zeros(M, nq * 128, dtype=torch.bfloat16, device="cuda")
         scale = 1 / math.sqrt(128)
-        ok(L.ck_attn_decode(p(q), p(pool), p(bt), p(rows), p(t_len), p(t_off), p(t_item0), p(t_work),
-                            len(work), S, bps, p(ws), p(tickets), p(out), nq, nkv, layer, layers, scale, stream()))
+        if impl == "tma":
+            ok(L.ck_attn_decode_tma(p(q), p(pool), pool.shape[0], p(bt), p(rows), p(t_len), p(t_off), p(t_item0),
+                                    p(t_work), len(work), S, cluster, p(ws), p(tickets), p(out), nq, nkv, layer,
+                                    layers, scale, stream()))
+        else:
+            ok(L.ck_attn_decode(p(q), p(pool), p(bt), p(rows), p(t_len), p(t_off), p(t_item0), p(t_work),
+                                len(work), S, bps, p(ws), p(tickets), p(out), nq, nkv, layer, layers, scale,
+                                stream()))
         assert tickets.abs().sum() == 0  # self-resetting
         for s_i, ln in enumerate(lens):
             r = int(rows[s_i])
             ref = attn_ref(q[r].view(1, nq, 128), ks[s_i], vs[s_i], torch.tensor([ln - 1], device="cuda"), scale)
             got = out[r].float().view(1, nq, 128)
-            assert torch.allclose(got, ref, rtol=2e-2, atol=2e-2), (bps, ln, (got - ref).abs().max().item())
+            assert torch.allclose(got, ref, rtol=2e-2, atol=2e-2), (bps, cluster, ln, (got - ref).abs().max().item())
 
 
 @pytest.mark.parametrize("impl", ["mma", "tc"])

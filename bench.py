@@ -131,9 +131,33 @@ def peaks():
         return 6650.0, 1590.0, 1400.0, "fallback"
 
 
-def roofline(stats):
-    """Dominant kernel class of the profiled step -> roofline object (+ all classes)."""
+TRAFFIC = os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")
+
+
+def traffic_ratios():
+    """DRAM bytes / algorithmic bytes per kernel class from the committed ncu --set full
+    captures (tools/scripts/ncu_full.sh -> tools/ncu_traffic.py); latest capture wins."""
+    try:
+        caps = json.load(open(TRAFFIC))["captures"]
+    except Exception:
+        return {}
+    out = {}
+    for name, c in caps.items():
+        if c.get("traffic_ratio"):
+            out[c["class"]] = (c["traffic_ratio"], f"{os.path.relpath(TRAFFIC, ROOT)}:{name}")
+    return out
+
+
+def roofline(stats, partition=None):
+    """Dominant kernel class of the profiled step -> roofline object (+ all classes).
+
+    Tensor-bound classes also get `frac_partition`: the fraction of the peak scaled to
+    the SMs the worker owns (PPI 40 / CPI 108 of 148 in the co-located split; CPI
+    iterations on lent SMs make the CPI figure conservative)."""
     hbm, tf_burst, tf_sus, src = peaks()
+    ratios = traffic_ratios()
+    sms = {"ppi": (partition or {}).get("ppi_sms"), "cpi": (partition or {}).get("cpi_sms")}
+    dev_sms = (partition or {}).get("device_sms") or 148
     classes = []
     for worker in ("cpi", "ppi"):
         for name, k in stats[worker].items():
@@ -147,14 +171,22 @@ def roofline(stats):
             else:
                 ach = k["flops"] / k["launches"] / (ms_avg / 1e3) / 1e12
                 peak, unit = tf_sus, "TFLOP/s"
-            classes.append({"kernel": f"{worker}.{name}", "bound": bound, "achieved": round(ach, 1), "peak": peak,
-                            "unit": unit, "frac": round(ach / peak, 4), "launches": k["launches"],
-                            "share_ms": round(k["ms"], 2), "avg_us": round(1e3 * ms_avg, 2),
-                            "algorithmic_per_launch": (k["bytes"] if bound == "hbm" else k["flops"]) / k["launches"]})
+            ent = {"kernel": f"{worker}.{name}", "bound": bound, "achieved": round(ach, 1), "peak": peak,
+                   "unit": unit, "frac": round(ach / peak, 4), "launches": k["launches"],
+                   "share_ms": round(k["ms"], 2), "avg_us": round(1e3 * ms_avg, 2),
+                   "algorithmic_per_launch": (k["bytes"] if bound == "hbm" else k["flops"]) / k["launches"]}
+            if bound == "tensor" and sms.get(worker):
+                ent["frac_partition"] = round(ach / (peak * sms[worker] / dev_sms), 4)
+            if f"{worker}.{name}" in ratios:
+                r, src_t = ratios[f"{worker}.{name}"]
+                ent["traffic"] = round(r * k["bytes"] / k["launches"])
+                ent["traffic_ratio"] = r
+                ent["traffic_source"] = src_t
+            classes.append(ent)
     classes.sort(key=lambda c: -c["share_ms"])
     top = dict(classes[0]) if classes else {}
     if top:
-        top["traffic"] = None
+        top.setdefault("traffic", None)
         top["peak_source"] = f"MEASURED_PEAKS.json ({src}; {'sustained' if top['bound'] == 'tensor' else 'copy'})"
     return top, classes
 
@@ -263,7 +295,7 @@ def run_ours(args, rank, world):
     if not args.no_profile and driver:
         pr = eng.serve(cfg, sub, events=False, profile=True)
         prof_stats = pr.extra["stats"]
-        roof, classes = roofline(prof_stats)
+        roof, classes = roofline(prof_stats, prof_stats.get("partition"))
 
     if rank != 0:
         return None

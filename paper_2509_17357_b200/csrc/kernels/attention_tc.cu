@@ -43,8 +43,8 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr int kOffQ = 0;
 constexpr int kOffK = kOffQ + kTileBytes;          // 2 stages
 constexpr int kOffV = kOffK + 2 * kTileBytes;      // 2 stages
-constexpr int kOffP = kOffV + 2 * kTileBytes;      // 1 buffer
-constexpr int kOffBar = kOffP + kTileBytes;
+constexpr int kOffP = kOffV + 2 * kTileBytes;      // 2 buffers (softmax j+1 overlaps PV j)
+constexpr int kOffBar = kOffP + 2 * kTileBytes;
 constexpr int kSmemBytes = kOffBar + 256 + 1024;
 
 struct AttnParams {
@@ -89,6 +89,21 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
         "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
         : "memory");
 }
+// 2^x on the FMA pipe: Cody-Waite split x = i + f, f in [0, 1), cubic fit of 2^f (max
+// relative error 2.6e-4, far below the bf16 rounding P gets next); x < -127 -> ~0.
+__device__ __forceinline__ float exp2_poly(float x) {
+    x = fmaxf(x, -127.f);
+    const float xi = floorf(x);
+    const float f = x - xi;
+    const float pf = fmaf(fmaf(fmaf(0.07558665f, f, 0.22877255f), f, 0.69511601f), f, 1.0f);
+    return __int_as_float(__float_as_int(pf) + (static_cast<int>(xi) << 23));
+}
+// MUFU.EX2 alone (exp2f adds range fix-ups: 3 more instructions per element)
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -99,16 +114,19 @@ __global__ void __launch_bounds__(192, 1)
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + kOffBar);
     uint64_t* q_full = bar + 0;
-    uint64_t* kv_full = bar + 1;   // [2]
-    uint64_t* kv_empty = bar + 3;  // [2]
-    uint64_t* s_full = bar + 5;    // [2]
-    uint64_t* s_empty = bar + 7;   // [2]
-    uint64_t* p_full = bar + 9;
-    uint64_t* pv_done = bar + 10;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+    uint64_t* k_full = bar + 1;    // [2] K tile landed
+    uint64_t* k_empty = bar + 3;   // [2] S MMA that read it retired
+    uint64_t* v_full = bar + 5;    // [2]
+    uint64_t* v_empty = bar + 7;   // [2] PV MMA that read it retired
+    uint64_t* s_full = bar + 9;    // [2]
+    uint64_t* s_empty = bar + 11;  // [2]
+    uint64_t* p_full = bar + 13;   // [2]
+    uint64_t* pv_done = bar + 15;  // [2] PV of the P buffer retired
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
 
     const int warp = warp_id(), lane = lane_id();
-    const int qt = blockIdx.x, h = blockIdx.y;
+    // heaviest (latest, most keys under the causal mask) query tiles are scheduled first
+    const int qt = gridDim.x - 1 - blockIdx.x, h = blockIdx.y;
     const int kvh = h / (p.nq / p.nkv);
     const int r_begin = qt * kQ;
     const int r_end = min(p.q_len, r_begin + kQ);
@@ -123,13 +141,15 @@ __global__ void __launch_bounds__(192, 1)
         tma_prefetch_desc(&tmKV);
         mbar_init(q_full, 1);
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&kv_full[i], 1);
-            mbar_init(&kv_empty[i], 1);
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+            mbar_init(&v_full[i], 1);
+            mbar_init(&v_empty[i], 1);
             mbar_init(&s_full[i], 1);
             mbar_init(&s_empty[i], 4);
+            mbar_init(&p_full[i], 4);
+            mbar_init(&pv_done[i], 1);
         }
-        mbar_init(p_full, 4);
-        mbar_init(pv_done, 1);
         fence_mbar_init();
     }
     tc_fence_before();
@@ -149,21 +169,30 @@ __global__ void __launch_bounds__(192, 1)
             tma_load_2d(sm + kOffQ, &tmQ, q_full, qcol, qrow);
             tma_load_2d(sm + kOffQ + kHalf, &tmQ, q_full, qcol + 64, qrow);
             const int n_tab = (n_keys + 15) / 16;
+            // K and V have separate rings: K(j) is free once S(j) retired (long before
+            // PV(j)), so tile j+2's keys stream in while the softmax of j still runs
+            auto row_of = [&](int j, int b) {
+                const int tb = j * (kKT / 16) + b;
+                const int blk = p.table[tb < n_tab ? tb : 0];  // past the end: any finite block (masked)
+                return ((blk * p.n_layers + p.layer) * 2 + 0) * p.nkv * 16 + kvh * 16;
+            };
             for (int j = 0; j < n_kt; ++j) {
                 const int s = j & 1;
-                mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&kv_full[s], 2 * kTileBytes);
+                mbar_wait(&k_empty[s], ((j >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(&k_full[s], kTileBytes);
                 uint8_t* K = sm + kOffK + s * kTileBytes;
+                for (int b = 0; b < kKT / 16; ++b) {
+                    const int row_k = row_of(j, b);
+                    tma_load_2d_hint(K + b * 2048, &tmKV, &k_full[s], 0, row_k, keep);
+                    tma_load_2d_hint(K + kHalf + b * 2048, &tmKV, &k_full[s], 64, row_k, keep);
+                }
+                mbar_wait(&v_empty[s], ((j >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(&v_full[s], kTileBytes);
                 uint8_t* V = sm + kOffV + s * kTileBytes;
                 for (int b = 0; b < kKT / 16; ++b) {
-                    const int tb = j * (kKT / 16) + b;
-                    const int blk = p.table[tb < n_tab ? tb : 0];  // past the end: any finite block (masked)
-                    const int row_k = ((blk * p.n_layers + p.layer) * 2 + 0) * p.nkv * 16 + kvh * 16;
-                    const int row_v = row_k + p.nkv * 16;
-                    tma_load_2d_hint(K + b * 2048, &tmKV, &kv_full[s], 0, row_k, keep);
-                    tma_load_2d_hint(K + kHalf + b * 2048, &tmKV, &kv_full[s], 64, row_k, keep);
-                    tma_load_2d_hint(V + b * 2048, &tmKV, &kv_full[s], 0, row_v, keep);
-                    tma_load_2d_hint(V + kHalf + b * 2048, &tmKV, &kv_full[s], 64, row_v, keep);
+                    const int row_v = row_of(j, b) + p.nkv * 16;
+                    tma_load_2d_hint(V + b * 2048, &tmKV, &v_full[s], 0, row_v, keep);
+                    tma_load_2d_hint(V + kHalf + b * 2048, &tmKV, &v_full[s], 64, row_v, keep);
                 }
             }
         }
@@ -172,11 +201,10 @@ __global__ void __launch_bounds__(192, 1)
         if (lane == 0) {
             constexpr uint32_t id_s = idesc_attn(false), id_o = idesc_attn(true);
             const uint32_t q0 = smem_u32(sm + kOffQ);
-            const uint32_t pbase = smem_u32(sm + kOffP);
             mbar_wait(q_full, 0);
             auto issue_s = [&](int j) {
                 const int s = j & 1;
-                mbar_wait(&kv_full[s], (j >> 1) & 1);
+                mbar_wait(&k_full[s], (j >> 1) & 1);
                 mbar_wait(&s_empty[s], ((j >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t k0 = smem_u32(sm + kOffK + s * kTileBytes);
@@ -186,20 +214,23 @@ __global__ void __launch_bounds__(192, 1)
                     tc_mma_bf16(tmem + s * 128, sdesc_sw128(q0 + off), sdesc_sw128(k0 + off), id_s, kk > 0);
                 }
                 tc_commit(&s_full[s]);
+                tc_commit(&k_empty[s]);  // K stage reusable
             };
             auto issue_pv = [&](int j) {
                 const int s = j & 1;
-                mbar_wait(p_full, j & 1);
+                mbar_wait(&p_full[s], (j >> 1) & 1);
+                mbar_wait(&v_full[s], (j >> 1) & 1);
                 tc_fence_after();
                 const uint32_t v0 = smem_u32(sm + kOffV + s * kTileBytes);
+                const uint32_t pbase = smem_u32(sm + kOffP + s * kTileBytes);
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {  // 8 x K=16 over the 128 keys
                     const uint32_t aoff = (kk >> 2) * kHalf + (kk & 3) * 32;
                     tc_mma_bf16(tmem + 256, sdesc_sw128(pbase + aoff), sdesc_mn_sw128(v0 + kk * 2048), id_o,
                                 (j > 0 || kk > 0) ? 1u : 0u);
                 }
-                tc_commit(&kv_empty[s]);  // K/V stage reusable
-                tc_commit(pv_done);       // P buffer reusable / O stable
+                tc_commit(&v_empty[s]);   // V stage reusable
+                tc_commit(&pv_done[s]);   // P buffer s reusable / O stable
             };
             issue_s(0);
             for (int j = 0; j < n_kt; ++j) {
@@ -214,9 +245,12 @@ __global__ void __launch_bounds__(192, 1)
         const int qpos = p.pos0 + r_begin + row;
         const uint32_t lane_base = static_cast<uint32_t>(qw * 32) << 16;
         float m_ref = -INFINITY, l_sum = 0.f;
-        uint8_t* P = sm + kOffP;
+        // the first key that may lie past this warp's earliest query: tiles starting
+        // before it need no causal mask (warp-uniform test)
+        const int warp_q0 = p.pos0 + r_begin + qw * 32;
         for (int j = 0; j < n_kt; ++j) {
             const int s = j & 1;
+            uint8_t* P = sm + kOffP + s * kTileBytes;
             mbar_wait(&s_full[s], (j >> 1) & 1);
             tc_fence_after();
             uint32_t sv[4][32];
@@ -227,20 +261,27 @@ __global__ void __launch_bounds__(192, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_empty[s]);
             // scale + causal mask (keys past this row's position, or past the sequence)
+            // raw scores here; the scale (> 0) is folded into one FFMA per element below
             const int key0 = j * kKT;
             float mx = -INFINITY;
+            if (key0 + kKT - 1 <= warp_q0) {  // tile entirely at or before every row of this warp
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
+                for (int c = 0; c < 4; ++c)
 #pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    const int key = key0 + c * 32 + e;
-                    float v = __uint_as_float(sv[c][e]) * p.scale_log2;
-                    if (key > qpos) v = -INFINITY;
-                    sv[c][e] = __float_as_uint(v);
-                    mx = fmaxf(mx, v);
-                }
-            // previous PV must be done before P is overwritten (and before any O rescale)
-            if (j > 0) mbar_wait(pv_done, (j - 1) & 1);
+                    for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sv[c][e]));
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const int key = key0 + c * 32 + e;
+                        if (key > qpos) sv[c][e] = __float_as_uint(-INFINITY);
+                        mx = fmaxf(mx, __uint_as_float(sv[c][e]));
+                    }
+            }
+            mx *= p.scale_log2;
+            // P buffer s was last read by PV(j-2): it must have retired before P(j) is written
+            if (j >= 2) mbar_wait(&pv_done[s], ((j - 2) >> 1) & 1);
             // The decision is warp-uniform: tcgen05.ld/st are warp-collective. Lanes that
             // did not need it rescale exactly (possibly by 1), which is always valid.
             const bool need = __any_sync(0xffffffffu, mx > m_ref + kRescaleThreshold || m_ref == -INFINITY);
@@ -250,6 +291,7 @@ __global__ void __launch_bounds__(192, 1)
                 l_sum *= corr;
                 m_ref = m_new;
                 if (j > 0) {  // rescale this warp's rows of the O accumulator in TMEM
+                    mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);  // O stable: PV(j-1) retired
                     tc_fence_after();
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
@@ -270,9 +312,13 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {  // 8 keys = one 16-byte chunk
                     float pv[8];
+                    // a share of the exponentials runs on the FMA pipe (the MUFU pipe
+                    // alone, 16/clk/SM, would take as long as the tile's two MMAs)
+                    const bool poly = g == 3;
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
-                        pv[e] = exp2f(__uint_as_float(sv[c][g * 8 + e]) - m_ref);
+                        const float x = fmaf(__uint_as_float(sv[c][g * 8 + e]), p.scale_log2, -m_ref);
+                        pv[e] = poly ? exp2_poly(x) : ex2_approx(x);
                         rs += pv[e];
                     }
                     const int key = c * 32 + g * 8;  // within the tile
@@ -289,10 +335,10 @@ __global__ void __launch_bounds__(192, 1)
             fence_async_smem();  // generic-proxy P writes -> visible to the tensor core
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(p_full);
+            if (lane == 0) mbar_arrive(&p_full[s]);
         }
         // ---- epilogue: O / l -> bf16 rows
-        mbar_wait(pv_done, (n_kt - 1) & 1);
+        mbar_wait(&pv_done[(n_kt - 1) & 1], ((n_kt - 1) >> 1) & 1);
         tc_fence_after();
         const int grow = r_begin + row;
         const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;

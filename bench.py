@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--warmup-requests", type=int, default=24)
     ap.add_argument("--model", default="llama3-8b")
     ap.add_argument("--config", default=None)
+    ap.add_argument("--policy", default="cronus", choices=["cronus", "dp", "disagg-lh", "disagg-hl"],
+                    help="serving policy on the pair (the paper's baselines besides cronus)")
     ap.add_argument("--ppi-sms", type=int, default=40)
     ap.add_argument("--arrival", default="all-at-zero", choices=["all-at-zero", "fixed-interval"])
     ap.add_argument("--interval-ms", type=float, default=0.0)
@@ -65,9 +67,13 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
-def load_cfg(path):
+def load_cfg(path, policy="cronus"):
+    """The cluster config text, with its `policy` line set to `policy` (the paper's
+    baselines dp / disagg-lh / disagg-hl run on the same pair and profiles)."""
     path = path or (DEFAULT_CFG if os.path.exists(DEFAULT_CFG) else FALLBACK_CFG)
-    return path, open(path).read()
+    lines = open(path).read().splitlines()
+    lines = [f"policy = {policy}" if ln.split("=")[0].strip() == "policy" else ln for ln in lines]
+    return path, "\n".join(lines) + "\n"
 
 
 def make_trace(args, pairs):
@@ -197,7 +203,7 @@ def run_ours(args, rank, world):
 
     pairs = max(1, world // 2)
     colocated = world == 1
-    cfg_path, cfg = load_cfg(args.config)
+    cfg_path, cfg = load_cfg(args.config, args.policy)
     trace = make_trace(args, pairs)
     if world > 1:
         import torch.distributed as dist
@@ -310,7 +316,7 @@ def run_ours(args, rank, world):
         "ttft_mean_ms": round(rep["ttft_mean_ms"], 3), "tbt_mean_ms": round(rep["tbt_mean_ms"], 3),
         "config": {"workload": ("LLaMA3-8B shapes, 1 B200, PPI+CPI co-located (green-context SM split)"
                                 if colocated else f"LLaMA3-8B shapes, {pairs} PPI/CPI pair(s) over NVLink"),
-                   "model": args.model, "requests_per_pair": len(sub), "pairs": pairs,
+                   "model": args.model, "policy": args.policy, "requests_per_pair": len(sub), "pairs": pairs,
                    "trace": f"synth(mean_in=1014, mean_out=247, seed=1, {args.arrival})",
                    "cluster_config": os.path.relpath(cfg_path, ROOT), "clock": "wall (CUDA events)",
                    "partition": st.get("partition"), "l2": "inputs > L2 (16 GB of weights streamed per iteration)",
@@ -345,7 +351,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return None
     from oracle import cpu_baseline as CB, refsim
-    _, cfg = load_cfg(args.config)
+    _, cfg = load_cfg(args.config, args.policy)
     from paper_2509_17357_b200 import engine as E  # trace synthesis only (identical draws to the reference)
     pairs = max(1, world // 2)
     trace = make_trace(args, pairs)

@@ -27,6 +27,7 @@
 
 #include "../host/scheduler.hpp"
 #include "cronus/gpu.hpp"
+#include "cronus/policies.hpp"
 #include "cronus_ck.h"
 #include "model.hpp"
 #include "partition.hpp"
@@ -137,18 +138,20 @@ struct GpuEngine::Impl {
     std::unique_ptr<gpu::KvPool> pool_ppi, pool_cpi;
     cudaStream_t s_ppi = nullptr, s_cpi = nullptr, s_copy = nullptr;
     cudaStream_t s_cpi_full = nullptr;  // primary-context stream for lent (all-SM) CPI iterations
+    cudaStream_t s_copy_low = nullptr;  // handoffs INTO the low side (disagg-hl) on its own device
     std::unique_ptr<gpu::Worker> ppi, cpi;
     std::unique_ptr<gpu::SmPartition> part;
     std::string partition_mode = "none";
     int ppi_ctas = 0, cpi_ctas = 0;  // persistent-grid caps per worker (0 = whole device)
-    int cpi_rows = 0;
+    int cpi_rows = 0, cpi_samples = 0, ppi_rows = 0, ppi_samples = 0;
     TokenBufs tok_cpi, tok_ppi;
     // pinned staging for handoff block lists
     static constexpr int kRing = 16;
     int* xfer_host[kRing] = {};
     cudaEvent_t xfer_ev[kRing] = {};
     int xfer_slot = 0;
-    DeviceBuf xfer_dev;  // kRing slices
+    DeviceBuf xfer_dev;      // kRing slices (handoffs into the high side)
+    DeviceBuf xfer_dev_low;  // kRing slices (handoffs into the low side, separate devices)
     long long xfer_cap = 0;  // ints per slice
     int sms = 148;
     uint64_t staged_hash = 0;  // trace whose synthesized prompts are resident in tok_*.prompt
@@ -194,10 +197,14 @@ struct GpuEngine::Impl {
             int can = 0;
             check_cuda(cudaDeviceCanAccessPeer(&can, opt.cpi_device, opt.ppi_device), "peer query");
             if (!can) throw std::runtime_error("CPI device cannot access the PPI device over NVLink (no P2P)");
-            check_cuda(cudaSetDevice(opt.cpi_device), "cudaSetDevice");
-            cudaError_t e = cudaDeviceEnablePeerAccess(opt.ppi_device, 0);
-            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) check_cuda(e, "enable peer access");
-            cudaGetLastError();
+            for (auto [a, b] : {std::pair{opt.cpi_device, opt.ppi_device}, std::pair{opt.ppi_device, opt.cpi_device}}) {
+                check_cuda(cudaSetDevice(a), "cudaSetDevice");
+                cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) check_cuda(e, "enable peer access");
+                cudaGetLastError();
+            }
+            check_cuda(cudaSetDevice(opt.ppi_device), "cudaSetDevice");
+            check_cuda(cudaStreamCreateWithPriority(&s_copy_low, cudaStreamNonBlocking, hi), "stream");
         }
         for (int i = 0; i < kRing; ++i) {
             check_cuda(cudaEventCreateWithFlags(&xfer_ev[i], cudaEventDisableTiming), "event");
@@ -212,6 +219,7 @@ struct GpuEngine::Impl {
         ppi.reset();
         cpi.reset();
         if (s_cpi_full) cudaStreamDestroy(s_cpi_full);
+        if (s_copy_low) cudaStreamDestroy(s_copy_low);
         if (part) {
             part.reset();  // owns the green-context streams
         } else {
@@ -222,6 +230,14 @@ struct GpuEngine::Impl {
     }
 
     int cpi_sm_count() const { return cpi_ctas > 0 ? cpi_ctas : sms; }
+    int ppi_sm_count() const { return ppi_ctas > 0 ? ppi_ctas : sms; }
+    // the two sides of a pair: high = the CPI partition / device, low = the PPI one
+    gpu::Worker& worker(bool high) { return high ? *cpi : *ppi; }
+    gpu::KvPool& pool(bool high) { return high ? *pool_cpi : *pool_ppi; }
+    int device(bool high) const { return high ? opt.cpi_device : opt.ppi_device; }
+    TokenBufs& tok(bool high) { return high || colocated ? tok_cpi : tok_ppi; }
+    cudaStream_t copy_stream(bool into_high) { return into_high || colocated ? s_copy : s_copy_low; }
+    DeviceBuf& xfer_buf(bool into_high) { return into_high || colocated ? xfer_dev : xfer_dev_low; }
 
     std::string describe(bool probe) {
         std::ostringstream o;
@@ -266,18 +282,30 @@ struct GpuEngine::Impl {
             pool_ppi.reset();
             pool_ppi = std::make_unique<gpu::KvPool>(opt.ppi_device, ppi_blocks, bb);
         }
-        const int B = cfg.max_batched_tokens_high;
-        if (!cpi || cpi_rows < B) {
+        // Each side's worker serves the roles the policy puts there: serial prefill in
+        // ppi_chunk-row slices and/or chunked iterations of up to B rows (all sampled).
+        bool serial[2] = {false, false}, chunked[2] = {false, false};
+        for (const InstanceSpec& in : bind_policy(cfg).instances)
+            (in.role == Role::PPI || in.role == Role::PurePrefill ? serial : chunked)[in.on_high_gpu] = true;
+        const int B[2] = {cfg.max_batched_tokens_low, cfg.max_batched_tokens_high};
+        auto rows = [&](int h) { return std::max(serial[h] ? opt.ppi_chunk : 0, chunked[h] ? B[h] : 0); };
+        auto samples = [&](int h) { return std::max(1, chunked[h] ? B[h] : 0); };
+        if (!cpi || cpi_rows < rows(1) || cpi_samples < samples(1)) {
             cpi.reset();
+            cpi_rows = std::max(cpi_rows, rows(1));
+            cpi_samples = std::max(cpi_samples, samples(1));
             check_cuda(cudaSetDevice(opt.cpi_device), "cudaSetDevice");
-            cpi = std::make_unique<gpu::Worker>(*w_cpi, B, B, static_cast<int>(pool_cpi->blocks) + B, s_cpi, cpi_ctas);
+            cpi = std::make_unique<gpu::Worker>(*w_cpi, cpi_rows, cpi_samples,
+                                                static_cast<int>(pool_cpi->blocks) + cpi_rows, s_cpi, cpi_ctas);
             cpi->set_persistent_decode(opt.persistent_decode);
-            cpi_rows = B;
         }
-        if (!ppi) {
+        if (!ppi || ppi_rows < rows(0) || ppi_samples < samples(0)) {
+            ppi.reset();
+            ppi_rows = std::max(ppi_rows, rows(0));
+            ppi_samples = std::max(ppi_samples, samples(0));
             check_cuda(cudaSetDevice(opt.ppi_device), "cudaSetDevice");
-            ppi = std::make_unique<gpu::Worker>(*w_ppi, opt.ppi_chunk, 1,
-                                                static_cast<int>(pool_ppi->blocks) + opt.ppi_chunk, s_ppi, ppi_ctas);
+            ppi = std::make_unique<gpu::Worker>(*w_ppi, ppi_rows, ppi_samples,
+                                                static_cast<int>(pool_ppi->blocks) + ppi_rows, s_ppi, ppi_ctas);
         }
         const long long need = 2 * std::max(pool_ppi->blocks, pool_cpi->blocks) + 64;
         if (xfer_cap < need) {
@@ -286,6 +314,7 @@ struct GpuEngine::Impl {
                 check_cuda(cudaMallocHost(&xfer_host[i], need * 4), "pinned xfer");
             }
             xfer_dev.ensure(opt.cpi_device, static_cast<size_t>(need) * 4 * kRing);
+            if (!colocated) xfer_dev_low.ensure(opt.ppi_device, static_cast<size_t>(need) * 4 * kRing);
             xfer_cap = need;
         }
     }
@@ -296,7 +325,16 @@ namespace {
 // ---------------------------------------------------------------------------------
 class PairExecutor : public sched::Executor {
   public:
-    PairExecutor(GpuEngine::Impl& e, const Trace& t, const GpuRunOptions& o) : E(e), trace(t), opts(o) {
+    PairExecutor(GpuEngine::Impl& e, const ClusterConfig& cfg, const Trace& t, const GpuRunOptions& o)
+        : E(e), trace(t), opts(o) {
+        // scheduler instance indices (serial / chunked, in binding order) -> pair side
+        for (const InstanceSpec& in : bind_policy(cfg).instances)
+            (in.role == Role::PPI || in.role == Role::PurePrefill ? serial_high : chunked_high)
+                .push_back(in.on_high_gpu);
+        // lending the low side's SMs to high-side iterations: only where the low side
+        // runs serial prefills that the lent iteration may delay (cronus, disagg-lh)
+        lending = cfg.policy == Policy::Cronus || cfg.policy == Policy::DisaggLowHigh;
+        cpi_stream = E.s_cpi;
         const int n = static_cast<int>(t.requests.size());
         prompt_off.resize(n);
         out_off.resize(n);
@@ -321,6 +359,9 @@ class PairExecutor : public sched::Executor {
         for (auto& q : done_q)
             for (auto& t : q) cudaEventDestroy(t.ev);
         for (cudaEvent_t ev : spare) cudaEventDestroy(ev);
+        for (cudaEvent_t ev : last_iter)
+            if (ev) cudaEventDestroy(ev);
+        if (stage_fence) cudaEventDestroy(stage_fence);
         if (t0_cpi) cudaEventDestroy(t0_cpi);
         if (t0_ppi) cudaEventDestroy(t0_ppi);
         if (pinned_prompt) cudaFreeHost(pinned_prompt);
@@ -381,126 +422,211 @@ class PairExecutor : public sched::Executor {
         cudaFree(d);
     }
 
-    TokenBufs& ppi_tok() { return E.colocated ? E.tok_cpi : E.tok_ppi; }
+    // Disaggregated handoff, second half: copy a request's staged KV into the blocks
+    // its decode instance allocated at admission (stream-ordered before its first row).
+    void place_staged(int rid, const std::vector<int32_t>& blocks, bool hi, cudaStream_t st) {
+        auto it = stage_slots.find(rid);
+        if (it == stage_slots.end()) return;
+        const std::vector<int32_t>& slots = it->second;
+        const int nb = static_cast<int>(slots.size());
+        if (static_cast<int>(blocks.size()) < nb) throw std::logic_error("staged handoff: table shorter than prefix");
+        const int slot = E.xfer_slot;
+        E.xfer_slot = (E.xfer_slot + 1) % GpuEngine::Impl::kRing;
+        check_cuda(cudaEventSynchronize(E.xfer_ev[slot]), "xfer staging");
+        int* h = E.xfer_host[slot];
+        std::memcpy(h, slots.data(), nb * 4);
+        std::memcpy(h + nb, blocks.data(), nb * 4);
+        int* d = static_cast<int*>(E.xfer_buf(hi).p) + slot * E.xfer_cap;
+        check_cuda(cudaMemcpyAsync(d, h, 2 * nb * 4, cudaMemcpyHostToDevice, st), "stage ids");
+        check_cuda(cudaEventRecord(E.xfer_ev[slot], st), "event");
+        check_ck(ck_kv_copy(E.pool(stage_side).base, d, E.pool(hi).base, d + nb, nb, E.pool(hi).block_bytes, st),
+                 "kv_copy (staged)");
+        ++copy_launches;
+        if (!E.colocated && stage_tok[rid]) {  // the first token travels with the KV
+            check_ck(ck_copy_token(static_cast<int*>(E.tok(stage_side).last_tok.p), rid,
+                                   static_cast<int*>(E.tok(hi).last_tok.p), rid,
+                                   static_cast<int*>(E.tok(hi).out_tok.p), out_off[rid], st),
+                     "copy_token");
+            ++copy_launches;
+        }
+        stage_fence = record(st, stage_fence);  // slots reusable once this copy ran
+        stage_free.insert(stage_free.end(), slots.begin(), slots.end());
+        stage_slots.erase(it);
+    }
+
+    // Staging region = the upper 3/4 of the prefill side's pool (its serial instance
+    // allocates lowest ids first and holds one or two requests at a time).
+    void init_staging(bool side) {
+        if (staging_ready) {
+            if (side != stage_side) throw std::logic_error("staging: prefill side changed within a run");
+            return;
+        }
+        staging_ready = true;
+        stage_side = side;
+        const long long n = E.pool(side).blocks;
+        stage_lo = static_cast<int32_t>(n / 4);
+        for (long long b = stage_lo; b < n; ++b) stage_free.push_back(static_cast<int32_t>(b));
+    }
+
+    // Stream of a side: the low side has one; the high side's current stream may be
+    // the lent all-SM one.
+    cudaStream_t side_stream(bool high) const { return high ? cpi_stream : E.s_ppi; }
 
     // ------------------------------------------------------------- work sites
     uint64_t prefill(const sched::PrefillWork& w) override {
-        check_cuda(cudaSetDevice(E.opt.ppi_device), "cudaSetDevice");
-        if (ppi_fence) {
-            check_cuda(cudaStreamWaitEvent(E.s_ppi, ppi_fence, 0), "wait fence");
-            ppi_fence = nullptr;
+        const bool hi = serial_high.at(w.instance);
+        check_cuda(cudaSetDevice(E.device(hi)), "cudaSetDevice");
+        cudaStream_t st = side_stream(hi);
+        if (serial_fence[hi]) {
+            check_cuda(cudaStreamWaitEvent(st, serial_fence[hi], 0), "wait fence");
+            serial_fence[hi] = nullptr;
         }
-        if (last_lent && last_cpi) {  // the in-flight CPI iteration holds the PPI's SMs too
-            check_cuda(cudaStreamWaitEvent(E.s_ppi, last_cpi, 0), "wait lent iteration");
+        if (!hi && last_lent && last_iter[1]) {  // the in-flight lent iteration holds these SMs too
+            check_cuda(cudaStreamWaitEvent(st, last_iter[1], 0), "wait lent iteration");
             last_lent = false;
         }
-        TokenBufs& tb = ppi_tok();
-        const Request& r = trace.requests[w.rid];
-        for (long long start = 0; start < w.tokens; start += E.opt.ppi_chunk) {
-            const long long len = std::min<long long>(E.opt.ppi_chunk, w.tokens - start);
+        if (staging_ready && hi == stage_side)
+            for (int32_t b : *w.blocks)
+                if (b >= stage_lo) throw std::runtime_error("serial prefill reached the staging region of its pool");
+        TokenBufs& tb = E.tok(hi);
+        gpu::Worker& W = E.worker(hi);
+        const long long slice = std::min<long long>(E.opt.ppi_chunk, W.max_rows());
+        for (long long start = 0; start < w.tokens; start += slice) {
+            const long long len = std::min<long long>(slice, w.tokens - start);
             const bool last = start + len == w.tokens;
             batch.clear();
             batch.add_prefill(w.rid, start, len, *w.blocks, last && w.sample_last, out_off[w.rid]);
-            E.ppi->forward(batch, *E.pool_ppi, static_cast<int*>(tb.prompt.p),
-                           static_cast<long long*>(tb.prompt_off.p), static_cast<int*>(tb.last_tok.p),
-                           static_cast<int*>(tb.out_tok.p));
+            W.forward(batch, E.pool(hi), static_cast<int*>(tb.prompt.p), static_cast<long long*>(tb.prompt_off.p),
+                      static_cast<int*>(tb.last_tok.p), static_cast<int*>(tb.out_tok.p));
         }
-        (void)r;
-        prefill_ev[w.rid] = record(E.s_ppi, prefill_ev[w.rid]);
+        prefill_ev[w.rid] = record(st, prefill_ev[w.rid]);
+        if (hi) last_iter[1] = record(st, last_iter[1]);  // keeps the high side's stream order
         prefill_tokens += w.tokens;
-        return complete(E.s_ppi, 0);
+        return complete(st, hi ? 2 : 0);
     }
 
     uint64_t transfer(const sched::TransferWork& w) override {
-        check_cuda(cudaSetDevice(E.opt.cpi_device), "cudaSetDevice");
-        if (prefill_ev[w.rid]) check_cuda(cudaStreamWaitEvent(E.s_copy, prefill_ev[w.rid], 0), "wait prefill");
-        if (cpi_fence) check_cuda(cudaStreamWaitEvent(E.s_copy, cpi_fence, 0), "wait cpi fence");
+        const bool src_hi = serial_high.at(w.src_instance), dst_hi = chunked_high.at(w.dst_instance);
+        // the pull kernel runs on the destination device (NVLink read of the source pool)
+        check_cuda(cudaSetDevice(E.device(dst_hi)), "cudaSetDevice");
+        cudaStream_t cs = E.copy_stream(dst_hi);
+        if (prefill_ev[w.rid]) check_cuda(cudaStreamWaitEvent(cs, prefill_ev[w.rid], 0), "wait prefill");
+        if (chunked_fence[dst_hi]) check_cuda(cudaStreamWaitEvent(cs, chunked_fence[dst_hi], 0), "wait fence");
         const int nb = static_cast<int>((w.tokens + 15) / 16);
-        if (static_cast<int>(w.src_blocks->size()) < nb || static_cast<int>(w.dst_blocks->size()) < nb)
-            throw std::logic_error("handoff: block tables shorter than the prefix");
+        if (static_cast<int>(w.src_blocks->size()) < nb) throw std::logic_error("handoff: source table too short");
+        // Cronus: the CPI reserved and allocated the prefix blocks before the link started.
+        // Disaggregated: the decode instance allocates only at admission, later. The
+        // prefill side then keeps the KV (moved into its pool's staging region, whose
+        // blocks its serial instance never reaches) until the decode side pulls it into
+        // the admitted request's blocks (place_staged) — the pull model of real
+        // disaggregated deployments; the link carries the bytes at that point.
+        const bool staged = static_cast<int>(w.dst_blocks->size()) < nb;
+        const std::vector<int32_t>* dst_ids = w.dst_blocks;
+        gpu::KvPool* dst_pool = &E.pool(dst_hi);
+        if (staged) {
+            check_cuda(cudaSetDevice(E.device(src_hi)), "cudaSetDevice");
+            cs = E.copy_stream(src_hi);
+            if (prefill_ev[w.rid]) check_cuda(cudaStreamWaitEvent(cs, prefill_ev[w.rid], 0), "wait prefill");
+            init_staging(src_hi);
+            if (static_cast<int>(stage_free.size()) < nb)
+                throw std::runtime_error("handoff: staging region of the prefill pool exhausted");
+            std::vector<int32_t>& slots = stage_slots[w.rid];
+            slots.assign(stage_free.end() - nb, stage_free.end());
+            stage_free.resize(stage_free.size() - nb);
+            dst_ids = &slots;
+            dst_pool = &E.pool(src_hi);
+            if (stage_fence) check_cuda(cudaStreamWaitEvent(cs, stage_fence, 0), "wait staging reuse");
+        }
         const int slot = E.xfer_slot;
         E.xfer_slot = (E.xfer_slot + 1) % GpuEngine::Impl::kRing;
         check_cuda(cudaEventSynchronize(E.xfer_ev[slot]), "xfer staging");
         int* h = E.xfer_host[slot];
         std::memcpy(h, w.src_blocks->data(), nb * 4);
-        std::memcpy(h + nb, w.dst_blocks->data(), nb * 4);
-        int* d = static_cast<int*>(E.xfer_dev.p) + slot * E.xfer_cap;
-        check_cuda(cudaMemcpyAsync(d, h, 2 * nb * 4, cudaMemcpyHostToDevice, E.s_copy), "xfer ids");
-        check_cuda(cudaEventRecord(E.xfer_ev[slot], E.s_copy), "event");
-        check_ck(ck_kv_copy(E.pool_ppi->base, d, E.pool_cpi->base, d + nb, nb, E.pool_cpi->block_bytes, E.s_copy),
-                 "kv_copy");
+        std::memcpy(h + nb, dst_ids->data(), nb * 4);
+        int* d = static_cast<int*>(E.xfer_buf(staged ? src_hi : dst_hi).p) + slot * E.xfer_cap;
+        check_cuda(cudaMemcpyAsync(d, h, 2 * nb * 4, cudaMemcpyHostToDevice, cs), "xfer ids");
+        check_cuda(cudaEventRecord(E.xfer_ev[slot], cs), "event");
+        check_ck(ck_kv_copy(E.pool(src_hi).base, d, dst_pool->base, d + nb, nb, dst_pool->block_bytes, cs), "kv_copy");
         ++copy_launches;
         const Request& r = trace.requests[w.rid];
-        if (!E.colocated && w.tokens == r.input_len) {
-            // the PPI sampled the first token: it travels with the KV
-            check_ck(ck_copy_token(static_cast<int*>(E.tok_ppi.last_tok.p), w.rid,
-                                   static_cast<int*>(E.tok_cpi.last_tok.p), w.rid,
-                                   static_cast<int*>(E.tok_cpi.out_tok.p), out_off[w.rid], E.s_copy),
+        if (!E.colocated && w.tokens == r.input_len && !staged) {
+            // the prefill side sampled the first token: it travels with the KV
+            check_ck(ck_copy_token(static_cast<int*>(E.tok(src_hi).last_tok.p), w.rid,
+                                   static_cast<int*>(E.tok(dst_hi).last_tok.p), w.rid,
+                                   static_cast<int*>(E.tok(dst_hi).out_tok.p), out_off[w.rid], cs),
                      "copy_token");
             ++copy_launches;
         }
-        xfer_ev[w.rid] = record(E.s_copy, xfer_ev[w.rid]);
+        xfer_ev[w.rid] = record(cs, xfer_ev[w.rid]);
         xfer_pending[w.rid] = 1;
-        handoff_bytes += static_cast<double>(nb) * E.pool_cpi->block_bytes;
+        if (staged) stage_tok[w.rid] = w.tokens == r.input_len;
+        handoff_bytes += static_cast<double>(nb) * E.pool(dst_hi).block_bytes;
         handoffs++;
-        return complete(E.s_copy, 1);
+        return complete(cs, 1);
     }
 
     uint64_t iteration(const sched::IterWork& w) override {
-        check_cuda(cudaSetDevice(E.opt.cpi_device), "cudaSetDevice");
-        // SM lending: nothing in flight on the PPI -> this iteration may use every SM
-        const bool lend = E.opt.wall && E.s_cpi_full && done_q[0].empty();
-        cudaStream_t cur = lend ? E.s_cpi_full : E.s_cpi;
-        if (cur != cpi_stream) {  // keep CPI iterations in order across the two streams
-            if (last_cpi) check_cuda(cudaStreamWaitEvent(cur, last_cpi, 0), "wait previous iteration");
-            cpi_stream = cur;
-            E.cpi->set_launch(cur, lend ? 0 : E.cpi_ctas);
+        const bool hi = chunked_high.at(w.instance);
+        check_cuda(cudaSetDevice(E.device(hi)), "cudaSetDevice");
+        // SM lending: nothing in flight on the low side -> this iteration may use every SM
+        const bool lend = hi && lending && E.opt.wall && E.s_cpi_full && done_q[0].empty();
+        cudaStream_t cur = E.s_ppi;
+        if (hi) {
+            cur = lend ? E.s_cpi_full : E.s_cpi;
+            if (cur != cpi_stream) {  // keep high-side work in order across the two streams
+                if (last_iter[1]) check_cuda(cudaStreamWaitEvent(cur, last_iter[1], 0), "wait previous iteration");
+                cpi_stream = cur;
+                E.cpi->set_launch(cur, lend ? 0 : E.cpi_ctas);
+            }
         }
-        auto need = [&](int rid) {
+        auto need = [&](int rid, const std::vector<int32_t>* blocks) {
             if (xfer_pending[rid]) {
                 check_cuda(cudaStreamWaitEvent(cur, xfer_ev[rid], 0), "wait handoff");
                 xfer_pending[rid] = 0;
             }
+            if (blocks) place_staged(rid, *blocks, hi, cur);
         };
         batch.clear();
         for (const sched::DecodeRow& d : w.decoders) {
-            need(d.rid);
+            need(d.rid, d.blocks);
             const long long emitted = d.ctx - trace.requests[d.rid].input_len;
             batch.add_decode(d.rid, d.ctx, *d.blocks, out_off[d.rid] + emitted);
         }
         if (w.chunk_rid >= 0) {
-            need(w.chunk_rid);
+            need(w.chunk_rid, w.chunk_blocks);
             batch.add_prefill(w.chunk_rid, w.chunk_start, w.chunk_len, *w.chunk_blocks, w.chunk_samples,
                               out_off[w.chunk_rid]);
         }
-        for (int rid : w.finishers) need(rid);
+        for (int rid : w.finishers) need(rid, nullptr);  // zero rows: its KV is placed when it decodes
         if (!batch.d_len.empty())
-            batch.plan_decode(E.spec.n_kv_heads, 2 * (lend ? E.sms : E.cpi_sm_count()),
+            batch.plan_decode(E.spec.n_kv_heads, 2 * (lend ? E.sms : hi ? E.cpi_sm_count() : E.ppi_sm_count()),
                               !E.opt.persistent_decode && gpu::decode_cluster_kernel());
-        if (E.opt.wall) {  // device-side start of this iteration (busy time = end - start)
+        if (E.opt.wall && hi) {  // device-side start of this iteration (busy time = end - start)
             iter_start = take_event();
             check_cuda(cudaEventRecord(iter_start, cur), "event record");
         }
-        E.cpi->forward(batch, *E.pool_cpi, static_cast<int*>(E.tok_cpi.prompt.p),
-                       static_cast<long long*>(E.tok_cpi.prompt_off.p), static_cast<int*>(E.tok_cpi.last_tok.p),
-                       static_cast<int*>(E.tok_cpi.out_tok.p));
+        TokenBufs& tb = E.tok(hi);
+        E.worker(hi).forward(batch, E.pool(hi), static_cast<int*>(tb.prompt.p),
+                             static_cast<long long*>(tb.prompt_off.p), static_cast<int*>(tb.last_tok.p),
+                             static_cast<int*>(tb.out_tok.p));
         iters++;
         lent_iters += lend ? 1 : 0;
-        last_lent = lend;
+        if (hi) last_lent = lend;
         iter_rows += batch.rows();
         decode_rows += static_cast<long long>(w.decoders.size());
         for (const sched::DecodeRow& d : w.decoders) decode_keys += d.ctx;
         chunk_rows += w.chunk_len;
-        last_cpi = record(cur, last_cpi);
-        return complete(cur, 2);
+        last_iter[hi] = record(cur, last_iter[hi]);
+        return complete(cur, hi ? 2 : 0);
     }
 
     void release(int instance, int rid) override {
         if (instance >= 1000) {
-            // PPI blocks of rid were read by its handoff (none: it failed before one)
-            if (xfer_ev[rid]) ppi_fence = xfer_ev[rid];
+            // serial-instance blocks of rid were read by its handoff (none: it failed before one)
+            if (xfer_ev[rid]) serial_fence[serial_high.at(instance - 1000)] = xfer_ev[rid];
         } else {
-            cpi_fence = last_cpi;      // freed at the end of the latest launched iteration
+            const bool hi = chunked_high.at(instance);
+            chunked_fence[hi] = last_iter[hi];  // freed at the end of the latest launched work there
         }
     }
 
@@ -642,7 +768,16 @@ class PairExecutor : public sched::Executor {
     gpu::Batch batch;
     std::vector<cudaEvent_t> prefill_ev, xfer_ev;
     std::vector<char> xfer_pending;
-    cudaEvent_t ppi_fence = nullptr, cpi_fence = nullptr, last_cpi = nullptr;
+    std::vector<char> serial_high, chunked_high;  // scheduler instance index -> on the high side
+    std::map<int, std::vector<int32_t>> stage_slots;  // rid -> staging slots holding its handed-off KV
+    std::map<int, bool> stage_tok;                    // rid -> the prefill side sampled its first token
+    std::vector<int32_t> stage_free;
+    bool staging_ready = false, stage_side = false;
+    int32_t stage_lo = 0;  // lowest staging block id of the prefill-side pool
+    cudaEvent_t stage_fence = nullptr;
+    bool lending = false;
+    // per side [low, high]: block-reuse fences and the latest work launched there
+    cudaEvent_t serial_fence[2] = {}, chunked_fence[2] = {}, last_iter[2] = {};
     struct Tick {
         uint64_t ticket;
         cudaEvent_t ev;
@@ -795,14 +930,12 @@ void GpuEngine::stage(const ClusterConfig& cfg, const Trace& trace) {
     impl_->prepare(cfg);
     GpuRunOptions o;
     impl_->staged_hash = 0;
-    PairExecutor ex(*impl_, trace, o);
+    PairExecutor ex(*impl_, cfg, trace, o);
     ex.upload();  // synthesizes the prompts on the device and marks them staged
 }
 
 RunReport GpuEngine::run(const ClusterConfig& cfg, const Trace& trace, const GpuRunOptions& opts) {
-    if (cfg.policy != Policy::Cronus)
-        throw std::invalid_argument("B200 engine: only the cronus policy runs on the GPU workers (baselines: "
-                                    "use the virtual-clock cronus::run)");
+    // every policy but pp runs on the pair (the scheduler rejects pp: out of scope)
     const auto errs = validate_config(cfg);
     if (!errs.empty() || trace.requests.empty()) return cronus::run(cfg, trace, opts);  // throws the same errors
     impl_->prepare(cfg);
@@ -810,7 +943,7 @@ RunReport GpuEngine::run(const ClusterConfig& cfg, const Trace& trace, const Gpu
     impl_->ppi->set_profiling(opts.profile || impl_->opt.profile);
     impl_->cpi->reset_stats();
     impl_->ppi->reset_stats();
-    PairExecutor ex(*impl_, trace, opts);
+    PairExecutor ex(*impl_, cfg, trace, opts);
     ex.upload();
     sched::SchedulerHooks hooks;
     hooks.executor = &ex;

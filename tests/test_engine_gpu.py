@@ -172,3 +172,33 @@ def test_wall_clock_sm_lending():
     total, exact = check_tokens(t, res.extra["tokens"], [0, 7, 40, 63], splits=splits)
     assert exact >= 0.95 * total
     eng.close()
+
+
+@pytest.mark.parametrize("policy", ["dp", "disagg-lh", "disagg-hl"])
+def test_baseline_policies_on_gpu(tiny_engine, policy):
+    """the DP+chunked and disaggregated baselines run on the
+    pair's two sides (low = PPI partition/device, high = CPI). Virtual clock: the
+    schedule stays byte-identical to the host scheduler (itself pinned to the
+    reference), and every request's tokens pass the fp32 oracle check; wall clock:
+    the run completes with all invariants."""
+    cfg = load_cfg("a100_a10_llama8b").replace("policy = cronus", f"policy = {policy}")
+    t = c1_trace().subset(np.arange(24))
+    res = tiny_engine.serve(cfg, t, want_tokens=True)
+    want = E.run(cfg, t)
+    assert res.json == want.json and res.events == want.events
+    rep = json.loads(res.json)
+    assert rep["violations"] == [] and rep["completed"] == len(t)
+    toks = res.extra["tokens"]
+    assert all(len(toks[i]) == t.output_len[i] for i in range(len(t)))
+    splits = [r["partial_prefill_len"] or None for r in rep["records"]]
+    total, exact = check_tokens(t, toks, [0, 5, 11, 23], splits=splits)
+    assert exact >= 0.95 * total
+    from paper_2509_17357_b200.serving import GpuEngine
+    eng = GpuEngine(model="tiny", clock="wall")
+    w = eng.serve(cfg, t, want_tokens=True)
+    wr = json.loads(w.json)
+    assert wr["violations"] == [] and wr["completed"] == len(t)
+    total, exact = check_tokens(t, w.extra["tokens"], [0, 23], splits=[r["partial_prefill_len"] or None
+                                                                        for r in wr["records"]])
+    assert exact >= 0.95 * total
+    eng.close()

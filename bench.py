@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--ppi-sms", type=int, default=40)
     ap.add_argument("--arrival", default="all-at-zero", choices=["all-at-zero", "fixed-interval"])
     ap.add_argument("--interval-ms", type=float, default=0.0)
+    ap.add_argument("--mean-in", type=float, default=1014, help="trace mean input tokens (paper: 1014; long: 4056)")
+    ap.add_argument("--mean-out", type=float, default=247, help="trace mean output tokens (paper: 247; long: 988)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -79,7 +81,7 @@ def load_cfg(path, policy="cronus"):
 def make_trace(args, pairs):
     from paper_2509_17357_b200 import engine as E
     arrival = E.FIXED_INTERVAL if args.arrival == "fixed-interval" else E.ALL_AT_ZERO
-    return E.synth_trace(args.requests * pairs, 1014, 247, arrival, args.interval_ms, 1)
+    return E.synth_trace(args.requests * pairs, args.mean_in, args.mean_out, arrival, args.interval_ms, 1)
 
 
 def pair_trace(trace, pair, pairs):
@@ -215,9 +217,8 @@ def run_ours(args, rank, world):
     eng = None
     if driver:
         opts = dict(model=args.model, clock="wall")
-        if colocated:
-            opts["ppi_sms"] = args.ppi_sms
-        else:
+        opts["ppi_sms"] = args.ppi_sms  # the low-end worker: an SM partition (its own GPU when N > 1)
+        if not colocated:
             opts.update(ppi_device=rank, cpi_device=rank + 1)
         eng = GpuEngine(**opts)
         sub = pair_trace(trace, pair, pairs)
@@ -317,7 +318,8 @@ def run_ours(args, rank, world):
         "config": {"workload": ("LLaMA3-8B shapes, 1 B200, PPI+CPI co-located (green-context SM split)"
                                 if colocated else f"LLaMA3-8B shapes, {pairs} PPI/CPI pair(s) over NVLink"),
                    "model": args.model, "policy": args.policy, "requests_per_pair": len(sub), "pairs": pairs,
-                   "trace": f"synth(mean_in=1014, mean_out=247, seed=1, {args.arrival})",
+                   "trace": (f"synth(mean_in={args.mean_in:g}, mean_out={args.mean_out:g}, seed=1, {args.arrival}"
+                             + (f" {args.interval_ms:g} ms)" if args.arrival == "fixed-interval" else ")")),
                    "cluster_config": os.path.relpath(cfg_path, ROOT), "clock": "wall (CUDA events)",
                    "partition": st.get("partition"), "l2": "inputs > L2 (16 GB of weights streamed per iteration)",
                    "parallelism": "replicas of worker pairs" if pairs > 1 else "co-located pair"},

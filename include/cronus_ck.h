@@ -141,9 +141,11 @@ int ck_silu_mul(float* gu, void* act_bf16, int M, int F, int zero_after, void* s
 
 /* Greedy sampling: token = argmax_v logits[r, v] (lowest index on ties), then
  * last_tok[rid[r]] = token, out_tok[out_idx[r]] = token. ws: 64 * R floats of
- * scratch; tickets: R ints, zero before the first call (left zero). One launch. */
-int ck_argmax_emit(const float* logits, int R, int V, const int* rid, const long long* out_idx, int* last_tok,
-                   int* out_tok, float* ws, int* tickets, void* stream);
+ * scratch; tickets: R ints, zero before the first call (left zero). zero_after:
+ * clear the R logits rows after reading them (a red.add LM head accumulates into
+ * them next). One launch. */
+int ck_argmax_emit(float* logits, int R, int V, const int* rid, const long long* out_idx, int* last_tok,
+                   int* out_tok, float* ws, int* tickets, int zero_after, void* stream);
 
 /* KV handoff: copy n_blocks blocks src_pool[src_ids[i]] -> dst_pool[dst_ids[i]]
  * (block_bytes each; src may be a peer-mapped pointer — pull over NVLink). */

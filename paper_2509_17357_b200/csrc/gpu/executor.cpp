@@ -142,6 +142,7 @@ struct GpuEngine::Impl {
     std::unique_ptr<gpu::Worker> ppi, cpi;
     std::unique_ptr<gpu::SmPartition> part;
     std::string partition_mode = "none";
+    bool own_cpi_streams = false, own_ppi_stream = false;  // streams created outside a partition
     int ppi_ctas = 0, cpi_ctas = 0;  // persistent-grid caps per worker (0 = whole device)
     int cpi_rows = 0, cpi_samples = 0, ppi_rows = 0, ppi_samples = 0;
     TokenBufs tok_cpi, tok_ppi;
@@ -186,12 +187,29 @@ struct GpuEngine::Impl {
                 partition_mode = "grid-cap";
             }
         }
-        if (!part) {
+        if (!colocated && opt.ppi_sms > 0) {
+            // separate devices: the low-end worker is emulated by SM-partitioning its own
+            // device (north star); only the partition's PPI stream is used
+            part = gpu::make_sm_partition(opt.ppi_device, opt.ppi_sms, lo, hi);
+            if (part) {
+                s_ppi = part->ppi_stream;
+                ppi_ctas = part->ppi_sms;
+                partition_mode = "green-context (ppi device)";
+            } else {
+                ppi_ctas = opt.ppi_sms;
+                partition_mode = "grid-cap (ppi device)";
+            }
+        }
+        if (!s_cpi) {
             check_cuda(cudaSetDevice(opt.cpi_device), "cudaSetDevice");
             check_cuda(cudaStreamCreateWithPriority(&s_cpi, cudaStreamNonBlocking, hi), "stream");
             check_cuda(cudaStreamCreateWithPriority(&s_copy, cudaStreamNonBlocking, hi), "stream");
+            own_cpi_streams = true;
+        }
+        if (!s_ppi) {
             check_cuda(cudaSetDevice(opt.ppi_device), "cudaSetDevice");
             check_cuda(cudaStreamCreateWithPriority(&s_ppi, cudaStreamNonBlocking, lo), "stream");
+            own_ppi_stream = true;
         }
         if (!colocated) {
             int can = 0;
@@ -220,13 +238,12 @@ struct GpuEngine::Impl {
         cpi.reset();
         if (s_cpi_full) cudaStreamDestroy(s_cpi_full);
         if (s_copy_low) cudaStreamDestroy(s_copy_low);
-        if (part) {
-            part.reset();  // owns the green-context streams
-        } else {
-            if (s_ppi) cudaStreamDestroy(s_ppi);
+        if (own_ppi_stream && s_ppi) cudaStreamDestroy(s_ppi);
+        if (own_cpi_streams) {
             if (s_cpi) cudaStreamDestroy(s_cpi);
             if (s_copy) cudaStreamDestroy(s_copy);
         }
+        part.reset();  // owns the green-context streams
     }
 
     int cpi_sm_count() const { return cpi_ctas > 0 ? cpi_ctas : sms; }

@@ -273,6 +273,7 @@ Worker::Worker(const Weights& w, int max_rows, int max_sample, int max_blocks_pe
     check_cuda(cudaMalloc(&act_, R * m_.ffn * 2), "alloc act");
     check_cuda(cudaMalloc(&hs_, static_cast<size_t>(max_sample) * H * 2), "alloc hs");
     check_cuda(cudaMalloc(&logits_, static_cast<size_t>(max_sample) * m_.vocab * 4), "alloc logits");
+    check_cuda(cudaMemset(logits_, 0, static_cast<size_t>(max_sample) * m_.vocab * 4), "zero logits");
     attn_ws_floats_ = 4096LL * m_.n_heads * (m_.head_dim + 2);
     check_cuda(cudaMalloc(&attn_ws_, attn_ws_floats_ * 4), "alloc attn ws");
     check_cuda(cudaMalloc(&attn_tickets_, R * m_.n_kv_heads * 4), "alloc attn tickets");
@@ -539,11 +540,17 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         check_ck(ck_rmsnorm(x_, w_.final_norm, hs_, D(o_s_row), R, H, m.rms_eps, nullptr, 0, stream_), "final norm");
         ++launches;
         done(a, &stat_other, 0, 0);
-        gemm(w_.lm_head, hs_, logits_, nullptr, R, m.vocab, H, CK_EPI_F32, 1);
+        // LM head: a 1 GB weight stream for a handful of rows -> stream-K red.add into the
+        // logits the previous argmax cleared (balanced over the grid); larger R: tile stores
+        if (R <= 128 && !logits_dirty_)
+            gemm(w_.lm_head, hs_, logits_, nullptr, R, m.vocab, H, CK_EPI_RED_F32, 0);
+        else
+            gemm(w_.lm_head, hs_, logits_, nullptr, R, m.vocab, H, CK_EPI_F32, 1);
         mark(a);
         check_ck(ck_argmax_emit(logits_, R, m.vocab, D(o_s_rid), reinterpret_cast<const long long*>(D(o_s_out)),
-                                last_tok, out_tok, arg_ws_, arg_tickets_, stream_),
+                                last_tok, out_tok, arg_ws_, arg_tickets_, 1, stream_),
                  "argmax");
+        logits_dirty_ = false;
         ++launches;
         done(a, &stat_other, 0, 0);
     }
@@ -578,6 +585,7 @@ bool Worker::forward_mega(const Batch& b, const KvPool& pool, const PassMeta& pm
     a.nq = m.n_heads, a.nkv = m.n_kv_heads, a.grid = max_ctas_ > 0 ? max_ctas_ : ck_device_sms();
     a.eps = m.rms_eps, a.scale = 1.0f / std::sqrt(static_cast<float>(m.head_dim));
     a.x = x_, a.h = h_, a.qkv = qkv_, a.q = q_, a.attn = attn_, a.gu = gu_, a.act = act_, a.hs = hs_, a.logits = logits_;
+    logits_dirty_ = true;  // its LM head stores, its argmax does not clear
     a.embed = w_.embed, a.final_norm = w_.final_norm, a.cos_tab = w_.cos_tab, a.sin_tab = w_.sin_tab;
     a.row_rid = pm.row_rid, a.row_pos = pm.row_pos, a.bt = pm.bt, a.d_row = pm.d_row, a.d_len = pm.d_len;
     a.d_bt = pm.d_bt, a.d_item0 = pm.d_item0, a.d_work = pm.d_work;

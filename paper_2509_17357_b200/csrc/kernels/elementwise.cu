@@ -219,9 +219,9 @@ __device__ __forceinline__ void arg_better(float& bv, int& bi, float v, int i) {
     }
 }
 
-__global__ void argmax_emit_kernel(const float* __restrict__ logits, int V, const int* rid, const long long* out_idx,
+__global__ void argmax_emit_kernel(float* __restrict__ logits, int V, const int* rid, const long long* out_idx,
                                    int* last_tok, int* out_tok, float* __restrict__ pv, int* __restrict__ pi,
-                                   int* __restrict__ tickets) {
+                                   int* __restrict__ tickets, int zero_after) {
     pdl_launch();
     pdl_wait();
     __shared__ float sb[32];
@@ -231,11 +231,12 @@ __global__ void argmax_emit_kernel(const float* __restrict__ logits, int V, cons
     const int n4 = V / 4;
     const int lo = static_cast<int>(static_cast<long long>(c) * n4 / kArgChunks);
     const int hi = static_cast<int>(static_cast<long long>(c + 1) * n4 / kArgChunks);
-    const float4* row = reinterpret_cast<const float4*>(logits + static_cast<size_t>(r) * V);
+    float4* row = reinterpret_cast<float4*>(logits + static_cast<size_t>(r) * V);
     float best = -INFINITY;
     int bi = 0x7fffffff;
     for (int v = lo + threadIdx.x; v < hi; v += blockDim.x) {
         const float4 x = row[v];
+        if (zero_after) row[v] = make_float4(0.f, 0.f, 0.f, 0.f);  // next red.add LM head starts from zero
         arg_better(best, bi, x.x, 4 * v);
         arg_better(best, bi, x.y, 4 * v + 1);
         arg_better(best, bi, x.z, 4 * v + 2);
@@ -390,14 +391,14 @@ int ck_silu_mul(float* gu, void* act, int M, int F, int zero_after, void* stream
     return launch_pdl(silu_mul_kernel, dim3(grid), dim3(256), 0, S(stream), gu, static_cast<__nv_bfloat16*>(act), n4, zero_after);
 }
 
-int ck_argmax_emit(const float* logits, int R, int V, const int* rid, const long long* out_idx, int* last_tok,
-                   int* out_tok, float* ws, int* tickets, void* stream) {
+int ck_argmax_emit(float* logits, int R, int V, const int* rid, const long long* out_idx, int* last_tok,
+                   int* out_tok, float* ws, int* tickets, int zero_after, void* stream) {
     if (R <= 0) return 0;
     if (V % 4) return static_cast<int>(cudaErrorInvalidValue);
     float* pv = ws;
     int* pi = reinterpret_cast<int*>(ws + static_cast<size_t>(R) * kArgChunks);
     return launch_pdl(argmax_emit_kernel, dim3(R, kArgChunks), dim3(256), 0, S(stream), logits, V, rid, out_idx,
-                      last_tok, out_tok, pv, pi, tickets);
+                      last_tok, out_tok, pv, pi, tickets, zero_after);
 }
 
 int ck_kv_copy(const void* src_pool, const int* src_ids, void* dst_pool, const int* dst_ids, int n_blocks,

@@ -260,7 +260,10 @@ def test_silu_mul_and_argmax(L):
     out_tok = torch.full((20,), -1, dtype=torch.int32, device="cuda")
     ws = torch.empty(64 * R, device="cuda")
     tickets = torch.zeros(R, dtype=torch.int32, device="cuda")
-    ok(L.ck_argmax_emit(p(logits), R, V, p(rid), p(out_idx), p(last), p(out_tok), p(ws), p(tickets), stream()))
+    keep = logits.clone()
+    ok(L.ck_argmax_emit(p(logits), R, V, p(rid), p(out_idx), p(last), p(out_tok), p(ws), p(tickets), 1, stream()))
+    assert logits.abs().sum() == 0  # zero_after: cleared for the next red.add LM head
+    logits = keep
     assert tickets.abs().sum() == 0
     want = logits.argmax(-1).int()
     assert int(want[1]) == 77

@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--mean-out", type=float, default=247, help="trace mean output tokens (paper: 247; long: 988)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--profile-requests", type=int, default=48, help="trace prefix profiled with CUPTI")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     return ap.parse_args()
@@ -156,6 +157,67 @@ def traffic_ratios():
     return out
 
 
+def kernel_class(name):
+    """Kernel name (CUPTI, demangled) -> the engine's kernel-time class."""
+    if "gemm_tc_kernel" in name:
+        return "gemm_tc" if "<256>" in name else "gemm_stream"  # BN <= 128 <=> M <= 128 rows
+    if "attn_decode" in name:
+        return "decode_attn"
+    if "attn_prefill" in name:
+        return "prefill_attn"
+    if "mega_decode" in name:
+        return "mega_decode"
+    return "other"
+
+
+def cupti_profile(eng, cfg, sample):
+    """Critical-path time per kernel class from CUPTI kernel records (torch.profiler) over a
+    bounded sample of the trace, with the PDL launch chains intact (no per-launch events).
+
+    Per worker (its streams: stream ids from the engine), kernels are ordered by end time and
+    each is charged end_i - max(end_{i-1}, start_i): the time it adds to the worker's chain,
+    so a kernel resident early at griddepcontrol.wait is not charged for waiting. Returns
+    the stats shape of GpuEngine (per worker/class: launches, ms, bytes, flops)."""
+    import tempfile
+    from collections import defaultdict
+
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        res = eng.serve(cfg, sample, events=False)
+        torch.cuda.synchronize()
+    fd, path = tempfile.mkstemp(suffix=".json")
+    os.close(fd)
+    try:
+        prof.export_chrome_trace(path)
+        tr = json.load(open(path))
+    finally:
+        os.remove(path)
+    st = res.extra["stats"]
+    sids = st["partition"].get("stream_ids", {})
+    worker_of = {sids.get("ppi"): "ppi", sids.get("cpi"): "cpi", sids.get("cpi_full"): "cpi"}
+    per_worker = defaultdict(list)
+    for e in tr.get("traceEvents", []):
+        if e.get("cat") == "kernel" and "args" in e:
+            w = worker_of.get(e["args"].get("stream"))
+            if w:
+                per_worker[w].append((e["ts"] + e["dur"], e["ts"], kernel_class(e["name"])))
+    out = {"cpi": {}, "ppi": {}, "partition": st["partition"], "sample_requests": len(sample)}
+    for w, ks in per_worker.items():
+        ks.sort()
+        prev = -1e30
+        ms = defaultdict(float)
+        for end, start, cls in ks:
+            ms[cls] += (end - max(prev, start)) / 1e3
+            prev = end
+        for cls, tally in st[w].items():
+            if cls in ms and tally.get("launches"):
+                out[w][cls] = dict(tally, ms=ms[cls])
+    return out
+
+
 def roofline(stats, partition=None):
     """Dominant kernel class of the profiled step -> roofline object (+ all classes).
 
@@ -169,7 +231,7 @@ def roofline(stats, partition=None):
     classes = []
     for worker in ("cpi", "ppi"):
         for name, k in stats[worker].items():
-            if name == "forward" or not k["launches"] or name == "other":
+            if name in ("forward", "other", "mega_decode") or not k["launches"] or k["ms"] <= 0:
                 continue
             bound = "hbm" if name in ("gemm_stream", "decode_attn") else "tensor"
             ms_avg = k["ms"] / k["launches"]
@@ -298,11 +360,27 @@ def run_ours(args, rank, world):
                "d2h_bytes_per_step": int(d2h)}
 
     # ---- profiled step (kernel classes timed with CUDA events on their streams)
-    roof, classes, prof_stats = {}, [], None
+    # Kernel rooflines. (1) CUPTI critical-path times on a bounded sample (the first
+    # --profile-requests requests; chains intact) -> `roofline` / `kernels`. (2) CUDA events
+    # around every launch over the whole trace -> `kernels_events`: events between kernels
+    # break the PDL overlap, so these per-kernel figures are conservative.
+    roof, classes, classes_ev, prof_stats = {}, [], [], None
     if not args.no_profile and driver:
+        sample = sub.subset(np.arange(min(args.profile_requests, len(sub))), name="profile-sample")
+        try:
+            cp = cupti_profile(eng, cfg, sample)
+            roof, classes = roofline(cp, cp["partition"])
+            if roof:
+                roof["timing"] = (f"CUPTI kernel records, critical-path time per launch, first {len(sample)} "
+                                  "requests of the trace")
+        except Exception as ex:  # profiler unavailable: fall back to the event-timed step
+            print(f"[bench] CUPTI profile failed ({ex}); using event timing", file=sys.stderr)
         pr = eng.serve(cfg, sub, events=False, profile=True)
         prof_stats = pr.extra["stats"]
-        roof, classes = roofline(prof_stats, prof_stats.get("partition"))
+        roof_ev, classes_ev = roofline(prof_stats, prof_stats.get("partition"))
+        if not roof:
+            roof, classes = roof_ev, classes_ev
+            roof["timing"] = "CUDA events around each launch (serialises PDL chains: conservative)"
 
     if rank != 0:
         return None
@@ -328,7 +406,7 @@ def run_ours(args, rank, world):
         "cpi_busy_ms": round(st.get("cpi_busy_ms", 0.0), 2),
         "cpi_lent_iterations": st.get("cpi_lent_iterations"),
         "iteration_shapes_count_ms_rows_ctx": st.get("iteration_shapes"),
-        "clocks": clocks, "e2e": e2e, "roofline": roof, "kernels": classes[:8],
+        "clocks": clocks, "e2e": e2e, "roofline": roof, "kernels": classes[:8], "kernels_events": classes_ev[:8],
     }
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(args, cfg, sub)

@@ -135,6 +135,13 @@ int ck_attn_prefill_tc(const void* q, int q_rows_total, const void* kv_pool, lon
                        int q_row0, int q_len, int pos0, void* out, int nq, int nkv, int layer, int n_layers,
                        float scale, void* stream);
 
+/* Same op, production path: two 128-row query tiles per CTA with one softmax warpgroup
+ * each (ping-pong on the tensor pipe) and P kept in TMEM as the A operand of the PV
+ * MMA. Same arguments and stale-slot requirement as ck_attn_prefill_tc. */
+int ck_attn_prefill_pp(const void* q, int q_rows_total, const void* kv_pool, long long pool_blocks, const int* bt,
+                       int q_row0, int q_len, int pos0, void* out, int nq, int nkv, int layer, int n_layers,
+                       float scale, void* stream);
+
 /* act[m, i] = silu(gu[m, 2i]) * gu[m, 2i+1]  (gate/up rows interleaved), fp32 in;
  * zero_after: clear gu after reading it. */
 int ck_silu_mul(float* gu, void* act_bf16, int M, int F, int zero_after, void* stream);

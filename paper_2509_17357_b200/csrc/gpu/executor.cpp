@@ -261,6 +261,14 @@ struct GpuEngine::Impl {
         o << "{\"mode\": \"" << partition_mode << "\", \"device_sms\": " << sms << ", \"ppi_sms\": "
           << (ppi_ctas ? ppi_ctas : sms) << ", \"cpi_sms\": " << cpi_sm_count()
           << ", \"sm_lending\": " << (s_cpi_full ? "true" : "false");
+        // CUDA stream ids (as CUPTI / profilers report them) of each worker's streams
+        auto sid = [](cudaStream_t st) {
+            unsigned long long id = 0;
+            if (st) cudaStreamGetId(st, &id);
+            return id;
+        };
+        o << ", \"stream_ids\": {\"ppi\": " << sid(s_ppi) << ", \"cpi\": " << sid(s_cpi)
+          << ", \"cpi_full\": " << sid(s_cpi_full) << ", \"copy\": " << sid(s_copy) << "}";
         if (probe) {
             auto seen = [&](int dev, cudaStream_t st) {
                 check_cuda(cudaSetDevice(dev), "cudaSetDevice");

@@ -247,6 +247,16 @@ void Batch::plan_decode_clusters(int n_kv_heads, int slots) {
     blocks_per_split = static_cast<int>(cap);
 }
 
+// Prefill / chunk attention: ping-pong kernel (default) or one query tile per CTA
+// (CRONUS_PREFILL_V1=1).
+bool prefill_attn_v1() {
+    static const bool on = [] {
+        const char* e = std::getenv("CRONUS_PREFILL_V1");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 bool decode_cluster_kernel() {
     static const bool on = [] {
         const char* e = std::getenv("CRONUS_DECODE_CPASYNC");
@@ -327,7 +337,12 @@ void Worker::mark(cudaEvent_t& a) {
     cudaEventRecord(a, stream_);
 }
 void Worker::done(cudaEvent_t a, KernelStat* into, double bytes, double flops) {
-    if (!profile_) return;
+    if (!profile_) {  // launches and algorithmic work are always tallied (no events, no timing)
+        into->launches++;
+        into->bytes += bytes;
+        into->flops += flops;
+        return;
+    }
     cudaEvent_t b = ev();
     cudaEventRecord(b, stream_);
     pending_.push_back({a, b, into, bytes, flops});
@@ -506,9 +521,10 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         }
         if (b.p_len > 0) {
             mark(a);
-            check_ck(ck_attn_prefill_tc(q_, max_rows_, pool.base, pool.blocks, bt + b.p_bt, b.p_row0, b.p_len,
-                                        b.p_pos0, attn_, m.n_heads, m.n_kv_heads, l, m.layers, scale, stream_),
-                     "attn_prefill_tc");
+            check_ck((prefill_attn_v1() ? ck_attn_prefill_tc : ck_attn_prefill_pp)(
+                         q_, max_rows_, pool.base, pool.blocks, bt + b.p_bt, b.p_row0, b.p_len, b.p_pos0, attn_,
+                         m.n_heads, m.n_kv_heads, l, m.layers, scale, stream_),
+                     "attn_prefill");
             ++launches;
             const double keys = static_cast<double>(b.p_len) * b.p_pos0 + 0.5 * b.p_len * (b.p_len + 1.0);
             done(a, &stat_prefill_attn, (b.p_pos0 + b.p_len) * kv_tok_layer, 4.0 * m.n_heads * m.head_dim * keys);

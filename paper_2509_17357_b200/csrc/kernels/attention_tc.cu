@@ -371,6 +371,291 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 
+
+// ============================================================ ping-pong variant (default)
+// Two 128-row query tiles of one head per CTA (rows [r0, r0+128) and [r0+128, r0+256)),
+// one softmax warpgroup each, sharing the K/V rings. P never leaves the tensor memory:
+// each softmax warpgroup writes its bf16 P over the first 64 columns of its own S tile
+// (tcgen05.st) and the PV MMA takes A straight from TMEM. The MMA warp interleaves
+//   PV_0(j), S_0(j+1), PV_1(j), S_1(j+1)
+// so while one warpgroup exponentiates, the tensor pipe works for the other. tcgen05
+// MMAs execute in issue order, so S_i(j+1) (same TMEM as P_i(j)) follows PV_i(j), and
+// "S_i(j) done" implies "PV_i(j-1) done": the O rescale needs no extra barrier.
+// TMEM: S_0 | S_1 | O_0 | O_1 (128 columns each). smem: Q_0, Q_1, K[2], V[2] = 192 KB.
+constexpr int kPPOffQ = 0;
+constexpr int kPPOffK = kPPOffQ + 2 * kTileBytes;
+constexpr int kPPOffV = kPPOffK + 2 * kTileBytes;
+constexpr int kPPOffBar = kPPOffV + 2 * kTileBytes;
+constexpr int kPPSmemBytes = kPPOffBar + 256 + 1024;
+constexpr int kPPThreads = 320;  // producer, MMA, 2 x 4 softmax warps
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+// D[tmem] (+)= A[tmem] * B[smem desc]: A (M=128 rows in lanes, K packed 2 x bf16 per column).
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(kPPThreads, 1)
+    attn_prefill_pp_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
+                           AttnParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + kPPOffBar);
+    uint64_t* q_full = bar + 0;    // [2] per query tile
+    uint64_t* k_full = bar + 2;    // [2] per stage
+    uint64_t* k_empty = bar + 4;   // [2]
+    uint64_t* v_full = bar + 6;    // [2]
+    uint64_t* v_empty = bar + 8;   // [2]
+    uint64_t* s_full = bar + 10;   // [2] per query tile
+    uint64_t* p_full = bar + 12;   // [2] per query tile (4 warp arrivals)
+    uint64_t* o_done = bar + 14;   // [2] per query tile
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+
+    const int warp = warp_id(), lane = lane_id();
+    const int ct = gridDim.x - 1 - blockIdx.x, h = blockIdx.y;  // heaviest tiles first
+    const int kvh = h / (p.nq / p.nkv);
+    const int r0 = ct * 2 * kQ;
+    const int n_qt = r0 + kQ < p.q_len ? 2 : 1;
+    int n_kt[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) n_kt[i] = (p.pos0 + min(p.q_len, r0 + (i + 1) * kQ) + kKT - 1) / kKT;
+    const int n_kt_max = n_kt[n_qt - 1];
+
+    if (warp == 1) {
+        tmem_alloc(tmem_slot, 512);
+        tmem_relinquish();
+    } else if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmQ);
+        tma_prefetch_desc(&tmKV);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&q_full[i], 1);
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+            mbar_init(&v_full[i], 1);
+            mbar_init(&v_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], 4);
+            mbar_init(&o_done[i], 1);
+        }
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_launch();
+    pdl_wait();
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            const uint64_t keep = policy_evict_last();
+            for (int i = 0; i < n_qt; ++i) {
+                mbar_arrive_expect_tx(&q_full[i], kTileBytes);
+                const int qrow = p.q_row0 + r0 + i * kQ;
+                tma_load_2d(sm + kPPOffQ + i * kTileBytes, &tmQ, &q_full[i], h * 128, qrow);
+                tma_load_2d(sm + kPPOffQ + i * kTileBytes + kHalf, &tmQ, &q_full[i], h * 128 + 64, qrow);
+            }
+            const int n_tab = (p.pos0 + min(p.q_len, r0 + n_qt * kQ) + 15) / 16;
+            auto row_of = [&](int j, int b) {
+                const int tb = j * (kKT / 16) + b;
+                const int blk = p.table[tb < n_tab ? tb : 0];  // past the end: any finite block (masked)
+                return ((blk * p.n_layers + p.layer) * 2 + 0) * p.nkv * 16 + kvh * 16;
+            };
+            for (int j = 0; j < n_kt_max; ++j) {
+                const int s = j & 1;
+                mbar_wait(&k_empty[s], ((j >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(&k_full[s], kTileBytes);
+                uint8_t* K = sm + kPPOffK + s * kTileBytes;
+                for (int b = 0; b < kKT / 16; ++b) {
+                    const int rk = row_of(j, b);
+                    tma_load_2d_hint(K + b * 2048, &tmKV, &k_full[s], 0, rk, keep);
+                    tma_load_2d_hint(K + kHalf + b * 2048, &tmKV, &k_full[s], 64, rk, keep);
+                }
+                mbar_wait(&v_empty[s], ((j >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(&v_full[s], kTileBytes);
+                uint8_t* V = sm + kPPOffV + s * kTileBytes;
+                for (int b = 0; b < kKT / 16; ++b) {
+                    const int rv = row_of(j, b) + p.nkv * 16;
+                    tma_load_2d_hint(V + b * 2048, &tmKV, &v_full[s], 0, rv, keep);
+                    tma_load_2d_hint(V + kHalf + b * 2048, &tmKV, &v_full[s], 64, rv, keep);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t id_s = idesc_attn(false), id_o = idesc_attn(true);
+            for (int i = 0; i < n_qt; ++i) mbar_wait(&q_full[i], 0);
+            auto issue_s = [&](int i, int j) {  // S_i(j) = Q_i K(j)^T -> TMEM cols [128 i, +128)
+                const uint32_t q0 = smem_u32(sm + kPPOffQ + i * kTileBytes);
+                const uint32_t k0 = smem_u32(sm + kPPOffK + (j & 1) * kTileBytes);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
+                    tc_mma_bf16(tmem + i * 128, sdesc_sw128(q0 + off), sdesc_sw128(k0 + off), id_s, kk > 0);
+                }
+                tc_commit(&s_full[i]);
+            };
+            auto issue_pv = [&](int i, int j) {  // O_i += P_i(j) V(j), P from TMEM (packed bf16 pairs)
+                mbar_wait(&p_full[i], j & 1);
+                tc_fence_after();
+                const uint32_t v0 = smem_u32(sm + kPPOffV + (j & 1) * kTileBytes);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    tc_mma_ts(tmem + 256 + i * 128, tmem + i * 128 + kk * 8, sdesc_mn_sw128(v0 + kk * 2048), id_o,
+                              (j > 0 || kk > 0) ? 1u : 0u);
+                if (j == n_kt[i] - 1) tc_commit(&o_done[i]);
+            };
+            auto k_ready = [&](int j) {
+                mbar_wait(&k_full[j & 1], (j >> 1) & 1);
+                tc_fence_after();
+            };
+            k_ready(0);
+            for (int i = 0; i < n_qt; ++i)
+                if (n_kt[i] > 0) issue_s(i, 0);
+            tc_commit(&k_empty[0]);
+            for (int j = 0; j < n_kt_max; ++j) {
+                const bool next = j + 1 < n_kt_max;
+                mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+                tc_fence_after();
+                if (next) k_ready(j + 1);
+                for (int i = 0; i < n_qt; ++i) {
+                    if (j < n_kt[i]) issue_pv(i, j);
+                    if (j + 1 < n_kt[i]) issue_s(i, j + 1);
+                }
+                tc_commit(&v_empty[j & 1]);
+                if (next) tc_commit(&k_empty[(j + 1) & 1]);
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ softmax warpgroups
+        const int i = (warp - 2) >> 2;  // query tile of this warpgroup
+        if (i < n_qt) {
+            const int qw = warp & 3;
+            const int row = qw * 32 + lane;
+            const int qbase = r0 + i * kQ;
+            const int qpos = p.pos0 + qbase + row;
+            const int warp_q0 = p.pos0 + qbase + qw * 32;
+            const uint32_t lane_base = static_cast<uint32_t>(qw * 32) << 16;
+            const uint32_t s_col = tmem + lane_base + i * 128, o_col = tmem + lane_base + 256 + i * 128;
+            float m_ref = -INFINITY, l_sum = 0.f;
+            for (int j = 0; j < n_kt[i]; ++j) {
+                mbar_wait(&s_full[i], j & 1);
+                tc_fence_after();
+                uint32_t sv[4][32];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tmem_ld32(s_col + c * 32, sv[c]);
+                tmem_ld_wait();
+                const int key0 = j * kKT;
+                float mx = -INFINITY;
+                if (key0 + kKT - 1 <= warp_q0) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sv[c][e]));
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) {
+                            if (key0 + c * 32 + e > qpos) sv[c][e] = __float_as_uint(-INFINITY);
+                            mx = fmaxf(mx, __uint_as_float(sv[c][e]));
+                        }
+                }
+                mx *= p.scale_log2;
+                const bool need = __any_sync(0xffffffffu, mx > m_ref + kRescaleThreshold || m_ref == -INFINITY);
+                if (need) {
+                    const float m_new = fmaxf(m_ref, mx);
+                    const float corr = m_ref == -INFINITY ? 0.f : exp2f(m_ref - m_new);
+                    l_sum *= corr;
+                    m_ref = m_new;
+                    if (j > 0) {  // PV_i(j-1) retired before S_i(j) (in-order tensor pipe)
+#pragma unroll 1
+                        for (int c = 0; c < 8; ++c) {  // 16 columns at a time: S stays in registers
+                            uint32_t o[16];
+                            tmem_ld16(o_col + c * 16, o);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+                            tmem_st16(o_col + c * 16, o);
+                        }
+                    }
+                }
+                // P = exp2(S * scale - m) -> bf16 pairs over S's first 64 columns
+                float rs = 0.f;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        const bool poly = g == 3;
+                        float pv[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const float x = fmaf(__uint_as_float(sv[c][g * 8 + e]), p.scale_log2, -m_ref);
+                            pv[e] = poly ? exp2_poly(x) : ex2_approx(x);
+                            rs += pv[e];
+                        }
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) pk[g * 4 + e] = pack_bf16x2(pv[2 * e], pv[2 * e + 1]);
+                    }
+                    tmem_st16(s_col + c * 16, pk);
+                }
+                tmem_st_wait();
+                l_sum += rs;
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&p_full[i]);
+            }
+            // ---- epilogue: O / l -> bf16 rows
+            mbar_wait(&o_done[i], 0);
+            tc_fence_after();
+            const int grow = qbase + row;
+            const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t o[32];
+                tmem_ld32(o_col + c * 32, o);
+                tmem_ld_wait();
+                if (grow < p.q_len) {
+                    __nv_bfloat16* dst = p.out + static_cast<size_t>(p.q_row0 + grow) * p.nq * 128 + h * 128 + c * 32;
+#pragma unroll
+                    for (int e = 0; e < 32; e += 8) {
+                        uint4 w;
+                        w.x = pack_bf16x2(__uint_as_float(o[e]) * inv, __uint_as_float(o[e + 1]) * inv);
+                        w.y = pack_bf16x2(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
+                        w.z = pack_bf16x2(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
+                        w.w = pack_bf16x2(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
+                        *reinterpret_cast<uint4*>(dst + e) = w;
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 }  // namespace
 
 namespace ck {
@@ -450,4 +735,41 @@ extern "C" int ck_attn_prefill_tc(const void* q, int q_rows_total, const void* k
     const dim3 grid((q_len + kQ - 1) / kQ, nq);
     return launch_pdl(attn_prefill_tc_kernel, grid, dim3(192), kSmemBytes, static_cast<cudaStream_t>(stream), mq, mkv,
                       prm);
+}
+
+extern "C" int ck_attn_prefill_pp(const void* q, int q_rows_total, const void* kv_pool, long long pool_blocks,
+                                  const int* bt, int q_row0, int q_len, int pos0, void* out, int nq, int nkv, int layer,
+                                  int n_layers, float scale, void* stream) {
+    if (q_len <= 0) return 0;
+    CUtensorMap mq, mkv;
+    int rc = make_map_2d(q, static_cast<unsigned long long>(q_rows_total), static_cast<unsigned long long>(nq) * 128,
+                         kQ, &mq);
+    if (rc) return rc;
+    const unsigned long long pool_rows = static_cast<unsigned long long>(pool_blocks) * n_layers * 2 * nkv * 16;
+    rc = make_map_2d(kv_pool, pool_rows, 128, 16, &mkv);
+    if (rc) return rc;
+    static unsigned mask = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(mask & (1u << dev))) {
+        cudaError_t e =
+            cudaFuncSetAttribute(attn_prefill_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPPSmemBytes);
+        if (e != cudaSuccess) return static_cast<int>(e);
+        mask |= 1u << dev;
+    }
+    AttnParams prm;
+    prm.q_row0 = q_row0;
+    prm.q_len = q_len;
+    prm.pos0 = pos0;
+    prm.nq = nq;
+    prm.nkv = nkv;
+    prm.layer = layer;
+    prm.n_layers = n_layers;
+    prm.row_stride_blk = n_layers * 2 * nkv * 16;
+    prm.scale_log2 = scale * kLog2e;
+    prm.out = static_cast<__nv_bfloat16*>(out);
+    prm.table = bt;
+    const dim3 grid((q_len + 2 * kQ - 1) / (2 * kQ), nq);
+    return launch_pdl(attn_prefill_pp_kernel, grid, dim3(kPPThreads), kPPSmemBytes, static_cast<cudaStream_t>(stream),
+                      mq, mkv, prm);
 }

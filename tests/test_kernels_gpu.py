@@ -213,7 +213,7 @@ def test_attn_decode(L, nq, nkv, impl):
             assert torch.allclose(got, ref, rtol=2e-2, atol=2e-2), (bps, cluster, ln, (got - ref).abs().max().item())
 
 
-@pytest.mark.parametrize("impl", ["mma", "tc"])
+@pytest.mark.parametrize("impl", ["mma", "tc", "pp"])
 @pytest.mark.parametrize("nq,nkv", [(2, 1), (32, 8), (28, 4)])
 @pytest.mark.parametrize("pos0,qlen", [(0, 1), (0, 77), (0, 256), (300, 64), (1000, 212), (48, 512), (2000, 700)])
 def test_attn_prefill(L, nq, nkv, pos0, qlen, impl):
@@ -231,8 +231,9 @@ def test_attn_prefill(L, nq, nkv, pos0, qlen, impl):
         ok(L.ck_attn_prefill(p(q), p(pool), p(tables[0]), row0, qlen, pos0, p(out), nq, nkv, layer, layers, scale,
                              stream()))
     else:
-        ok(L.ck_attn_prefill_tc(p(q), q.shape[0], p(pool), pool.shape[0], p(tables[0]), row0, qlen, pos0, p(out), nq,
-                                nkv, layer, layers, scale, stream()))
+        fn = L.ck_attn_prefill_tc if impl == "tc" else L.ck_attn_prefill_pp
+        ok(fn(p(q), q.shape[0], p(pool), pool.shape[0], p(tables[0]), row0, qlen, pos0, p(out), nq, nkv, layer,
+              layers, scale, stream()))
     qpos = torch.arange(pos0, T, device="cuda")
     ref = attn_ref(q[row0:row0 + qlen].view(qlen, nq, 128), ks[0], vs[0], qpos, scale)
     got = out[row0:row0 + qlen].float().view(qlen, nq, 128)

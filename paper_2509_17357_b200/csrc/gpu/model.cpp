@@ -371,7 +371,8 @@ void Worker::gemm(const void* W, const void* X, void* out, const void* bias, int
     ++launches;
     // algorithmic bytes: weights + activations in + output (red.add counted once)
     done(a, M <= 128 ? &stat_gemm_stream : &stat_gemm_tc,
-         2.0 * (static_cast<double>(N) * K + static_cast<double>(M) * K) + (epi == CK_EPI_BF16 ? 2.0 : 4.0) * M * N,
+         2.0 * (static_cast<double>(N) * K + static_cast<double>(M) * K) +
+             (epi == CK_EPI_BF16 ? 2.0 : epi == CK_EPI_SILU_BF16 ? 1.0 : 4.0) * M * N,
          2.0 * M * N * K);
 }
 
@@ -464,7 +465,7 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         qkv_dirty_rows_ = gu_dirty_rows_ = 0;
     } else {
         qkv_dirty_rows_ = std::max(qkv_dirty_rows_, M);
-        gu_dirty_rows_ = std::max(gu_dirty_rows_, M);
+        if (fuse_epilogue()) gu_dirty_rows_ = std::max(gu_dirty_rows_, M);  // else gate/up go straight to act
     }
     cudaEvent_t a = nullptr;
     mark(a);
@@ -542,6 +543,10 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         fs.act = act_;
         if (fuse_epilogue()) {
             gemm(L.wgu, h_, gu_, nullptr, M, 2 * F, H, small ? CK_EPI_RED_F32 : CK_EPI_F32, small ? 0 : 1, &fs);
+        } else if (!small) {
+            // tensor regime: whole tiles per CTA -> SiLU(gate) * up straight from TMEM (the
+            // fp32 gate/up tensor never reaches HBM)
+            gemm(L.wgu, h_, act_, nullptr, M, 2 * F, H, CK_EPI_SILU_BF16, 1);
         } else {
             gemm(L.wgu, h_, gu_, nullptr, M, 2 * F, H, small ? CK_EPI_RED_F32 : CK_EPI_F32, small ? 0 : 1);
             mark(a);

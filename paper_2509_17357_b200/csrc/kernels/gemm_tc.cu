@@ -328,6 +328,17 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
                         if (j < mlim) o[static_cast<size_t>(j) * p.ldo] = f2bf(__uint_as_float(v[j]) + bias);
+                } else if (p.epi == CK_EPI_SILU_BF16) {
+                    // adjacent lanes hold the (gate, up) rows of one activation column
+                    __nv_bfloat16* o =
+                        static_cast<__nv_bfloat16*>(p.out) + static_cast<size_t>(m_base + c) * p.ldo + (n >> 1);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const float g = __uint_as_float(v[j]);
+                        const float u = __shfl_xor_sync(0xffffffffu, g, 1);
+                        if (!(lane & 1) && j < mlim)
+                            o[static_cast<size_t>(j) * p.ldo] = f2bf(__fdividef(g, 1.f + __expf(-g)) * u);
+                    }
                 } else if (p.epi == CK_EPI_F32) {
                     float* o = static_cast<float*>(p.out) + static_cast<size_t>(m_base + c) * p.ldo + n;
 #pragma unroll
@@ -555,7 +566,7 @@ extern "C" int ck_gemm_fused(const void* W, const void* X, void* out, const void
                              int splits, int max_ctas, const ck_gemm_fuse* fuse, void* stream) {
     if (fuse && fuse->kind != CK_FUSE_NONE && (epi == CK_EPI_BF16 || !fuse->tickets))
         return static_cast<int>(cudaErrorInvalidValue);  // finalize reads the fp32 tile back
-    return gemm_impl(W, X, out, bias, M, N, K, N, epi, splits, max_ctas, fuse, stream);
+    return gemm_impl(W, X, out, bias, M, N, K, 0, epi, splits, max_ctas, fuse, stream);
 }
 
 namespace {
@@ -564,7 +575,8 @@ int gemm_impl(const void* W, const void* X, void* out, const void* bias, int M, 
     if (M <= 0) return 0;
     if (N % kTileN != 0 || K % kTileK != 0 || N <= 0 || K <= 0) return static_cast<int>(cudaErrorInvalidValue);
     if ((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(X)) & 15) return static_cast<int>(cudaErrorMisalignedAddress);
-    if (epi < CK_EPI_BF16 || epi > CK_EPI_RED_F32) return static_cast<int>(cudaErrorInvalidValue);
+    if (epi < CK_EPI_BF16 || epi > CK_EPI_SILU_BF16) return static_cast<int>(cudaErrorInvalidValue);
+    if (epi == CK_EPI_SILU_BF16 && (splits != 1 || bias != nullptr)) return static_cast<int>(cudaErrorInvalidValue);
     const int BN = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
     GemmParams p{};
     p.out = out;
@@ -572,7 +584,7 @@ int gemm_impl(const void* W, const void* X, void* out, const void* bias, int M, 
     p.M = M;
     p.N = N;
     p.K = K;
-    p.ldo = ldo > 0 ? ldo : N;
+    p.ldo = ldo > 0 ? ldo : (epi == CK_EPI_SILU_BF16 ? N / 2 : N);
     p.epi = epi;
     p.fuse = fuse ? *fuse : ck_gemm_fuse{};
     p.m_tiles = (M + BN - 1) / BN;

@@ -167,3 +167,22 @@ def test_gemm_fused_qkv_rope_matches_unfused(L, M):
         outs.append((q_out.float(), pool.float()))
     assert torch.allclose(outs[0][0], outs[1][0], rtol=1e-2, atol=1e-2)
     assert torch.allclose(outs[0][1], outs[1][1], rtol=1e-2, atol=1e-2)
+
+
+@pytest.mark.parametrize("M", [129, 300, 512, 1000])
+def test_gemm_silu_epilogue(L, M):
+    """CK_EPI_SILU_BF16: interleaved gate/up weight rows -> bf16 silu(gate) * up, written
+    straight from the accumulator (tensor regime, whole tiles per CTA)."""
+    g = torch.Generator(device="cuda").manual_seed(M)
+    F, K = 640, 512
+    W = (torch.randn(2 * F, K, device="cuda", generator=g) * 0.05).bfloat16()
+    X = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    act = torch.full((M, F), float("nan"), device="cuda", dtype=torch.bfloat16)
+    s = torch.cuda.current_stream().cuda_stream
+    assert L.ck_gemm_fused(p(W), p(X), p(act), None, M, 2 * F, K, 3, 1, 0, None, ctypes.c_void_p(s)) == 0
+    torch.cuda.synchronize()
+    ref = X.float() @ W.float().t()
+    want = torch.nn.functional.silu(ref[:, 0::2]) * ref[:, 1::2]
+    assert torch.allclose(act.float(), want, rtol=2e-2, atol=2e-2), (act.float() - want).abs().max().item()
+    bad = L.ck_gemm_fused(p(W), p(X), p(act), None, M, 2 * F, K, 3, 0, 0, None, ctypes.c_void_p(s))
+    assert bad != 0  # split-K / stream-K cannot fuse the gate-up pairing

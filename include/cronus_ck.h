@@ -119,10 +119,18 @@ int ck_attn_decode(const void* q, const void* kv_pool, const int* bt, const int*
  * merge through ws / tickets as in ck_attn_decode. Partially filled last blocks are
  * read whole and masked, so never-written slots must hold finite values (the engine
  * zero-fills its pools). pool rows must be < 2^31. */
+typedef struct {
+    const float* qkv;     /* fp32 QKV rows [*, (nq + 2 nkv) * 128] (bias included), row = seq_row */
+    const float* cos_tab; /* RoPE tables [max_pos][64] (ck_rope_table) */
+    const float* sin_tab;
+} ck_decode_rope;
+/* rope != NULL: fused RoPE + KV append of the decode token (position seq_len - 1): q, k,
+ * v come from rope->qkv (q is unused) and the token's K/V is written to its pool slot
+ * (replaces ck_qkv_rope_append for decode-only passes; qkv is left for the caller to clear). */
 int ck_attn_decode_tma(const void* q, const void* kv_pool, long long pool_blocks, const int* bt, const int* seq_row,
                        const int* seq_len, const int* seq_bt, const int* seq_item0, const int* work, int n_work,
                        int n_seq, int cluster, float* ws, int* tickets, void* out, int nq, int nkv, int layer,
-                       int n_layers, float scale, void* stream);
+                       int n_layers, float scale, const ck_decode_rope* rope, void* stream);
 
 /* Prefill/chunk attention, causal: query rows [q_row0, q_row0+q_len) sit at
  * positions [pos0, pos0+q_len); keys [0, pos0+q_len) from the paged pool via bt. */

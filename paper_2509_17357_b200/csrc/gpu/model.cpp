@@ -257,6 +257,16 @@ bool prefill_attn_v1() {
     return on;
 }
 
+// Decode-only passes fuse RoPE + KV append into the decode attention unless
+// CRONUS_DECODE_ROPE_KERNEL=1 (separate qkv_rope_append kernel, for comparison).
+bool decode_rope_kernel() {
+    static const bool on = [] {
+        const char* e = std::getenv("CRONUS_DECODE_ROPE_KERNEL");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 bool decode_cluster_kernel() {
     static const bool on = [] {
         const char* e = std::getenv("CRONUS_DECODE_CPASYNC");
@@ -467,6 +477,12 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         qkv_dirty_rows_ = std::max(qkv_dirty_rows_, M);
         if (fuse_epilogue()) gu_dirty_rows_ = std::max(gu_dirty_rows_, M);  // else gate/up go straight to act
     }
+    // decode-only weight-streaming pass: RoPE + KV append of the decode tokens run inside
+    // the decode attention (reads the fp32 qkv accumulator), one kernel fewer per layer
+    const bool fused_rope = small && b.p_len == 0 && n_dec == M && b.decode_cluster > 0 && !fuse_epilogue() &&
+                            !decode_rope_kernel();
+    const ck_decode_rope rope{qkv_, w_.cos_tab, w_.sin_tab};
+    if (fused_rope) qkv_dirty_rows_ = std::max(qkv_dirty_rows_, M);  // the last layer's rows: next pass clears
     cudaEvent_t a = nullptr;
     mark(a);
     check_ck(ck_embed(x_, w_.embed, row_rid, row_pos, row_dec, prompt, prompt_off, last_tok, M, H, stream_), "embed");
@@ -477,7 +493,10 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         mark(a);
         // weight-streaming regime (M <= 128): qkv accumulates with red.add (stream-K GEMM),
         // so the norm kernel clears it; tensor regime: plain fp32 tile stores
-        check_ck(ck_rmsnorm(x_, L.attn_norm, h_, nullptr, M, H, m.rms_eps, nullptr, 0, stream_), "rmsnorm");
+        // fused decode RoPE: the attention left the previous layer's qkv rows for this norm to clear
+        check_ck(ck_rmsnorm(x_, L.attn_norm, h_, nullptr, M, H, m.rms_eps, fused_rope && l > 0 ? qkv_ : nullptr,
+                            Q, stream_),
+                 "rmsnorm");
         ++launches;
         done(a, &stat_other, 0, 0);
         // QKV projection with RoPE + KV append fused into its tile finalize
@@ -497,6 +516,8 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
             gemm(L.wqkv, h_, qkv_, L.bqkv, M, Q, H, small ? CK_EPI_RED_F32 : CK_EPI_F32, small ? 0 : 1, &fq);
         } else {
             gemm(L.wqkv, h_, qkv_, L.bqkv, M, Q, H, small ? CK_EPI_RED_F32 : CK_EPI_F32, small ? 0 : 1);
+        }
+        if (!fuse_epilogue() && !fused_rope) {
             mark(a);
             check_ck(ck_qkv_rope_append(qkv_, nullptr, q_, pool.base, bt, row_bt, row_pos, w_.cos_tab, w_.sin_tab, M,
                                         m.n_heads, m.n_kv_heads, l, m.layers, small ? 1 : 0, stream_),
@@ -515,7 +536,7 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
                 check_ck(ck_attn_decode_tma(q_, pool.base, pool.blocks, bt, D(o_d_row), D(o_d_len), D(o_d_bt),
                                             D(o_d_item0), D(o_d_work), n_work, n_dec, b.decode_cluster, attn_ws_,
                                             attn_tickets_, attn_, m.n_heads, m.n_kv_heads, l, m.layers, scale,
-                                            stream_),
+                                            fused_rope ? &rope : nullptr, stream_),
                          "attn_decode_tma");
             ++launches;
             done(a, &stat_decode_attn, dec_keys * kv_tok_layer, 4.0 * m.n_heads * m.head_dim * dec_keys);

@@ -337,12 +337,30 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
         for (int i = 0; i < STAGES; ++i) mbar_init(&bar[i], 1);
         fence_mbar_init();
-        while (issued < pre && first + 4 * issued != nblk - 1) load(issued++);
+        // fused RoPE: no kernel writes the pool before us -> the last block may go early too
+        while (issued < pre && (a.qkv || first + 4 * issued != nblk - 1)) load(issued++);
     }
     pdl_wait();
     if (lane == 0)
         while (issued < pre) load(issued++);
-    {  // Q (G rows, zero padded to 16) — written by the previous kernel
+    const int pos = len - 1;  // the decode token
+    const int qkv_w = (a.nq + 2 * a.nkv) * kDHD;
+    if (a.qkv) {  // Q = RoPE(q) from the fp32 accumulator (G heads x 64 rotate-half pairs)
+        const float* qrow = a.qkv + static_cast<size_t>(a.seq_row[s]) * qkv_w + static_cast<size_t>(kvh) * G * kDHD;
+        const float* cs = a.cos_tab + static_cast<size_t>(pos) * 64;
+        const float* sn = a.sin_tab + static_cast<size_t>(pos) * 64;
+        for (int c = t; c < 16 * 64; c += 128) {
+            const int r = c >> 6, i = c & 63;
+            float lo = 0.f, hi = 0.f;
+            if (r < G) {
+                const float x = qrow[r * kDHD + i], y = qrow[r * kDHD + i + 64];
+                lo = x * cs[i] - y * sn[i];
+                hi = y * cs[i] + x * sn[i];
+            }
+            reinterpret_cast<__nv_bfloat16*>(sQ + swz(r, i >> 3))[i & 7] = f2bf(lo);
+            reinterpret_cast<__nv_bfloat16*>(sQ + swz(r, 8 + (i >> 3)))[i & 7] = f2bf(hi);
+        }
+    } else {  // Q (G rows, zero padded to 16) — written by the previous kernel
         const __nv_bfloat16* qrow =
             a.q + static_cast<size_t>(a.seq_row[s]) * a.nq * kDHD + static_cast<size_t>(kvh) * G * kDHD;
         for (int c = t; c < 16 * 16; c += 128) {
@@ -362,7 +380,36 @@ __global__ void __launch_bounds__(128)
     float m_run = -INFINITY, l_run = 0.f;
     for (int i = 0; i < mine; ++i) {
         mbar_wait(&bar[i % STAGES], (i / STAGES) & 1);
-        const uint8_t* K = ring + (i % STAGES) * 2 * kDTileBytes;
+        uint8_t* K = ring + (i % STAGES) * 2 * kDTileBytes;
+        if (a.qkv && first + 4 * i == nblk - 1) {
+            // the decode token's K (RoPE) / V: computed from the accumulator, written to
+            // its pool slot and patched into the staged block (4 dims per lane)
+            const float* krow = a.qkv + static_cast<size_t>(a.seq_row[s]) * qkv_w + (a.nq + kvh) * kDHD;
+            const float* vrow = krow + a.nkv * kDHD;
+            const int d0 = lane * 4, r = pos & 15;
+            float kr[4], vr[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int d = d0 + e, ii = d & 63;
+                const float x = krow[d], y = krow[d ^ 64];
+                const float c = a.cos_tab[static_cast<size_t>(pos) * 64 + ii];
+                const float sn = a.sin_tab[static_cast<size_t>(pos) * 64 + ii];
+                kr[e] = d < 64 ? x * c - y * sn : x * c + y * sn;
+                vr[e] = vrow[d];
+            }
+            uint2 kp, vp;
+            kp.x = pack_bf16x2(kr[0], kr[1]), kp.y = pack_bf16x2(kr[2], kr[3]);
+            vp.x = pack_bf16x2(vr[0], vr[1]), vp.y = pack_bf16x2(vr[2], vr[3]);
+            const uint32_t off = (d0 >> 6) * 2048 + r * 128 + ((((d0 & 63) >> 3) ^ (r & 7)) << 4) + (d0 & 7) * 2;
+            *reinterpret_cast<uint2*>(K + off) = kp;
+            *reinterpret_cast<uint2*>(K + kDTileBytes + off) = vp;
+            __nv_bfloat16* slot = const_cast<__nv_bfloat16*>(a.pool) +
+                                  kv_tile_off(table[nblk - 1], a.layer, 0, kvh, a.n_layers, a.nkv) + r * kDHD + d0;
+            *reinterpret_cast<uint2*>(slot) = kp;
+            *reinterpret_cast<uint2*>(slot + static_cast<size_t>(a.nkv) * kDTile) = vp;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before TMA refills the slot
+            __syncwarp();
+        }
         dec_block<SwzTma128>(K, K + kDTileBytes, qf, o, m_run, l_run, (first + 4 * i) * kDBlk, len,
                              a.qk_scale_log2, lane);
         __syncwarp();
@@ -526,7 +573,8 @@ extern "C" int ck_attn_decode(const void* q, const void* kv_pool, const int* bt,
 extern "C" int ck_attn_decode_tma(const void* q, const void* kv_pool, long long pool_blocks, const int* bt,
                                   const int* seq_row, const int* seq_len, const int* seq_bt, const int* seq_item0,
                                   const int* work, int n_work, int n_seq, int cluster, float* ws, int* tickets,
-                                  void* out, int nq, int nkv, int layer, int n_layers, float scale, void* stream) {
+                                  void* out, int nq, int nkv, int layer, int n_layers, float scale,
+                                  const ck_decode_rope* rope, void* stream) {
     if (n_seq <= 0 || n_work <= 0) return 0;
     if (cluster < 1 || cluster > 16) return static_cast<int>(cudaErrorInvalidValue);
     CUtensorMap tm;
@@ -536,7 +584,8 @@ extern "C" int ck_attn_decode_tma(const void* q, const void* kv_pool, long long 
     if (rc) return rc;
     const DecodeAttnArgs a{static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(kv_pool), bt,
                            seq_row, seq_len, seq_bt, seq_item0, work, 0, ws, tickets,
-                           static_cast<__nv_bfloat16*>(out), nq, nkv, layer, n_layers, scale * kLog2e};
+                           static_cast<__nv_bfloat16*>(out), nq, nkv, layer, n_layers, scale * kLog2e,
+                           rope ? rope->qkv : nullptr, rope ? rope->cos_tab : nullptr, rope ? rope->sin_tab : nullptr};
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (nq / nkv) {
         case 1: return launch_decode_tma_g<1>(tm, a, n_work, cluster, st);

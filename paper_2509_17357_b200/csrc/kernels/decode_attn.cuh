@@ -71,6 +71,12 @@ struct DecodeAttnArgs {
     __nv_bfloat16* out;
     int nq, nkv, layer, n_layers;
     float qk_scale_log2;
+    // Fused RoPE + KV append of the decode token (TMA kernel only; null = off): q, k, v
+    // are read from the fp32 QKV accumulator [rows][(nq + 2 nkv) * 128] instead of `q`,
+    // the token's K/V is written to its pool slot and patched into the staged block.
+    const float* qkv;
+    const float* cos_tab;
+    const float* sin_tab;
 };
 
 // [16 tok][256 B] rows (cp.async ring): 16-B chunk c of row r at c ^ (r & 7).

@@ -200,7 +200,7 @@ def test_attn_decode(L, nq, nkv, impl):
         if impl == "tma":
             ok(L.ck_attn_decode_tma(p(q), p(pool), pool.shape[0], p(bt), p(rows), p(t_len), p(t_off), p(t_item0),
                                     p(t_work), len(work), S, cluster, p(ws), p(tickets), p(out), nq, nkv, layer,
-                                    layers, scale, stream()))
+                                    layers, scale, None, stream()))
         else:
             ok(L.ck_attn_decode(p(q), p(pool), p(bt), p(rows), p(t_len), p(t_off), p(t_item0), p(t_work),
                                 len(work), S, bps, p(ws), p(tickets), p(out), nq, nkv, layer, layers, scale,
@@ -282,3 +282,71 @@ def test_kv_copy(L):
     for s, d in zip(sid.tolist(), did.tolist()):
         assert torch.equal(dst[d * bb:(d + 1) * bb], src[s * bb:(s + 1) * bb])
     assert dst[bb:2 * bb].sum() == 0
+
+
+class DecodeRope(ctypes.Structure):
+    _fields_ = [("qkv", ctypes.c_void_p), ("cos_tab", ctypes.c_void_p), ("sin_tab", ctypes.c_void_p)]
+
+
+@pytest.mark.parametrize("nq,nkv", [(32, 8), (28, 4)])
+def test_attn_decode_fused_rope(L, nq, nkv):
+    """ck_attn_decode_tma with a ck_decode_rope: RoPE(q), RoPE(k) / v of the decode token
+    from the fp32 qkv rows, the token's K/V written to its pool slot, attention over the
+    whole context == ck_qkv_rope_append followed by the unfused kernel."""
+    gen = torch.Generator(device="cuda").manual_seed(nq + 1)
+    layers, layer, theta = 2, 1, 500000.0
+    lens = [1, 16, 17, 300, 1025, 2048]
+    S = len(lens)
+    pool = make_pool(sum((n + 15) // 16 for n in lens) + 2, layers, nkv, fill=0.0)
+    tables, ks, vs = fill_sequences(pool, layer, [n - 1 for n in lens], nkv, gen) if False else (None, None, None)
+    # context of len-1 tokens per sequence, the last slot left for the decode token
+    perm = torch.randperm(pool.shape[0], device="cuda", generator=gen).int()
+    tables, used = [], 0
+    for n in lens:
+        nb = (n + 15) // 16
+        tables.append(perm[used:used + nb])
+        used += nb
+        for j in range(n - 1):
+            pool[int(tables[-1][j // 16]), layer, :, :, j % 16] = torch.randn(2, nkv, 128, device="cuda",
+                                                                             generator=gen).bfloat16()
+    width = (nq + 2 * nkv) * 128
+    rows = torch.arange(S, dtype=torch.int32, device="cuda")
+    qkv = torch.randn(S, width, device="cuda", generator=gen)
+    c = torch.empty(4096 * 64, device="cuda"); s_ = torch.empty(4096 * 64, device="cuda")
+    ok(L.ck_rope_table(p(c), p(s_), 4096, theta, stream()))
+    bt = torch.cat(tables)
+    offs = torch.tensor(np.concatenate([[0], np.cumsum([len(t) for t in tables])[:-1]]), dtype=torch.int32,
+                        device="cuda")
+    t_len = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    pos = t_len - 1
+    scale = 1 / math.sqrt(128)
+    for cluster in (1, 4):
+        work, item0 = [], []
+        for s_i in range(S):
+            item0.append(len(work))
+            work.append(s_i << 16)
+        item0.append(len(work))
+        t_item0 = torch.tensor(item0, dtype=torch.int32, device="cuda")
+        t_work = torch.tensor(work, dtype=torch.int32, device="cuda")
+        ws = torch.empty(len(work) * nq * 130, device="cuda")
+        tickets = torch.zeros(S * nkv, dtype=torch.int32, device="cuda")
+        # reference: rope kernel (writes q and the token's K/V) + unfused attention
+        pool_ref = pool.clone()
+        q = torch.empty(S, nq * 128, dtype=torch.bfloat16, device="cuda")
+        row_bt = offs.clone()
+        ok(L.ck_qkv_rope_append(p(qkv.clone()), None, p(q), p(pool_ref), p(bt), p(row_bt), p(pos), p(c), p(s_), S,
+                                nq, nkv, layer, layers, 0, stream()))
+        out_ref = torch.zeros(S, nq * 128, dtype=torch.bfloat16, device="cuda")
+        ok(L.ck_attn_decode_tma(p(q), p(pool_ref), pool.shape[0], p(bt), p(rows), p(t_len), p(offs), p(t_item0),
+                                p(t_work), len(work), S, cluster, p(ws), p(tickets), p(out_ref), nq, nkv, layer,
+                                layers, scale, None, stream()))
+        # fused
+        pool_f = pool.clone()
+        out = torch.zeros_like(out_ref)
+        rope = DecodeRope(qkv.data_ptr(), c.data_ptr(), s_.data_ptr())
+        ok(L.ck_attn_decode_tma(None, p(pool_f), pool.shape[0], p(bt), p(rows), p(t_len), p(offs), p(t_item0),
+                                p(t_work), len(work), S, cluster, p(ws), p(tickets), p(out), nq, nkv, layer,
+                                layers, scale, ctypes.byref(rope), stream()))
+        assert torch.allclose(out.float(), out_ref.float(), rtol=2e-2, atol=2e-2), \
+            (cluster, (out.float() - out_ref.float()).abs().max().item())
+        assert torch.equal(pool_f, pool_ref)  # the token's K/V slot written identically

@@ -149,7 +149,7 @@ struct GpuEngine::Impl {
     // pinned staging for handoff block lists
     static constexpr int kRing = 16;
     int* xfer_host[kRing] = {};
-    cudaEvent_t xfer_ev[kRing] = {};
+    cudaEvent_t xfer_ev[2][kRing] = {};  // per side's device: [low, high]
     int xfer_slot = 0;
     DeviceBuf xfer_dev;      // kRing slices (handoffs into the high side)
     DeviceBuf xfer_dev_low;  // kRing slices (handoffs into the low side, separate devices)
@@ -224,15 +224,19 @@ struct GpuEngine::Impl {
             check_cuda(cudaSetDevice(opt.ppi_device), "cudaSetDevice");
             check_cuda(cudaStreamCreateWithPriority(&s_copy_low, cudaStreamNonBlocking, hi), "stream");
         }
-        for (int i = 0; i < kRing; ++i) {
-            check_cuda(cudaEventCreateWithFlags(&xfer_ev[i], cudaEventDisableTiming), "event");
+        for (int side = 0; side < 2; ++side) {  // events must live on the device whose streams record them
+            check_cuda(cudaSetDevice(side ? opt.cpi_device : opt.ppi_device), "cudaSetDevice");
+            for (int i = 0; i < kRing; ++i)
+                check_cuda(cudaEventCreateWithFlags(&xfer_ev[side][i], cudaEventDisableTiming), "event");
         }
+        check_cuda(cudaSetDevice(opt.cpi_device), "cudaSetDevice");
     }
 
     ~Impl() {
         for (int i = 0; i < kRing; ++i) {
             if (xfer_host[i]) cudaFreeHost(xfer_host[i]);
-            if (xfer_ev[i]) cudaEventDestroy(xfer_ev[i]);
+            for (int side = 0; side < 2; ++side)
+                if (xfer_ev[side][i]) cudaEventDestroy(xfer_ev[side][i]);
         }
         ppi.reset();
         cpi.reset();
@@ -383,7 +387,8 @@ class PairExecutor : public sched::Executor {
                 if (ev) cudaEventDestroy(ev);
         for (auto& q : done_q)
             for (auto& t : q) cudaEventDestroy(t.ev);
-        for (cudaEvent_t ev : spare) cudaEventDestroy(ev);
+        for (auto& pool : spare)
+            for (cudaEvent_t ev : pool) cudaEventDestroy(ev);
         for (cudaEvent_t ev : last_iter)
             if (ev) cudaEventDestroy(ev);
         if (stage_fence) cudaEventDestroy(stage_fence);
@@ -457,13 +462,13 @@ class PairExecutor : public sched::Executor {
         if (static_cast<int>(blocks.size()) < nb) throw std::logic_error("staged handoff: table shorter than prefix");
         const int slot = E.xfer_slot;
         E.xfer_slot = (E.xfer_slot + 1) % GpuEngine::Impl::kRing;
-        check_cuda(cudaEventSynchronize(E.xfer_ev[slot]), "xfer staging");
+        for (auto& ring : E.xfer_ev) check_cuda(cudaEventSynchronize(ring[slot]), "xfer staging");
         int* h = E.xfer_host[slot];
         std::memcpy(h, slots.data(), nb * 4);
         std::memcpy(h + nb, blocks.data(), nb * 4);
         int* d = static_cast<int*>(E.xfer_buf(hi).p) + slot * E.xfer_cap;
         check_cuda(cudaMemcpyAsync(d, h, 2 * nb * 4, cudaMemcpyHostToDevice, st), "stage ids");
-        check_cuda(cudaEventRecord(E.xfer_ev[slot], st), "event");
+        check_cuda(cudaEventRecord(E.xfer_ev[hi][slot], st), "event");
         check_ck(ck_kv_copy(E.pool(stage_side).base, d, E.pool(hi).base, d + nb, nb, E.pool(hi).block_bytes, st),
                  "kv_copy (staged)");
         ++copy_launches;
@@ -527,7 +532,7 @@ class PairExecutor : public sched::Executor {
         prefill_ev[w.rid] = record(st, prefill_ev[w.rid]);
         if (hi) last_iter[1] = record(st, last_iter[1]);  // keeps the high side's stream order
         prefill_tokens += w.tokens;
-        return complete(st, hi ? 2 : 0);
+        return complete(st, hi ? 2 : 0, hi);
     }
 
     uint64_t transfer(const sched::TransferWork& w) override {
@@ -564,13 +569,13 @@ class PairExecutor : public sched::Executor {
         }
         const int slot = E.xfer_slot;
         E.xfer_slot = (E.xfer_slot + 1) % GpuEngine::Impl::kRing;
-        check_cuda(cudaEventSynchronize(E.xfer_ev[slot]), "xfer staging");
+        for (auto& ring : E.xfer_ev) check_cuda(cudaEventSynchronize(ring[slot]), "xfer staging");
         int* h = E.xfer_host[slot];
         std::memcpy(h, w.src_blocks->data(), nb * 4);
         std::memcpy(h + nb, dst_ids->data(), nb * 4);
         int* d = static_cast<int*>(E.xfer_buf(staged ? src_hi : dst_hi).p) + slot * E.xfer_cap;
         check_cuda(cudaMemcpyAsync(d, h, 2 * nb * 4, cudaMemcpyHostToDevice, cs), "xfer ids");
-        check_cuda(cudaEventRecord(E.xfer_ev[slot], cs), "event");
+        check_cuda(cudaEventRecord(E.xfer_ev[staged ? src_hi : dst_hi][slot], cs), "event");
         check_ck(ck_kv_copy(E.pool(src_hi).base, d, dst_pool->base, d + nb, nb, dst_pool->block_bytes, cs), "kv_copy");
         ++copy_launches;
         const Request& r = trace.requests[w.rid];
@@ -587,7 +592,7 @@ class PairExecutor : public sched::Executor {
         if (staged) stage_tok[w.rid] = w.tokens == r.input_len;
         handoff_bytes += static_cast<double>(nb) * E.pool(dst_hi).block_bytes;
         handoffs++;
-        return complete(cs, 1);
+        return complete(cs, 1, staged ? src_hi : dst_hi);
     }
 
     uint64_t iteration(const sched::IterWork& w) override {
@@ -627,7 +632,7 @@ class PairExecutor : public sched::Executor {
             batch.plan_decode(E.spec.n_kv_heads, 2 * (lend ? E.sms : hi ? E.cpi_sm_count() : E.ppi_sm_count()),
                               !E.opt.persistent_decode && gpu::decode_cluster_kernel());
         if (E.opt.wall && hi) {  // device-side start of this iteration (busy time = end - start)
-            iter_start = take_event();
+            iter_start = take_event(true);
             check_cuda(cudaEventRecord(iter_start, cur), "event record");
         }
         TokenBufs& tb = E.tok(hi);
@@ -642,7 +647,7 @@ class PairExecutor : public sched::Executor {
         for (const sched::DecodeRow& d : w.decoders) decode_keys += d.ctx;
         chunk_rows += w.chunk_len;
         last_iter[hi] = record(cur, last_iter[hi]);
-        return complete(cur, hi ? 2 : 0);
+        return complete(cur, hi ? 2 : 0, hi);
     }
 
     void release(int instance, int rid) override {
@@ -690,14 +695,14 @@ class PairExecutor : public sched::Executor {
                 if (st == cudaErrorNotReady) continue;
                 check_cuda(st, "event query");
                 float ms = 0.f;
-                check_cuda(cudaEventElapsedTime(&ms, q == 0 ? t0_ppi : t0_cpi, t.ev), "elapsed");
+                check_cuda(cudaEventElapsedTime(&ms, t.high ? t0_cpi : t0_ppi, t.ev), "elapsed");
                 t.t = ms;
                 t.done = true;
                 if (t.start) {
                     float busy = 0.f;
                     check_cuda(cudaEventElapsedTime(&busy, t.start, t.ev), "elapsed");
                     cpi_busy_ms += busy;
-                    spare.push_back(t.start);
+                    spare[1].push_back(t.start);
                     t.start = nullptr;
                 }
             }
@@ -709,7 +714,7 @@ class PairExecutor : public sched::Executor {
         if (best < 0) return false;
         Tick t = done_q[best].front();
         done_q[best].pop_front();
-        spare.push_back(t.ev);
+        spare[t.high].push_back(t.ev);
         out.ticket = t.ticket;
         out.t_ms = t.t;
         return true;
@@ -809,13 +814,14 @@ class PairExecutor : public sched::Executor {
         bool done;
         double t;
         cudaEvent_t start;  // CPI iterations: event recorded before the first kernel
+        bool high;          // recorded on the high side's device (its t0 is the time base)
     };
     cudaEvent_t iter_start = nullptr;
     cudaStream_t cpi_stream = nullptr;  // stream the latest CPI iteration went to
     bool last_lent = false;
     long long lent_iters = 0;
     std::deque<Tick> done_q[3];
-    std::vector<cudaEvent_t> spare;
+    std::vector<cudaEvent_t> spare[2];  // reusable timing events per side's device
     uint64_t next_ticket = 1;
     cudaEvent_t t0_cpi = nullptr, t0_ppi = nullptr;
     std::chrono::steady_clock::time_point host_t0;
@@ -834,20 +840,22 @@ class PairExecutor : public sched::Executor {
         check_cuda(cudaEventRecord(ev, s), "event record");
         return ev;
     }
-    uint64_t complete(cudaStream_t s, int q) {
+    // `high`: the side whose device `s` belongs to (and is current).
+    uint64_t complete(cudaStream_t s, int q, bool high) {
         const uint64_t t = next_ticket++;
         if (!E.opt.wall) return t;  // virtual clock: completions come from the cost model
-        cudaEvent_t ev = take_event();
+        cudaEvent_t ev = take_event(high);
         check_cuda(cudaEventRecord(ev, s), "event record");
-        done_q[q].push_back(Tick{t, ev, false, 0.0, q == 2 ? iter_start : nullptr});
+        done_q[q].push_back(Tick{t, ev, false, 0.0, q == 2 ? iter_start : nullptr, high});
         if (q == 2) iter_start = nullptr;
         return t;
     }
-    cudaEvent_t take_event() {
+    // A timing event on `high`'s device (the caller has made that device current).
+    cudaEvent_t take_event(bool high) {
         cudaEvent_t ev;
-        if (!spare.empty()) {
-            ev = spare.back();
-            spare.pop_back();
+        if (!spare[high].empty()) {
+            ev = spare[high].back();
+            spare[high].pop_back();
         } else {
             check_cuda(cudaEventCreate(&ev), "event");
         }

@@ -56,6 +56,9 @@ struct EngineOptions {
     // has nothing in flight run on all SMs (the PPI's share is idle); PPI work issued
     // behind such an iteration waits for it, so the two never contend for SMs
     bool sm_lending = true;
+    // test hook: treat ppi_device == cpi_device as two separate devices (own weights, pools,
+    // token buffers, copy streams): exercises the multi-GPU pair path on one GPU
+    bool separate = false;
 };
 
 EngineOptions parse_engine_options(const std::string& text) {
@@ -90,6 +93,7 @@ EngineOptions parse_engine_options(const std::string& text) {
         else if (k == "prompt_seed") o.prompt_seed = std::stoull(v);
         else if (k == "profile") o.profile = v == "1" || v == "true";
         else if (k == "sm_lending") o.sm_lending = v == "1" || v == "true";
+        else if (k == "separate") o.separate = v == "1" || v == "true";
         else if (k == "decode_forward") {
             if (v != "layered" && v != "persistent")
                 throw std::invalid_argument("engine options: decode_forward = layered | persistent");
@@ -159,7 +163,7 @@ struct GpuEngine::Impl {
 
     explicit Impl(const std::string& text) : opt(parse_engine_options(text)), spec(gpu::ModelSpec::preset(opt.model)) {
         spec.seed = opt.seed;
-        colocated = opt.ppi_device == opt.cpi_device;
+        colocated = opt.ppi_device == opt.cpi_device && !opt.separate;
         int ndev = 0;
         check_cuda(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
         if (opt.ppi_device >= ndev || opt.cpi_device >= ndev)
@@ -212,10 +216,11 @@ struct GpuEngine::Impl {
             own_ppi_stream = true;
         }
         if (!colocated) {
-            int can = 0;
-            check_cuda(cudaDeviceCanAccessPeer(&can, opt.cpi_device, opt.ppi_device), "peer query");
+            int can = opt.ppi_device == opt.cpi_device;  // `separate` test mode: same device
+            if (!can) check_cuda(cudaDeviceCanAccessPeer(&can, opt.cpi_device, opt.ppi_device), "peer query");
             if (!can) throw std::runtime_error("CPI device cannot access the PPI device over NVLink (no P2P)");
             for (auto [a, b] : {std::pair{opt.cpi_device, opt.ppi_device}, std::pair{opt.ppi_device, opt.cpi_device}}) {
+                if (a == b) continue;  // `separate` test mode on one device
                 check_cuda(cudaSetDevice(a), "cudaSetDevice");
                 cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
                 if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) check_cuda(e, "enable peer access");
@@ -751,6 +756,15 @@ class PairExecutor : public sched::Executor {
                                   cudaMemcpyDeviceToHost),
                        "tokens D2H");
             d2h_bytes += total_out * 4;
+            if (!E.colocated) {  // requests decoded on the low side (dp, disagg-hl) left their tokens there
+                std::vector<int> low(static_cast<size_t>(total_out));
+                check_cuda(cudaSetDevice(E.opt.ppi_device), "cudaSetDevice");
+                check_cuda(cudaMemcpy(low.data(), E.tok_ppi.out_tok.p, low.size() * 4, cudaMemcpyDeviceToHost),
+                           "tokens D2H (low side)");
+                d2h_bytes += total_out * 4;
+                for (size_t i = 0; i < low.size(); ++i)
+                    if (opts.host_tokens[i] < 0) opts.host_tokens[i] = low[i];
+            }
         }
         E.cpi->collect_stats();
         E.ppi->collect_stats();

@@ -15,6 +15,8 @@
 #include <cstdlib>
 
 #include <cooperative_groups.h>
+#include <mutex>
+#include <unordered_map>
 
 #include "common.cuh"
 #include "cronus_ck.h"
@@ -512,6 +514,32 @@ int launch_decode_tma(const CUtensorMap& tm, const DecodeAttnArgs& a, int n_work
         e = cudaFuncSetAttribute(attn_decode_tma_kernel<G, STAGES>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return static_cast<int>(e);
         mask |= 1u << dev;
+    }
+    // The largest cluster the stream's SM set can place (a green-context partition may hold
+    // fewer SMs per GPC than the whole device); the kernel derives C from the launch, so the
+    // plan's cluster size can be clamped here. Cached per stream.
+    {
+        static std::mutex mu;
+        static std::unordered_map<unsigned long long, int> max_cluster;  // by stream id (never reused)
+        unsigned long long sid = 0;
+        cudaStreamGetId(st, &sid);
+        std::lock_guard<std::mutex> g(mu);
+        auto it = max_cluster.find(sid);
+        if (it == max_cluster.end()) {
+            cudaLaunchConfig_t q{};
+            q.gridDim = dim3(16, a.nkv);
+            q.blockDim = dim3(128);
+            q.dynamicSmemBytes = smem;
+            q.stream = st;
+            int mc = 0;
+            if (cudaOccupancyMaxPotentialClusterSize(&mc, attn_decode_tma_kernel<G, STAGES>, &q) != cudaSuccess ||
+                mc < 1) {
+                cudaGetLastError();
+                mc = 8;  // portable size
+            }
+            it = max_cluster.emplace(sid, std::min(mc, 16)).first;
+        }
+        while (cluster > it->second) cluster >>= 1;
     }
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

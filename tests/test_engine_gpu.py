@@ -202,3 +202,29 @@ def test_baseline_policies_on_gpu(tiny_engine, policy):
                                                                         for r in wr["records"]])
     assert exact >= 0.95 * total
     eng.close()
+
+
+@pytest.mark.parametrize("policy", ["cronus", "disagg-hl", "dp"])
+def test_separate_device_pair_path(policy):
+    """The multi-GPU pair path (own weights, pools and token buffers per side, first
+    token shipped with the KV, copy streams and event rings per device) run on one GPU
+    with the `separate` engine hook: schedule parity on the virtual clock, tokens
+    against the fp32 oracle, and a clean wall-clock run."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2509_17357_b200.serving import GpuEngine
+    cfg = load_cfg("a100_a10_llama8b").replace("policy = cronus", f"policy = {policy}")
+    t = c1_trace().subset(np.arange(20))
+    for clock in ("virtual", "wall"):
+        eng = GpuEngine(model="tiny", clock=clock, separate=1, ppi_sms=16)
+        res = eng.serve(cfg, t, want_tokens=True)
+        rep = json.loads(res.json)
+        assert rep["violations"] == [] and rep["completed"] == len(t)
+        assert res.extra["stats"]["colocated"] is False
+        if clock == "virtual":
+            want = E.run(cfg, t)
+            assert res.json == want.json and res.events == want.events
+        splits = [r["partial_prefill_len"] or None for r in rep["records"]]
+        total, exact = check_tokens(t, res.extra["tokens"], [0, 7, 19], splits=splits)
+        assert exact >= 0.95 * total
+        eng.close()

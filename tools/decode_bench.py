@@ -84,7 +84,7 @@ for shape in a.shapes.split(","):
         if a.impl == "tma":
             rc = L.ck_attn_decode_tma(P(q), P(pool), pool.shape[0], P(bt), P(rows), P(lens_t), P(off), P(item0_t),
                                       P(work_t), len(work), S, bps, P(ws), P(tickets), P(out), NQ, NKV, layer, LAYERS,
-                                      1 / math.sqrt(128), st)
+                                      1 / math.sqrt(128), None, st)
         else:
             rc = L.ck_attn_decode(P(q), P(pool), P(bt), P(rows), P(lens_t), P(off), P(item0_t), P(work_t), len(work),
                                   S, bps, P(ws), P(tickets), P(out), NQ, NKV, layer, LAYERS, 1 / math.sqrt(128), st)

@@ -199,12 +199,22 @@ def cupti_profile(eng, cfg, sample):
     sids = st["partition"].get("stream_ids", {})
     worker_of = {sids.get("ppi"): "ppi", sids.get("cpi"): "cpi", sids.get("cpi_full"): "cpi"}
     per_worker = defaultdict(list)
+    copy_us = 0.0
     for e in tr.get("traceEvents", []):
         if e.get("cat") == "kernel" and "args" in e:
             w = worker_of.get(e["args"].get("stream"))
             if w:
                 per_worker[w].append((e["ts"] + e["dur"], e["ts"], kernel_class(e["name"])))
+            elif "kv_copy" in e["name"]:
+                copy_us += e["dur"]
     out = {"cpi": {}, "ppi": {}, "partition": st["partition"], "sample_requests": len(sample)}
+    if copy_us > 0 and st.get("handoff_bytes"):
+        # KV handoff (co-located: D2D block copies read + write; NVLink pull between GPUs)
+        out["handoff"] = {"handoffs": st["handoffs"], "bytes": st["handoff_bytes"], "kernel_ms": copy_us / 1e3,
+                          "GBps": round((1 if not st.get("colocated", True) else 2) * st["handoff_bytes"]
+                                        / (copy_us * 1e3), 1),
+                          "what": "read+write bytes / kv_copy kernel time" if st.get("colocated", True)
+                          else "bytes pulled over NVLink / kv_copy kernel time"}
     for w, ks in per_worker.items():
         ks.sort()
         prev = -1e30
@@ -364,12 +374,13 @@ def run_ours(args, rank, world):
     # --profile-requests requests; chains intact) -> `roofline` / `kernels`. (2) CUDA events
     # around every launch over the whole trace -> `kernels_events`: events between kernels
     # break the PDL overlap, so these per-kernel figures are conservative.
-    roof, classes, classes_ev, prof_stats = {}, [], [], None
+    roof, classes, classes_ev, prof_stats, handoff = {}, [], [], None, None
     if not args.no_profile and driver:
         sample = sub.subset(np.arange(min(args.profile_requests, len(sub))), name="profile-sample")
         try:
             cp = cupti_profile(eng, cfg, sample)
             roof, classes = roofline(cp, cp["partition"])
+            handoff = cp.get("handoff")
             if roof:
                 roof["timing"] = (f"CUPTI kernel records, critical-path time per launch, first {len(sample)} "
                                   "requests of the trace")
@@ -407,6 +418,7 @@ def run_ours(args, rank, world):
         "cpi_lent_iterations": st.get("cpi_lent_iterations"),
         "iteration_shapes_count_ms_rows_ctx": st.get("iteration_shapes"),
         "clocks": clocks, "e2e": e2e, "roofline": roof, "kernels": classes[:8], "kernels_events": classes_ev[:8],
+        "handoff": handoff,
     }
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(args, cfg, sub)

@@ -1,0 +1,57 @@
+"""Token parity at the benchmarked shapes (LLaMA3-8B, Qwen2-7B): the B200 engine serves a few
+requests through the Cronus split (PPI partial prefill -> handoff -> CPI chunked prefill +
+decode) and every generated token is checked, teacher-forced, against a plain PyTorch fp32
+reference decoder on the GPU (tests/torch_ref.py) built from bit-identical weights.
+
+Tolerance: 0.5 logits (logit std ~3 at these shapes; bf16 activations through 28-32 layers):
+each GPU token's reference logit must be within 0.5 of the reference max, and equal to the
+reference argmax whenever the reference's top-1/top-2 margin exceeds 0.5.
+"""
+import json
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from conftest import load_cfg  # noqa: E402
+from oracle import numerics as NUM  # noqa: E402
+from paper_2509_17357_b200 import engine as E  # noqa: E402
+
+TOL = 0.5
+
+
+@pytest.mark.parametrize("model,cfg_name", [("llama3-8b", "a100_a10_llama8b"), ("qwen2-7b", "a100_a30_qwen7b")])
+def test_real_shape_tokens(model, cfg_name):
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2509_17357_b200._lib import lib
+    from paper_2509_17357_b200.serving import GpuEngine
+    from torch_ref import TorchWeights, greedy_check
+
+    spec = NUM.PRESETS[model]
+    cfg = load_cfg(cfg_name)
+    ins = np.array([37, 300, 700, 129], np.int32)
+    t = E.Trace(np.arange(len(ins), dtype=np.int32), np.zeros(len(ins)), ins, np.full(len(ins), 6, np.int32),
+                "real-shape parity")
+    eng = GpuEngine(model=model, clock="virtual", ppi_sms=40)
+    res = eng.serve(cfg, t, want_tokens=True)
+    eng.close()
+    rep = json.loads(res.json)
+    assert rep["violations"] == [] and rep["completed"] == len(t)
+    assert res.json == E.run(cfg, t).json  # the schedule is the reference's
+    torch.cuda.empty_cache()
+    w = TorchWeights(spec, lib())
+    total = exact = 0
+    deficit = 0.0
+    for i, r in enumerate(rep["records"]):
+        prompt = NUM.prompt_tokens(99, int(t.ids[i]), int(ins[i]), spec.vocab)
+        n, e, _, d = greedy_check(w, prompt, res.extra["tokens"][i], TOL, split=r["partial_prefill_len"] or None)
+        total += n
+        exact += e
+        deficit = max(deficit, d)
+    print(f"{model}: {exact}/{total} tokens equal to the reference argmax, max logit deficit {deficit:.3f}")
+    # every token is within TOL of the reference max (asserted per step); most are the argmax
+    # (random-init models at 128-152k vocab have frequent near-ties below TOL)
+    assert exact >= 0.7 * total, f"{exact}/{total} tokens equal to the reference argmax"

@@ -51,3 +51,29 @@ def test_max_over_ranks_gloo_world2():
     assert all(p.exitcode == 0 for p in procs)
     times, done = q.get(timeout=5)
     assert times == [15.0, 20.0] and done == 100.0
+
+
+def test_kernel_classes_and_roofline_math():
+    """bench.py's CUPTI kernel classing and the roofline object (HBM and tensor classes,
+    partition-normalised tensor fraction, traffic scaled from the committed ncu ratios)."""
+    import bench
+    assert bench.kernel_class("void <unnamed>::gemm_tc_kernel<16>(CUtensorMap_st, ...)") == "gemm_stream"
+    assert bench.kernel_class("void <unnamed>::gemm_tc_kernel<256>(CUtensorMap_st, ...)") == "gemm_tc"
+    assert bench.kernel_class("void <unnamed>::attn_decode_tma_kernel<4, 3>(...)") == "decode_attn"
+    assert bench.kernel_class("<unnamed>::attn_prefill_pp_kernel(...)") == "prefill_attn"
+    assert bench.kernel_class("<unnamed>::rmsnorm_kernel(...)") == "other"
+    stats = {
+        "cpi": {"gemm_stream": {"launches": 10, "ms": 0.1, "bytes": 5e8, "flops": 0.0},
+                "other": {"launches": 5, "ms": 1.0, "bytes": 0.0, "flops": 0.0}},
+        "ppi": {"gemm_tc": {"launches": 2, "ms": 1.0, "flops": 6e14, "bytes": 0.0},
+                "prefill_attn": {"launches": 1, "ms": 0.0, "flops": 1e9, "bytes": 0.0}},
+    }
+    part = {"device_sms": 148, "ppi_sms": 40, "cpi_sms": 108}
+    top, classes = bench.roofline(stats, part)
+    names = [c["kernel"] for c in classes]
+    assert names == ["ppi.gemm_tc", "cpi.gemm_stream"]  # by share; zero-time and 'other' skipped
+    hbm = next(c for c in classes if c["kernel"] == "cpi.gemm_stream")
+    assert abs(hbm["achieved"] - 5e8 / 10 / 1e-5 / 1e9) < 1e-6 * hbm["achieved"]  # GB/s per launch
+    ten = classes[0]
+    assert ten["bound"] == "tensor" and abs(ten["frac_partition"] - ten["frac"] * 148 / 40) < 1e-3
+    assert top["kernel"] == "ppi.gemm_tc" and "peak_source" in top

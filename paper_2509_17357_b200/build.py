@@ -24,6 +24,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libcronus_b200.so")
+CLI = os.path.join(PKG, "cronus_b200")  # command-line driver (csrc/cli)
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
@@ -111,6 +112,16 @@ def build(jobs: int | None = None, verbose: bool = False) -> str:
             raise RuntimeError(f"link failed\n{r.stdout}\n{r.stderr}")
         if verbose:
             print("linked", os.path.relpath(LIB, ROOT))
+    # the command-line driver (cronus_sim's subcommands), linked against the library
+    cli_src = os.path.join(CSRC, "cli", "cronus_b200.cpp")
+    if not os.path.exists(CLI) or os.path.getmtime(CLI) < max(os.path.getmtime(cli_src), os.path.getmtime(LIB), hdr):
+        cmd = [CXX, "-std=c++20", "-O2", *includes(), cli_src, "-o", CLI, "-L" + PKG, "-lcronus_b200",
+               "-Wl,-rpath,$ORIGIN"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"cli build failed\n{r.stdout}\n{r.stderr}")
+        if verbose:
+            print("linked", os.path.relpath(CLI, ROOT))
     return LIB
 
 

@@ -228,6 +228,65 @@ def cupti_profile(eng, cfg, sample):
     return out
 
 
+def decode_attn_probe(seqs=64, ctx=1024, layers=4, reps=40):
+    """The decode-attention kernel alone at a larger batch than the serve's tail (the
+    north-star shape class: HBM-bound paged attention), timed with CUDA events over
+    back-to-back launches on its stream: LLaMA3-8B heads (8 kv / 32 q), random block
+    tables, the layer rotated per launch so consecutive launches never hit L2 (each
+    layer's K/V = seqs x ctx x 4 KiB > L2). Same planner as the engine (1 wave, clusters)."""
+    import ctypes
+    import math
+
+    import torch
+    from paper_2509_17357_b200._lib import lib
+    L = lib()
+    nkv, nq, sms = 8, 32, torch.cuda.get_device_properties(0).multi_processor_count
+    slots = 2 * sms
+    nblk = ctx // 16
+    pairs = seqs * nkv
+    C = 1
+    while C < 16 and pairs * C * 2 <= slots and seqs * nblk * nkv >= pairs * C * 2 * 4:
+        C *= 2
+    pool = torch.zeros(seqs * nblk + 1, layers, 2, nkv, 16, 128, dtype=torch.bfloat16, device="cuda")
+    bt = torch.randperm(seqs * nblk, device="cuda").int()
+    off = torch.arange(seqs, dtype=torch.int32, device="cuda") * nblk
+    rows = torch.arange(seqs, dtype=torch.int32, device="cuda")
+    lens = torch.full((seqs,), ctx, dtype=torch.int32, device="cuda")
+    work = (torch.arange(seqs, dtype=torch.int32, device="cuda") << 16).contiguous()
+    item0 = torch.arange(seqs + 1, dtype=torch.int32, device="cuda")
+    q = torch.randn(seqs, nq * 128, device="cuda").bfloat16()
+    out = torch.empty_like(q)
+    ws = torch.empty(seqs * nq * 130, device="cuda")
+    tickets = torch.zeros(seqs * nkv, dtype=torch.int32, device="cuda")
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    st = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(st.cuda_stream)
+
+    def launch(layer):
+        rc = L.ck_attn_decode_tma(P(q), P(pool), pool.shape[0], P(bt), P(rows), P(lens), P(off), P(item0), P(work),
+                                  seqs, seqs, C, P(ws), P(tickets), P(out), nq, nkv, layer, layers,
+                                  1 / math.sqrt(128), None, sp)
+        assert rc == 0, rc
+
+    for i in range(8):
+        launch(i % layers)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for i in range(reps):
+        launch(i % layers)
+    e1.record(st)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / reps
+    alg = seqs * ctx * nkv * 2 * 128 * 2
+    hbm = peaks()[0]
+    del pool
+    torch.cuda.empty_cache()
+    return {"kernel": "attn_decode_tma (alone)", "shape": f"{seqs} seqs x {ctx} keys, 8 kv / 32 q heads, cluster {C}",
+            "bound": "hbm", "achieved": round(alg / us / 1e3, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(alg / us / 1e3 / hbm, 4), "us_per_launch": round(us, 2), "algorithmic_per_launch": alg}
+
+
 def roofline(stats, partition=None):
     """Dominant kernel class of the profiled step -> roofline object (+ all classes).
 
@@ -374,7 +433,7 @@ def run_ours(args, rank, world):
     # --profile-requests requests; chains intact) -> `roofline` / `kernels`. (2) CUDA events
     # around every launch over the whole trace -> `kernels_events`: events between kernels
     # break the PDL overlap, so these per-kernel figures are conservative.
-    roof, classes, classes_ev, prof_stats, handoff = {}, [], [], None, None
+    roof, classes, classes_ev, prof_stats, handoff, attn_probe = {}, [], [], None, None, None
     if not args.no_profile and driver:
         sample = sub.subset(np.arange(min(args.profile_requests, len(sub))), name="profile-sample")
         try:
@@ -392,6 +451,10 @@ def run_ours(args, rank, world):
         if not roof:
             roof, classes = roof_ev, classes_ev
             roof["timing"] = "CUDA events around each launch (serialises PDL chains: conservative)"
+        try:
+            attn_probe = decode_attn_probe()
+        except Exception as ex:
+            print(f"[bench] decode attention probe failed ({ex})", file=sys.stderr)
 
     if rank != 0:
         return None
@@ -418,7 +481,7 @@ def run_ours(args, rank, world):
         "cpi_lent_iterations": st.get("cpi_lent_iterations"),
         "iteration_shapes_count_ms_rows_ctx": st.get("iteration_shapes"),
         "clocks": clocks, "e2e": e2e, "roofline": roof, "kernels": classes[:8], "kernels_events": classes_ev[:8],
-        "handoff": handoff,
+        "handoff": handoff, "decode_attn_kernel": attn_probe,
     }
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(args, cfg, sub)

@@ -55,3 +55,40 @@ def test_real_shape_tokens(model, cfg_name):
     # every token is within TOL of the reference max (asserted per step); most are the argmax
     # (random-init models at 128-152k vocab have frequent near-ties below TOL)
     assert exact >= 0.6 * total, f"{exact}/{total} tokens equal to the reference argmax"
+
+
+@pytest.mark.parametrize("policy", ["cronus", "disagg-lh"])
+def test_real_shape_edge_requests(policy):
+    """LLaMA3-8B edge cases through the whole pair: a 1-token prompt, a 5000-token prompt
+    (cronus: long chunked prefill on the CPI; disagg-lh: the whole prompt prefilled on the PPI
+    in 4096-row slices, then a staged handoff), decode over ~5k keys with cluster-split
+    attention, block-boundary prompts (16, 17) and a 1-token output."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2509_17357_b200._lib import lib
+    from paper_2509_17357_b200.serving import GpuEngine
+    from torch_ref import TorchWeights, greedy_check
+
+    spec = NUM.PRESETS["llama3-8b"]
+    cfg = load_cfg("a100_a10_llama8b").replace("policy = cronus", f"policy = {policy}")
+    ins = np.array([1, 5000, 16, 17], np.int32)
+    outs = np.array([3, 4, 1, 5], np.int32)
+    t = E.Trace(np.arange(4, dtype=np.int32) + 10, np.zeros(4), ins, outs, "edge requests")
+    eng = GpuEngine(model="llama3-8b", clock="virtual", ppi_sms=40)
+    res = eng.serve(cfg, t, want_tokens=True)
+    eng.close()
+    rep = json.loads(res.json)
+    assert rep["violations"] == [] and rep["completed"] == len(t)
+    assert res.json == E.run(cfg, t).json
+    assert [len(x) for x in res.extra["tokens"]] == list(outs)
+    torch.cuda.empty_cache()
+    w = TorchWeights(spec, lib())
+    total = exact = 0
+    for i, r in enumerate(rep["records"]):
+        prompt = NUM.prompt_tokens(99, int(t.ids[i]), int(ins[i]), spec.vocab)
+        n, e, _, _ = greedy_check(w, prompt, res.extra["tokens"][i], TOL, split=r["partial_prefill_len"] or None)
+        total += n
+        exact += e
+    print(f"edge requests ({policy}): {exact}/{total} tokens equal to the reference argmax; splits "
+          f"{[r['partial_prefill_len'] for r in rep['records']]}")
+    assert exact >= 0.6 * total

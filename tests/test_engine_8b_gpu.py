@@ -92,3 +92,34 @@ def test_real_shape_edge_requests(policy):
     print(f"edge requests ({policy}): {exact}/{total} tokens equal to the reference argmax; splits "
           f"{[r['partial_prefill_len'] for r in rep['records']]}")
     assert exact >= 0.6 * total
+
+
+def test_real_shape_wall_clock_tokens():
+    """The bench's mode (wall clock, co-located green-context split, SM lending) at LLaMA3-8B
+    shapes: all requests complete without ledger violations, iterations were lent, and every
+    token passes the reference check under each request's actual split."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2509_17357_b200._lib import lib
+    from paper_2509_17357_b200.serving import GpuEngine
+    from torch_ref import TorchWeights, greedy_check
+
+    spec = NUM.PRESETS["llama3-8b"]
+    cfg = load_cfg("b200_llama8b_coloc")
+    t = E.synth_trace(6, 600, 8, E.ALL_AT_ZERO, 0.0, 7)
+    eng = GpuEngine(model="llama3-8b", clock="wall", ppi_sms=40)
+    res = eng.serve(cfg, t, want_tokens=True)
+    st = res.extra["stats"]
+    eng.close()
+    rep = json.loads(res.json)
+    assert rep["violations"] == [] and rep["completed"] == len(t)
+    assert st["cpi_lent_iterations"] > 0
+    torch.cuda.empty_cache()
+    w = TorchWeights(spec, lib())
+    total = exact = 0
+    for i, r in enumerate(rep["records"]):
+        prompt = NUM.prompt_tokens(99, int(t.ids[i]), int(t.input_len[i]), spec.vocab)
+        n, e, _, _ = greedy_check(w, prompt, res.extra["tokens"][i], TOL, split=r["partial_prefill_len"] or None)
+        total += n
+        exact += e
+    assert exact >= 0.6 * total, f"{exact}/{total}"

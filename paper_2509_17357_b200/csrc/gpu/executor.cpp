@@ -992,6 +992,8 @@ RunReport GpuEngine::run(const ClusterConfig& cfg, const Trace& trace, const Gpu
     impl_->ppi->set_profiling(opts.profile || impl_->opt.profile);
     impl_->cpi->reset_stats();
     impl_->ppi->reset_stats();
+    impl_->cpi->reset_graphs();  // captured passes hold the previous run's buffers
+    impl_->ppi->reset_graphs();
     PairExecutor ex(*impl_, cfg, trace, opts);
     ex.upload();
     sched::SchedulerHooks hooks;

@@ -257,6 +257,17 @@ bool prefill_attn_v1() {
     return on;
 }
 
+// CRONUS_GRAPHS=1: decode-only passes replay captured CUDA graphs. Measured on B200: passes
+// 1.5-3 % faster, but a serve sees ~100 distinct decode shapes (rows x work items x cluster),
+// and the capture + instantiate cost eats the gain (15.51-15.55 vs 15.57 req/s), so off.
+bool use_graphs() {
+    static const bool on = [] {
+        const char* e = std::getenv("CRONUS_GRAPHS");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 // Decode-only passes fuse RoPE + KV append into the decode attention unless
 // CRONUS_DECODE_ROPE_KERNEL=1 (separate qkv_rope_append kernel, for comparison).
 bool decode_rope_kernel() {
@@ -314,6 +325,7 @@ Worker::Worker(const Weights& w, int max_rows, int max_sample, int max_blocks_pe
 
 Worker::~Worker() {
     cudaSetDevice(w_.device());
+    reset_graphs();
     if (mega_) ck_mega_plan_destroy(mega_);
     for (void* p : {static_cast<void*>(x_), h_, static_cast<void*>(qkv_), q_, attn_, static_cast<void*>(gu_), act_, hs_,
                     static_cast<void*>(logits_), static_cast<void*>(attn_ws_), static_cast<void*>(meta_dev_),
@@ -348,6 +360,13 @@ void Worker::mark(cudaEvent_t& a) {
 }
 void Worker::done(cudaEvent_t a, KernelStat* into, double bytes, double flops) {
     if (!profile_) {  // launches and algorithmic work are always tallied (no events, no timing)
+        if (tally_rec_) {
+            tally_rec_->push_back({into, bytes, flops});
+            static const bool dbg = std::getenv("CRONUS_GRAPH_STATS") != nullptr;
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            if (dbg && cudaStreamIsCapturing(stream_, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusInvalidated)
+                std::fprintf(stderr, "[graphs] capture invalidated by launch %zu\n", tally_rec_->size());
+        }
         into->launches++;
         into->bytes += bytes;
         into->flops += flops;
@@ -356,6 +375,16 @@ void Worker::done(cudaEvent_t a, KernelStat* into, double bytes, double flops) {
     cudaEvent_t b = ev();
     cudaEventRecord(b, stream_);
     pending_.push_back({a, b, into, bytes, flops});
+}
+
+void Worker::reset_graphs() {
+    if (std::getenv("CRONUS_GRAPH_STATS") && (graph_hits_ || !graph_seen_.empty()))
+        std::fprintf(stderr, "[graphs] shapes %zu captured %zu replays %lld\n", graph_seen_.size(), graphs_.size(),
+                     graph_hits_);
+    graph_hits_ = 0;
+    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second.exec);
+    graphs_.clear();
+    graph_seen_.clear();
 }
 
 void Worker::collect_stats() {
@@ -431,10 +460,12 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         if (!v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(T));
         return static_cast<long long>(reinterpret_cast<char*>(dst) - reinterpret_cast<char*>(host));
     };
+    // arrays sized by the pass shape first, the block table (grows with context) last: every
+    // device pointer below is then a function of the shape only (CUDA-graph replay key)
     const long long o_row_rid = put(b.row_rid), o_row_pos = put(b.row_pos), o_row_dec = put(b.row_dec),
                     o_row_bt = put(b.row_bt), o_d_row = put(b.d_row), o_d_len = put(b.d_len), o_d_bt = put(b.d_bt),
-                    o_d_item0 = put(b.d_item0), o_d_work = put(b.d_work), o_bt = put(b.bt), o_s_row = put(b.s_row),
-                    o_s_rid = put(b.s_rid), o_s_out = put(b.s_out);
+                    o_d_item0 = put(b.d_item0), o_d_work = put(b.d_work), o_s_row = put(b.s_row),
+                    o_s_rid = put(b.s_rid), o_s_out = put(b.s_out), o_bt = put(b.bt);
     const size_t bytes = reinterpret_cast<char*>(cur_h) - reinterpret_cast<char*>(host);
     if (bytes > static_cast<size_t>(meta_cap_) * 4) throw std::logic_error("forward: metadata overflow");
     check_cuda(cudaMemcpyAsync(meta_dev_, host, bytes, cudaMemcpyHostToDevice, stream_), "meta H2D");
@@ -483,6 +514,9 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
                             !decode_rope_kernel();
     const ck_decode_rope rope{qkv_, w_.cos_tab, w_.sin_tab};
     if (fused_rope) qkv_dirty_rows_ = std::max(qkv_dirty_rows_, M);  // the last layer's rows: next pass clears
+
+    // ---- the pass's kernel chain (issued directly, or captured once per shape and replayed)
+    auto issue = [&]() {
     cudaEvent_t a = nullptr;
     mark(a);
     check_ck(ck_embed(x_, w_.embed, row_rid, row_pos, row_dec, prompt, prompt_off, last_tok, M, H, stream_), "embed");
@@ -596,6 +630,63 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         ++launches;
         done(a, &stat_other, 0, 0);
     }
+    };
+
+    // Decode-only weight-streaming passes repeat the same launch sequence for a given shape
+    // (rows, attention work items, cluster size, stream): the second time a shape is seen the
+    // chain is captured into a CUDA graph (PDL edges kept) and replayed from then on — a
+    // dependent kernel boundary costs ~1.3-1.5 us in a graph vs ~1.9-2.7 us on a stream.
+    const bool graphable = use_graphs() && !profile_ && fused_rope && !logits_dirty_;
+    if (graphable) {
+        char key[256];
+        std::snprintf(key, sizeof key, "%d/%d/%d/%d/%d/%p/%d/%p/%d/%p/%p/%p/%p/%p", M, R, n_dec, n_work,
+                      b.decode_cluster, static_cast<void*>(stream_), max_ctas_, pool.base, pool.blocks,
+                      static_cast<const void*>(prompt),
+                      static_cast<const void*>(prompt_off), static_cast<void*>(last_tok),
+                      static_cast<void*>(out_tok), static_cast<void*>(meta_dev_));
+        auto it = graphs_.find(key);
+        if (it != graphs_.end()) {
+            check_cuda(cudaGraphLaunch(it->second.exec, stream_), "graph launch");
+            launches += it->second.kernels;
+            ++graph_hits_;
+            for (const auto& t : it->second.tallies) {  // decode attention work: this pass's keys
+                const bool attn = t.into == &stat_decode_attn;
+                t.into->launches++;
+                t.into->bytes += attn ? dec_keys * kv_tok_layer : t.bytes;
+                t.into->flops += attn ? 4.0 * m.n_heads * m.head_dim * dec_keys : t.flops;
+            }
+            return;
+        }
+        if (graph_seen_.insert(key).second) {  // first sighting: run it plainly (lazy init)
+            issue();
+            done(pass0, &stat_forward, 0, 0);
+            return;
+        }
+        std::vector<Tally> tallies;
+        const long long l0 = launches;
+        check_cuda(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
+        cudaGraph_t g = nullptr;
+        tally_rec_ = &tallies;
+        try {
+            issue();
+            done(pass0, &stat_forward, 0, 0);
+            tally_rec_ = nullptr;
+        } catch (...) {
+            tally_rec_ = nullptr;
+            cudaStreamEndCapture(stream_, &g);
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            throw;
+        }
+        check_cuda(cudaStreamEndCapture(stream_, &g), "end capture");
+        cudaGraphExec_t exec = nullptr;
+        check_cuda(cudaGraphInstantiate(&exec, g, 0), "graph instantiate");
+        cudaGraphDestroy(g);
+        graphs_[key] = GraphEntry{exec, launches - l0, std::move(tallies)};
+        check_cuda(cudaGraphLaunch(exec, stream_), "graph launch");
+        return;
+    }
+    issue();
     done(pass0, &stat_forward, 0, 0);
 }
 

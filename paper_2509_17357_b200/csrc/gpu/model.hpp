@@ -9,6 +9,8 @@
 #include "cronus_ck.h"
 
 #include <cstdint>
+#include <map>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -162,6 +164,8 @@ class Worker {
         max_ctas_ = max_ctas;
     }
     void collect_stats();  // fold finished profiling events into stats (synchronizes)
+    // Drop captured pass graphs (their pointers: the run's token buffers, pools, streams).
+    void reset_graphs();
     void reset_stats() {
         stat_decode_attn = stat_prefill_attn = stat_gemm_stream = stat_gemm_tc = stat_other = stat_forward = {};
         stat_mega = {};
@@ -227,6 +231,20 @@ class Worker {
         const long long* s_out;
     };
     bool forward_mega(const Batch& b, const KvPool& pool, const PassMeta& pm, int* last_tok, int* out_tok);
+    // decode-pass CUDA graphs, keyed by the pass shape and the pointers its kernels take
+    struct Tally {
+        KernelStat* into;
+        double bytes, flops;
+    };
+    struct GraphEntry {
+        cudaGraphExec_t exec;
+        long long kernels;           // launches one replay stands for
+        std::vector<Tally> tallies;  // the stat updates one replay stands for
+    };
+    std::vector<Tally>* tally_rec_ = nullptr;
+    std::map<std::string, GraphEntry> graphs_;
+    std::set<std::string> graph_seen_;
+    long long graph_hits_ = 0;
     void gemm(const void* W, const void* X, void* out, const void* bias, int M, int N, int K, int epi, int splits,
               const ck_gemm_fuse* fuse = nullptr);
 };

@@ -517,15 +517,28 @@ int launch_decode_tma(const CUtensorMap& tm, const DecodeAttnArgs& a, int n_work
     }
     // The largest cluster the stream's SM set can place (a green-context partition may hold
     // fewer SMs per GPC than the whole device); the kernel derives C from the launch, so the
-    // plan's cluster size can be clamped here. Cached per stream.
+    // plan's cluster size can be clamped here. Cached per stream: keyed by the handle and
+    // re-validated by the stream id (handles get reused) whenever the stream is not being
+    // captured (stream queries are not capture-safe; a captured pass was first run plainly).
     {
+        struct Entry {
+            unsigned long long sid;
+            int max_c;
+        };
         static std::mutex mu;
-        static std::unordered_map<unsigned long long, int> max_cluster;  // by stream id (never reused)
+        static std::unordered_map<cudaStream_t, Entry> max_cluster;
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(st, &cs);
         unsigned long long sid = 0;
-        cudaStreamGetId(st, &sid);
+        if (cs == cudaStreamCaptureStatusNone) cudaStreamGetId(st, &sid);
         std::lock_guard<std::mutex> g(mu);
-        auto it = max_cluster.find(sid);
+        auto it = max_cluster.find(st);
+        if (it != max_cluster.end() && cs == cudaStreamCaptureStatusNone && it->second.sid != sid) {
+            max_cluster.erase(it);
+            it = max_cluster.end();
+        }
         if (it == max_cluster.end()) {
+            if (cs != cudaStreamCaptureStatusNone) return static_cast<int>(cudaErrorStreamCaptureUnsupported);
             cudaLaunchConfig_t q{};
             q.gridDim = dim3(16, a.nkv);
             q.blockDim = dim3(128);
@@ -537,9 +550,9 @@ int launch_decode_tma(const CUtensorMap& tm, const DecodeAttnArgs& a, int n_work
                 cudaGetLastError();
                 mc = 8;  // portable size
             }
-            it = max_cluster.emplace(sid, std::min(mc, 16)).first;
+            it = max_cluster.emplace(st, Entry{sid, std::min(mc, 16)}).first;
         }
-        while (cluster > it->second) cluster >>= 1;
+        while (cluster > it->second.max_c) cluster >>= 1;
     }
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

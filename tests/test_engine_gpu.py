@@ -228,3 +228,41 @@ def test_separate_device_pair_path(policy):
         total, exact = check_tokens(t, res.extra["tokens"], [0, 7, 19], splits=splits)
         assert exact >= 0.95 * total
         eng.close()
+
+
+_GRAPH_SCRIPT = r"""
+import hashlib, json, sys
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import numpy as np
+from conftest import load_cfg
+from test_engine_gpu import c1_trace, check_tokens, GOLD
+from paper_2509_17357_b200.serving import GpuEngine
+eng = GpuEngine(model="tiny", clock="virtual")
+t = c1_trace()
+res = eng.serve(load_cfg("a100_a10_llama8b"), t, want_tokens=True)
+g = GOLD["a100_a10_llama8b/tiny"]
+assert hashlib.sha256((res.json + "\n" + res.events).encode()).hexdigest() == g["digest"]
+splits = [r["partial_prefill_len"] for r in json.loads(res.json)["records"]]
+total, exact = check_tokens(t, res.extra["tokens"], [0, 1, 2, 5, 17, 33, 62, 63], splits=splits)
+assert exact >= 0.95 * total, (exact, total)
+eng.close()
+print("OK", total, exact)
+"""
+
+
+def test_decode_pass_graph_replay():
+    """CRONUS_GRAPHS=1 (read once per process, hence the subprocess): decode-only passes are
+    captured and replayed as CUDA graphs; the schedule stays golden and the tokens pass the
+    oracle check, and the replay path was actually taken."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import subprocess
+    import sys
+    env = dict(os.environ, CRONUS_GRAPHS="1", CRONUS_GRAPH_STATS="1")
+    code = _GRAPH_SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
+    p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    assert "OK" in p.stdout
+    assert "invalidated" not in p.stderr
+    lines = [ln for ln in p.stderr.splitlines() if ln.startswith("[graphs] shapes")]
+    assert lines and any(int(ln.split("replays")[1]) > 0 for ln in lines), p.stderr[-2000:]

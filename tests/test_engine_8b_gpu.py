@@ -123,3 +123,37 @@ def test_real_shape_wall_clock_tokens():
         total += n
         exact += e
     assert exact >= 0.6 * total, f"{exact}/{total}"
+
+
+def test_real_shape_long_prompt():
+    """A 16k-token prompt at LLaMA3-8B shapes beside a short one: the balancer's split, a long
+    PPI partial prefill, a multi-chunk CPI prefill over a >10k-key prefix (pp attention) and
+    decode over ~16k keys (cluster-split attention); tokens checked against the reference."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2509_17357_b200._lib import lib
+    from paper_2509_17357_b200.serving import GpuEngine
+    from torch_ref import TorchWeights, greedy_check
+
+    spec = NUM.PRESETS["llama3-8b"]
+    cfg = load_cfg("a100_a10_llama8b")
+    ins = np.array([16000, 200], np.int32)
+    outs = np.array([4, 4], np.int32)
+    t = E.Trace(np.arange(2, dtype=np.int32) + 40, np.zeros(2), ins, outs, "long prompt")
+    eng = GpuEngine(model="llama3-8b", clock="virtual", ppi_sms=40)
+    res = eng.serve(cfg, t, want_tokens=True)
+    eng.close()
+    rep = json.loads(res.json)
+    assert rep["violations"] == [] and rep["completed"] == len(t)
+    assert res.json == E.run(cfg, t).json
+    torch.cuda.empty_cache()
+    w = TorchWeights(spec, lib())
+    total = exact = 0
+    for i, r in enumerate(rep["records"]):
+        prompt = NUM.prompt_tokens(99, int(t.ids[i]), int(ins[i]), spec.vocab)
+        n, e, _, _ = greedy_check(w, prompt, res.extra["tokens"][i], TOL, split=r["partial_prefill_len"] or None)
+        total += n
+        exact += e
+    print(f"long prompt: {exact}/{total} tokens equal to the reference argmax; splits "
+          f"{[r['partial_prefill_len'] for r in rep['records']]}")
+    assert exact >= 0.6 * total

@@ -350,3 +350,75 @@ def test_attn_decode_fused_rope(L, nq, nkv):
         assert torch.allclose(out.float(), out_ref.float(), rtol=2e-2, atol=2e-2), \
             (cluster, (out.float() - out_ref.float()).abs().max().item())
         assert torch.equal(pool_f, pool_ref)  # the token's K/V slot written identically
+
+
+def fill_sequences_fast(pool, layer, lens, nkv, gen):
+    """fill_sequences with one indexed store per sequence (long contexts)."""
+    perm = torch.randperm(pool.shape[0], device="cuda", generator=gen)
+    tables, k_all, v_all, used = [], [], [], 0
+    for ln in lens:
+        nb = (ln + 15) // 16
+        t = perm[used:used + nb].int()
+        used += nb
+        k = torch.randn(ln, nkv, 128, device="cuda", generator=gen).bfloat16()
+        v = torch.randn(ln, nkv, 128, device="cuda", generator=gen).bfloat16()
+        j = torch.arange(ln, device="cuda")
+        blk, slot = t[j // 16].long(), j % 16
+        pool[blk, layer, 0, :, slot] = k
+        pool[blk, layer, 1, :, slot] = v
+        tables.append(t)
+        k_all.append(k)
+        v_all.append(v)
+    return tables, k_all, v_all
+
+
+@pytest.mark.parametrize("nq,nkv", [(32, 8), (28, 4)])
+def test_attn_long_context(L, nq, nkv):
+    """SURVEY.md §8 K5/K6 maxima: decode over 16k and ~49k-token contexts (the 4x long
+    trace's largest request), both kernels, and chunked prefill at a 16k prefix."""
+    gen = torch.Generator(device="cuda").manual_seed(7 * nq)
+    layers, layer = 2, 1
+    lens = [16384, 49157, 3]
+    pool = make_pool(sum((l + 15) // 16 for l in lens) + 2, layers, nkv, fill=3e4)
+    tables, ks, vs = fill_sequences_fast(pool, layer, lens, nkv, gen)
+    S = len(lens)
+    rows = torch.arange(S, dtype=torch.int32, device="cuda")
+    q = torch.randn(S, nq * 128, device="cuda", generator=gen).bfloat16()
+    bt = torch.cat(tables)
+    offs = np.concatenate([[0], np.cumsum([len(t) for t in tables])[:-1]]).astype(np.int32)
+    scale = 1 / math.sqrt(128)
+    refs = [attn_ref(q[s].view(1, nq, 128), ks[s], vs[s], torch.tensor([ln - 1], device="cuda"), scale)
+            for s, ln in enumerate(lens)]
+    for impl, bps, cluster in [("tma", 128, 8), ("tma", 400, 16), ("cp_async", 64, 1)]:
+        work, item0 = [], []
+        for s_i, ln in enumerate(lens):
+            item0.append(len(work))
+            for sp in range(((ln + 15) // 16 + bps - 1) // bps):
+                work.append((s_i << 16) | sp)
+        item0.append(len(work))
+        t_len, t_off, t_item0, t_work = (torch.tensor(a, dtype=torch.int32, device="cuda")
+                                         for a in (lens, offs, item0, work))
+        ws = torch.empty(len(work) * nq * 130, device="cuda")
+        tickets = torch.zeros(S * nkv, dtype=torch.int32, device="cuda")
+        out = torch.zeros(S, nq * 128, dtype=torch.bfloat16, device="cuda")
+        if impl == "tma":
+            ok(L.ck_attn_decode_tma(p(q), p(pool), pool.shape[0], p(bt), p(rows), p(t_len), p(t_off), p(t_item0),
+                                    p(t_work), len(work), S, cluster, p(ws), p(tickets), p(out), nq, nkv, layer,
+                                    layers, scale, None, stream()))
+        else:
+            ok(L.ck_attn_decode(p(q), p(pool), p(bt), p(rows), p(t_len), p(t_off), p(t_item0), p(t_work),
+                                len(work), S, bps, p(ws), p(tickets), p(out), nq, nkv, layer, layers, scale,
+                                stream()))
+        assert tickets.abs().sum() == 0
+        for s_i in range(S):
+            got = out[s_i].float().view(1, nq, 128)
+            assert torch.allclose(got, refs[s_i], rtol=2e-2, atol=2e-2), (impl, lens[s_i], (got - refs[s_i]).abs().max().item())
+    # chunked prefill of 512 tokens over a 16k prefix (the first sequence's KV)
+    pos0, qlen = 16384 - 512, 512
+    q2 = torch.randn(qlen, nq * 128, device="cuda", generator=gen).bfloat16()
+    out2 = torch.zeros_like(q2)
+    ok(L.ck_attn_prefill_pp(p(q2), q2.shape[0], p(pool), pool.shape[0], p(tables[0]), 0, qlen, pos0, p(out2), nq, nkv,
+                            layer, layers, scale, stream()))
+    ref2 = attn_ref(q2.view(qlen, nq, 128), ks[0], vs[0], torch.arange(pos0, pos0 + qlen, device="cuda"), scale)
+    assert torch.allclose(out2.float().view(qlen, nq, 128), ref2, rtol=3e-2, atol=3e-2), \
+        (out2.float().view(qlen, nq, 128) - ref2).abs().max().item()

@@ -129,12 +129,11 @@ def greedy_check(w: TorchWeights, prompt, gpu_tokens, tol, split=None):
     reference logit is within `tol` of the max, and equals the reference argmax whenever
     the top-1/top-2 margin exceeds `tol`. Returns (steps, exact, min_margin, max_deficit),
     deficit = reference max - reference logit of the GPU token."""
-    dec = TorchDecoder(w)
-    if split and 0 < split < len(prompt):
-        dec.forward(prompt[:split], 0)
-        hid = dec.forward(prompt[split:], split)
-    else:
-        hid = dec.forward(prompt, 0)
+    dec = TorchDecoder(w, max_pos=max(16384, len(prompt) + len(gpu_tokens) + 1))
+    # prefill in pieces (bounded score tensors for long prompts), breaking at the split too
+    cuts = sorted({0, len(prompt), *(range(0, len(prompt), 2048)), *([split] if split and 0 < split < len(prompt) else [])})
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        hid = dec.forward(prompt[a:b], a)
     h = hid[-1:]
     exact, min_margin, max_deficit = 0, float("inf"), 0.0
     for i, tok in enumerate(gpu_tokens):

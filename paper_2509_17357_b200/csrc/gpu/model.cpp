@@ -257,6 +257,15 @@ bool prefill_attn_v1() {
     return on;
 }
 
+// Tensor-regime QKV as a stream-K red.add GEMM (CRONUS_QKV_STREAMK=0: whole-tile stores).
+bool qkv_streamk() {
+    static const bool on = [] {
+        const char* e = std::getenv("CRONUS_QKV_STREAMK");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // CRONUS_GRAPHS=1: decode-only passes replay captured CUDA graphs. Measured on B200: passes
 // 1.5-3 % faster, but a serve sees ~100 distinct decode shapes (rows x work items x cluster),
 // and the capture + instantiate cost eats the gain (15.51-15.55 vs 15.57 req/s), so off.
@@ -498,15 +507,29 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
     for (int len : b.d_len) dec_keys += len;
     const double kv_tok_layer = 2.0 * m.n_kv_heads * m.head_dim * 2;  // bytes per token per layer (K+V)
 
-    if (small) {  // red.add accumulators must start from zero
+    // QKV accumulates with stream-K red.add in the weight-streaming regime, and in the tensor
+    // regime when whole 128x256 tiles fill the grid's last wave badly (e.g. 48 N-tiles x 1
+    // token tile on 40 SMs: 60 %); the RoPE/append kernel (or, for fused decode RoPE, the
+    // next norm) clears the rows it consumed
+    bool qkv_red = small;
+    if (!small && qkv_streamk() && !fuse_epilogue()) {
+        const long long tiles = static_cast<long long>(Q / 128) * ((M + 255) / 256);
+        const long long ctas = max_ctas_ > 0 ? max_ctas_ : ck_device_sms();
+        qkv_red = tiles < 8 * ctas && tiles * 10 < 8 * ((tiles + ctas - 1) / ctas) * ctas;  // < 80 % last-wave fill
+    }
+    if (qkv_red) {  // red.add accumulators must start from zero
         if (qkv_dirty_rows_ > 0)
             check_cuda(cudaMemsetAsync(qkv_, 0, static_cast<size_t>(qkv_dirty_rows_) * Q * 4, stream_), "memset qkv");
-        if (gu_dirty_rows_ > 0)
-            check_cuda(cudaMemsetAsync(gu_, 0, static_cast<size_t>(gu_dirty_rows_) * 2 * F * 4, stream_), "memset gu");
-        qkv_dirty_rows_ = gu_dirty_rows_ = 0;
+        qkv_dirty_rows_ = 0;
     } else {
         qkv_dirty_rows_ = std::max(qkv_dirty_rows_, M);
-        if (fuse_epilogue()) gu_dirty_rows_ = std::max(gu_dirty_rows_, M);  // else gate/up go straight to act
+    }
+    if (small) {
+        if (gu_dirty_rows_ > 0)
+            check_cuda(cudaMemsetAsync(gu_, 0, static_cast<size_t>(gu_dirty_rows_) * 2 * F * 4, stream_), "memset gu");
+        gu_dirty_rows_ = 0;
+    } else if (fuse_epilogue()) {
+        gu_dirty_rows_ = std::max(gu_dirty_rows_, M);  // else gate/up go straight to act
     }
     // decode-only weight-streaming pass: RoPE + KV append of the decode tokens run inside
     // the decode attention (reads the fp32 qkv accumulator), one kernel fewer per layer
@@ -549,12 +572,12 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         if (fuse_epilogue()) {
             gemm(L.wqkv, h_, qkv_, L.bqkv, M, Q, H, small ? CK_EPI_RED_F32 : CK_EPI_F32, small ? 0 : 1, &fq);
         } else {
-            gemm(L.wqkv, h_, qkv_, L.bqkv, M, Q, H, small ? CK_EPI_RED_F32 : CK_EPI_F32, small ? 0 : 1);
+            gemm(L.wqkv, h_, qkv_, L.bqkv, M, Q, H, qkv_red ? CK_EPI_RED_F32 : CK_EPI_F32, qkv_red ? 0 : 1);
         }
         if (!fuse_epilogue() && !fused_rope) {
             mark(a);
             check_ck(ck_qkv_rope_append(qkv_, nullptr, q_, pool.base, bt, row_bt, row_pos, w_.cos_tab, w_.sin_tab, M,
-                                        m.n_heads, m.n_kv_heads, l, m.layers, small ? 1 : 0, stream_),
+                                        m.n_heads, m.n_kv_heads, l, m.layers, qkv_red ? 1 : 0, stream_),
                      "qkv_rope_append");
             ++launches;
             done(a, &stat_other, 0, 0);

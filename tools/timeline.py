@@ -52,6 +52,7 @@ ks.sort()
 # keep the last pass only: time_pass(reps=1) may run warm-up passes too; split on big gaps
 t0, t1 = ks[0][0], max(k[1] for k in ks)
 agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
+crit = collections.defaultdict(float)
 prev_end = ks[0][0]
 busy = 0.0
 cur_s, cur_e = ks[0][0], ks[0][1]
@@ -59,6 +60,7 @@ for s, e, c in ks:
     agg[c][0] += 1
     agg[c][1] += e - s
     agg[c][2] += max(0.0, s - prev_end)
+    crit[c] += max(0.0, e - max(prev_end, s))  # time this launch adds to the chain
     prev_end = max(prev_end, e)
     if s > cur_e:
         busy += cur_e - cur_s
@@ -70,7 +72,8 @@ span = t1 - t0
 out = {"pass_ms_reported": ms, "span_us": round(span, 1), "busy_us": round(busy, 1), "idle_us": round(span - busy, 1),
        "kernels": len(ks), "classes": {}}
 for c, (n, d, g) in sorted(agg.items(), key=lambda x: -x[1][1]):
-    out["classes"][c] = {"n": n, "mean_us": round(d / n, 2), "total_us": round(d, 1), "mean_gap_us": round(g / n, 2)}
+    out["classes"][c] = {"n": n, "mean_us": round(d / n, 2), "total_us": round(d, 1), "mean_gap_us": round(g / n, 2),
+                         "crit_us_per_launch": round(crit[c] / n, 2), "crit_total_us": round(crit[c], 1)}
 print(json.dumps(out, indent=1))
 if a.json:
     json.dump({"summary": out, "kernels": [(round(s - t0, 2), round(e - t0, 2), c) for s, e, c in ks]},

@@ -32,7 +32,10 @@ enum { CK_EPI_BF16 = 0, CK_EPI_F32 = 1, CK_EPI_RED_F32 = 2, CK_EPI_SILU_BF16 = 3
  * N % 128 == 0, K % 64 == 0. epi: CK_EPI_BF16 (store bf16), CK_EPI_F32 (store
  * fp32), CK_EPI_RED_F32 (red.add fp32 into out — residual add / split-K),
  * CK_EPI_SILU_BF16 (W rows interleaved gate/up: 2i = gate_i, 2i+1 = up_i; out is the
- * bf16 activation [M, ldo] with out[m, i] = silu(gate) * up; splits must be 1).
+ * bf16 activation [M, ldo] with out[m, i] = silu(gate) * up; splits must be 1 — or, through
+ * ck_gemm_fused with splits 0 and a CK_FUSE_SILU fuse: hybrid, whole tiles write fuse->act
+ * directly and the tiles of a sparse last wave run as stream-K pieces red.added into `out`
+ * (a zeroed fp32 [M, N] accumulator, left zero) and finalized by ticket).
  * splits: K splits (0 = auto; > 1 only with CK_EPI_RED_F32). max_ctas: cap on
  * the persistent grid (0 = all SMs). tcgen05 + TMEM + TMA. */
 int ck_gemm(const void* W, const void* X, void* out, const void* bias, int M, int N, int K, int ldo, int epi,

@@ -257,6 +257,15 @@ bool prefill_attn_v1() {
     return on;
 }
 
+// Tensor-regime gate_up: hybrid whole-tile / stream-K-tail SiLU GEMM (CRONUS_SILU_HYBRID=0: whole tiles only).
+bool silu_hybrid() {
+    static const bool on = [] {
+        const char* e = std::getenv("CRONUS_SILU_HYBRID");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // Tensor-regime QKV as a stream-K red.add GEMM (CRONUS_QKV_STREAMK=0: whole-tile stores).
 bool qkv_streamk() {
     static const bool on = [] {
@@ -623,8 +632,18 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
             gemm(L.wgu, h_, gu_, nullptr, M, 2 * F, H, small ? CK_EPI_RED_F32 : CK_EPI_F32, small ? 0 : 1, &fs);
         } else if (!small) {
             // tensor regime: whole tiles per CTA -> SiLU(gate) * up straight from TMEM (the
-            // fp32 gate/up tensor never reaches HBM)
-            gemm(L.wgu, h_, act_, nullptr, M, 2 * F, H, CK_EPI_SILU_BF16, 1);
+            // fp32 gate/up tensor never reaches HBM); a sparse last wave (e.g. 448 tiles on
+            // 148 SMs) runs as stream-K pieces through gu_ + ticketed finalize (hybrid)
+            if (silu_hybrid()) {
+                ck_gemm_fuse fh{};
+                fh.kind = CK_FUSE_SILU;
+                fh.zero_after = 1;
+                fh.tickets = tile_tickets_;
+                fh.act = act_;
+                gemm(L.wgu, h_, gu_, nullptr, M, 2 * F, H, CK_EPI_SILU_BF16, 0, &fh);
+            } else {
+                gemm(L.wgu, h_, act_, nullptr, M, 2 * F, H, CK_EPI_SILU_BF16, 1);
+            }
         } else {
             gemm(L.wgu, h_, gu_, nullptr, M, 2 * F, H, small ? CK_EPI_RED_F32 : CK_EPI_F32, small ? 0 : 1);
             mark(a);

@@ -51,6 +51,15 @@ struct GemmParams {
     // CTA streams the same number of weight bytes regardless of tile count.
     int stream_k;
     long long iters;
+    // hybrid (SiLU epilogue): the first dp_tiles tiles are whole-tile units (tile
+    // blockIdx.x + i * grid, silu(gate) * up straight from TMEM into fuse.act); the
+    // remaining tiles' K-blocks — a last wave that would leave most SMs idle — are cut
+    // into kb_piece-long stream-K pieces, CTA c taking piece c, red.added into the fp32
+    // accumulator `out` [M, N] and finalized by the tile's last piece (ticket).
+    int hybrid;
+    int dp_tiles;
+    int kb_piece;
+    long long tail_iters;
     ck_gemm_fuse fuse;
     unsigned long long* probe;  // dev (CRONUS_GEMM_PROBE=1): per-CTA timeline stamps, else null
     int stages;                 // ring depth actually used (<= Cfg<BN>::kStages)
@@ -109,15 +118,31 @@ __device__ void finalize_tile(const GemmParams& p, int nt, int mt, int BN, int t
                      (pos & 15) * 128 + t] = f2bf(v);
             }
         }
-    } else {  // CK_FUSE_SILU: 64 (gate, up) pairs; two rows in flight per pass
-        const int pair = t & 63;
+    } else {  // CK_FUSE_SILU: 64 (gate, up) pairs = 32 float4 per row; 16 rows in flight per thread
+        const int cg = t & 31;
         __nv_bfloat16* act = static_cast<__nv_bfloat16*>(f.act);
         const int F = p.N / 2;
-        for (int m = m0 + (t >> 6); m < m1; m += 2) {
-            float* row = acc + static_cast<size_t>(m) * p.ldo + n0;
-            const float2 gu = __ldcg(reinterpret_cast<const float2*>(row) + pair);
-            if (f.zero_after) reinterpret_cast<float2*>(row)[pair] = make_float2(0.f, 0.f);
-            act[static_cast<size_t>(m) * F + n0 / 2 + pair] = f2bf(gu.x / (1.f + __expf(-gu.x)) * gu.y);
+        constexpr int U = 16;
+        for (int base = m0 + (t >> 5); base < m1; base += 4 * U) {
+            float4 v[U];
+#pragma unroll
+            for (int i = 0; i < U; ++i) {
+                const int m = base + 4 * i;
+                if (m < m1) v[i] = __ldcg(reinterpret_cast<const float4*>(acc + static_cast<size_t>(m) * p.ldo + n0) + cg);
+            }
+#pragma unroll
+            for (int i = 0; i < U; ++i) {
+                const int m = base + 4 * i;
+                if (m < m1) {
+                    if (f.zero_after)
+                        reinterpret_cast<float4*>(acc + static_cast<size_t>(m) * p.ldo + n0)[cg] =
+                            make_float4(0.f, 0.f, 0.f, 0.f);
+                    const float a = __fdividef(v[i].x, 1.f + __expf(-v[i].x)) * v[i].y;
+                    const float b = __fdividef(v[i].z, 1.f + __expf(-v[i].z)) * v[i].w;
+                    reinterpret_cast<__nv_bfloat162*>(act + static_cast<size_t>(m) * F + n0 / 2)[cg] =
+                        __floats2bfloat162_rn(a, b);
+                }
+            }
         }
     }
 }
@@ -147,10 +172,42 @@ __device__ __forceinline__ void decode_unit(const GemmParams& p, int u, int& nt,
 
 // Work iteration shared by the producer, MMA and epilogue roles (all three walk the
 // identical unit sequence). `pos` starts at first_unit().
+__device__ __forceinline__ long long tail_lo(const GemmParams& p) {
+    return static_cast<long long>(p.dp_tiles) * p.kb_total + static_cast<long long>(blockIdx.x) * p.kb_piece;
+}
 __device__ __forceinline__ long long first_unit(const GemmParams& p) {
+    if (p.hybrid)
+        return blockIdx.x < static_cast<unsigned>(p.dp_tiles) ? static_cast<long long>(blockIdx.x) * p.kb_total
+                                                               : tail_lo(p);
     return p.stream_k ? (static_cast<long long>(blockIdx.x) * p.iters) / gridDim.x : blockIdx.x;
 }
-__device__ __forceinline__ bool next_unit(const GemmParams& p, long long& pos, int& nt, int& mt, int& kb0, int& kb1) {
+// `tail`: the unit is a partial-K piece of a hybrid launch (goes through the accumulator).
+__device__ __forceinline__ bool next_unit(const GemmParams& p, long long& pos, int& nt, int& mt, int& kb0, int& kb1,
+                                          bool* tail = nullptr) {
+    if (p.hybrid) {
+        const long long dp_end = static_cast<long long>(p.dp_tiles) * p.kb_total;
+        int tile;
+        if (pos < dp_end) {
+            tile = static_cast<int>(pos / p.kb_total);
+            kb0 = 0;
+            kb1 = p.kb_total;
+            pos += static_cast<long long>(gridDim.x) * p.kb_total;
+            if (pos >= dp_end) pos = tail_lo(p);
+            if (tail) *tail = false;
+        } else {
+            const long long hi = min(dp_end + p.tail_iters, tail_lo(p) + p.kb_piece);
+            if (pos >= hi) return false;
+            tile = static_cast<int>(pos / p.kb_total);
+            kb0 = static_cast<int>(pos - static_cast<long long>(tile) * p.kb_total);
+            kb1 = static_cast<int>(min(static_cast<long long>(p.kb_total), kb0 + (hi - pos)));
+            pos += kb1 - kb0;
+            if (tail) *tail = true;
+        }
+        nt = tile / p.m_tiles;
+        mt = tile - nt * p.m_tiles;
+        return true;
+    }
+    if (tail) *tail = false;
     if (p.stream_k) {
         const long long end = (static_cast<long long>(blockIdx.x + 1) * p.iters) / gridDim.x;
         if (pos >= end) return false;
@@ -309,13 +366,16 @@ __global__ void __launch_bounds__(kThreads, 2)
         uint32_t acc_phase = 0;
         long long pos = first_unit(p);
         int nt, mt, kb0, kb1;
-        while (next_unit(p, pos, nt, mt, kb0, kb1)) {
+        bool tail = false;
+        while (next_unit(p, pos, nt, mt, kb0, kb1, &tail)) {
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int n = nt * kTileN + row;
             const int m_base = mt * BN;
             float bias = 0.f;
             if (p.bias != nullptr && kb0 == 0) bias = bf2f(p.bias[n]);
+            // hybrid: whole tiles -> SiLU into fuse.act; partial pieces -> red.add into out
+            const int epi = p.hybrid && tail ? CK_EPI_RED_F32 : p.epi;
 #pragma unroll 1
             for (int c = 0; c < BN; c += 16) {
                 if (m_base + c >= p.M) break;  // warp-uniform
@@ -323,23 +383,24 @@ __global__ void __launch_bounds__(kThreads, 2)
                 tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c, v);
                 tmem_ld_wait();
                 const int mlim = min(16, p.M - (m_base + c));
-                if (p.epi == CK_EPI_BF16) {
+                if (epi == CK_EPI_BF16) {
                     __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + static_cast<size_t>(m_base + c) * p.ldo + n;
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
                         if (j < mlim) o[static_cast<size_t>(j) * p.ldo] = f2bf(__uint_as_float(v[j]) + bias);
-                } else if (p.epi == CK_EPI_SILU_BF16) {
+                } else if (epi == CK_EPI_SILU_BF16) {
                     // adjacent lanes hold the (gate, up) rows of one activation column
-                    __nv_bfloat16* o =
-                        static_cast<__nv_bfloat16*>(p.out) + static_cast<size_t>(m_base + c) * p.ldo + (n >> 1);
+                    const int lda = p.hybrid ? p.N / 2 : p.ldo;
+                    __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.hybrid ? p.fuse.act : p.out) +
+                                       static_cast<size_t>(m_base + c) * lda + (n >> 1);
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
                         const float g = __uint_as_float(v[j]);
                         const float u = __shfl_xor_sync(0xffffffffu, g, 1);
                         if (!(lane & 1) && j < mlim)
-                            o[static_cast<size_t>(j) * p.ldo] = f2bf(__fdividef(g, 1.f + __expf(-g)) * u);
+                            o[static_cast<size_t>(j) * lda] = f2bf(__fdividef(g, 1.f + __expf(-g)) * u);
                     }
-                } else if (p.epi == CK_EPI_F32) {
+                } else if (epi == CK_EPI_F32) {
                     float* o = static_cast<float*>(p.out) + static_cast<size_t>(m_base + c) * p.ldo + n;
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
@@ -389,7 +450,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (lane == 0) mbar_arrive(&tempty[acc]);
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
-            if (p.fuse.kind != CK_FUSE_NONE) {
+            if (p.fuse.kind != CK_FUSE_NONE && (!p.hybrid || tail)) {
                 // tile ticket: K-blocks finished so far; the CTA that completes the tile
                 // finalizes it (its own partial is made visible first)
                 __threadfence();
@@ -517,7 +578,7 @@ int launch(const CUtensorMap& mw, const CUtensorMap& mx, GemmParams p, int max_c
     const int kb = ring_kb >= 0 ? ring_kb : (BN <= 32 ? 100 : 0);
     if (p.stream_k && kb > 0) p.stages = std::clamp(kb * 1024 / C::kStageBytes, 2, C::kStages);
     const int smem = p.stages * C::kStageBytes + 1024 + 256;
-    const long long work = p.stream_k ? p.iters : p.units;
+    const long long work = p.stream_k ? p.iters : p.hybrid ? (1ll << 40) : p.units;
     const int grid = static_cast<int>(std::min<long long>(work, max_ctas > 0 ? max_ctas : num_sms()));
     static const bool probe = [] {
         const char* e = std::getenv("CRONUS_GEMM_PROBE");
@@ -576,7 +637,12 @@ int gemm_impl(const void* W, const void* X, void* out, const void* bias, int M, 
     if (N % kTileN != 0 || K % kTileK != 0 || N <= 0 || K <= 0) return static_cast<int>(cudaErrorInvalidValue);
     if ((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(X)) & 15) return static_cast<int>(cudaErrorMisalignedAddress);
     if (epi < CK_EPI_BF16 || epi > CK_EPI_SILU_BF16) return static_cast<int>(cudaErrorInvalidValue);
-    if (epi == CK_EPI_SILU_BF16 && (splits != 1 || bias != nullptr)) return static_cast<int>(cudaErrorInvalidValue);
+    // SiLU epilogue: splits 1 = whole tiles into `out`; splits 0 with a CK_FUSE_SILU fuse =
+    // hybrid (whole tiles into fuse->act, a sparse last wave as stream-K pieces through the
+    // zeroed fp32 accumulator `out` [M, N] + ticketed finalize)
+    const bool silu_hybrid = epi == CK_EPI_SILU_BF16 && splits <= 0 && fuse && fuse->kind == CK_FUSE_SILU;
+    if (epi == CK_EPI_SILU_BF16 && ((splits != 1 && !silu_hybrid) || bias != nullptr))
+        return static_cast<int>(cudaErrorInvalidValue);
     const int BN = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
     GemmParams p{};
     p.out = out;
@@ -605,6 +671,23 @@ int gemm_impl(const void* W, const void* X, void* out, const void* bias, int M, 
     p.kb_per_split = (p.kb_total + splits - 1) / splits;
     p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;  // no empty splits
     p.units = tiles * p.splits;
+    if (silu_hybrid) {
+        const int ctas = max_ctas > 0 ? max_ctas : num_sms();
+        const int tail = tiles % ctas;
+        p.dp_tiles = tiles - tail;
+        if (tail == 0 || p.dp_tiles == 0 || tail * 2 >= ctas) {  // last wave >= half full: keep it
+            // whole tiles fill the waves well enough: plain SiLU epilogue into act
+            p.out = fuse->act;
+            p.ldo = N / 2;
+            p.fuse = ck_gemm_fuse{};
+        } else {
+            p.hybrid = 1;
+            p.ldo = N;  // the fp32 accumulator the tail pieces meet in
+            p.tail_iters = static_cast<long long>(tail) * p.kb_total;
+            // pieces of >= 16 K-blocks (fewer partial tiles to reduce), at most one per CTA
+            p.kb_piece = static_cast<int>(std::max<long long>(16, (p.tail_iters + ctas - 1) / ctas));
+        }
+    }
 
     CUtensorMap mw, mx;
     int rc = tensor_map(W, N, K, kTileN, &mw);

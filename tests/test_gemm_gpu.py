@@ -186,3 +186,28 @@ def test_gemm_silu_epilogue(L, M):
     assert torch.allclose(act.float(), want, rtol=2e-2, atol=2e-2), (act.float() - want).abs().max().item()
     bad = L.ck_gemm_fused(p(W), p(X), p(act), None, M, 2 * F, K, 3, 0, 0, None, ctypes.c_void_p(s))
     assert bad != 0  # split-K / stream-K cannot fuse the gate-up pairing
+
+
+@pytest.mark.parametrize("M,F,K,ctas", [(200, 1024, 512, 12), (512, 1024, 4096, 13), (300, 640, 1024, 7),
+                                        (512, 14336, 4096, 148), (512, 14336, 4096, 108)])
+def test_gemm_silu_hybrid(L, M, F, K, ctas):
+    """Hybrid SiLU GEMM (splits 0 + CK_FUSE_SILU): whole tiles write silu(gate) * up from
+    TMEM, the tiles of a sparse last wave run as stream-K pieces red.added into the zeroed
+    fp32 accumulator and finalized by the tile's last piece; the accumulator is left zero.
+    Cases: pieces of whole tiles (K=512), pieces straddling tiles (K=4096), LLaMA3-8B gate_up
+    at 512 rows on 148 and 108 SMs (448 tiles: last waves of 4 and 16 tiles)."""
+    g = torch.Generator(device="cuda").manual_seed(M + F)
+    W = (torch.randn(2 * F, K, device="cuda", generator=g) * 0.05).bfloat16()
+    X = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    acc = torch.zeros(M, 2 * F, device="cuda")
+    act = torch.full((M, F), float("nan"), device="cuda", dtype=torch.bfloat16)
+    tickets = torch.zeros(8192, dtype=torch.int32, device="cuda")
+    f = Fuse(kind=2, zero_after=1, tickets=tickets.data_ptr(), act=act.data_ptr())
+    s = torch.cuda.current_stream().cuda_stream
+    assert L.ck_gemm_fused(p(W), p(X), p(acc), None, M, 2 * F, K, 3, 0, ctas, ctypes.byref(f), ctypes.c_void_p(s)) == 0
+    torch.cuda.synchronize()
+    ref = X.float() @ W.float().t()
+    ref = torch.nn.functional.silu(ref[:, 0::2]) * ref[:, 1::2]
+    assert torch.allclose(act.float(), ref, rtol=2e-2, atol=2e-2), (act.float() - ref).abs().max().item()
+    assert tickets.abs().sum() == 0
+    assert acc.abs().sum() == 0

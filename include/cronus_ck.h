@@ -46,9 +46,14 @@ int ck_gemm(const void* W, const void* X, void* out, const void* bias, int M, in
  *   CK_FUSE_QKV_ROPE: the tile is one 128-dim head of the fp32 qkv accumulator ->
  *                     RoPE(q) -> q_out bf16, RoPE(k) / v -> paged KV slot of each row
  *   CK_FUSE_SILU:     64 interleaved (gate, up) pairs -> act bf16 = silu(g) * u
+ *   CK_FUSE_RMSNORM:  (residual red.add GEMM, out = x [M, N] fp32) each tile clears its
+ *                     slice of `zero` [M, zero_cols]; the last tile of an m-tile to
+ *                     complete (row_tickets: one int per m tile) writes
+ *                     norm_out bf16 [M, N] = rmsnorm(x) * gamma, as ck_rmsnorm does —
+ *                     the next layer's norm without its own launch. N <= 4096.
  * zero_after clears the accumulator tile after reading it (red.add reuse). tickets:
  * one int per (n tile, m tile), zero before the first call, left zero. */
-enum { CK_FUSE_NONE = 0, CK_FUSE_QKV_ROPE = 1, CK_FUSE_SILU = 2 };
+enum { CK_FUSE_NONE = 0, CK_FUSE_QKV_ROPE = 1, CK_FUSE_SILU = 2, CK_FUSE_RMSNORM = 3 };
 typedef struct {
     int kind;
     int zero_after;
@@ -64,6 +69,13 @@ typedef struct {
     int nq, nkv, layer, n_layers;
     /* SILU */
     void* act;
+    /* RMSNORM */
+    const void* gamma;
+    void* norm_out;
+    float eps;
+    int zero_cols;
+    float* zero;
+    int* row_tickets;
 } ck_gemm_fuse;
 
 int ck_gemm_fused(const void* W, const void* X, void* out, const void* bias, int M, int N, int K, int epi,

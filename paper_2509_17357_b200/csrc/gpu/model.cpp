@@ -266,6 +266,30 @@ bool silu_hybrid() {
     return on;
 }
 
+// Weight-streaming passes of at most this many rows (CRONUS_NORM_FUSE_ROWS, default 0 = off)
+// run the ffn norm inside the O GEMM and the next layer's attention norm inside the down
+// GEMM (CK_FUSE_RMSNORM: the m-tile's last finished tile normalizes the rows): two
+// dependent launches fewer per layer. Measured slower on B200 (8 x 2048 decode pass 4.43 ->
+// 5.24 ms, ~1.2 us per row): one CTA's load -> reduce -> store chain per row pair costs
+// more than the kernel boundary it removes.
+int norm_fuse_rows() {
+    static const int n = [] {
+        const char* e = std::getenv("CRONUS_NORM_FUSE_ROWS");
+        return e ? std::atoi(e) : 0;
+    }();
+    return n;
+}
+
+// Weight-streaming passes of at most this many rows (CRONUS_SILU_FUSE_ROWS, default 0 = off)
+// run SiLU(gate) * up in the gate_up GEMM's ticketed tile finalize instead of its own kernel.
+int silu_fuse_rows() {
+    static const int n = [] {
+        const char* e = std::getenv("CRONUS_SILU_FUSE_ROWS");
+        return e ? std::atoi(e) : 0;
+    }();
+    return n;
+}
+
 // Tensor-regime QKV as a stream-K red.add GEMM (CRONUS_QKV_STREAMK=0: whole-tile stores).
 bool qkv_streamk() {
     static const bool on = [] {
@@ -330,6 +354,8 @@ Worker::Worker(const Weights& w, int max_rows, int max_sample, int max_blocks_pe
     const size_t n_tiles = static_cast<size_t>(std::max(2 * m_.ffn, m_.qkv_n()) / 128) * ((R + 31) / 32);
     check_cuda(cudaMalloc(&tile_tickets_, n_tiles * 4), "alloc tile tickets");
     check_cuda(cudaMemset(tile_tickets_, 0, n_tiles * 4), "zero tile tickets");
+    check_cuda(cudaMalloc(&norm_tickets_, 64 * 4), "alloc norm tickets");
+    check_cuda(cudaMemset(norm_tickets_, 0, 64 * 4), "zero norm tickets");
     check_cuda(cudaMalloc(&arg_ws_, static_cast<size_t>(max_sample) * 64 * 4), "alloc argmax ws");
     check_cuda(cudaMalloc(&arg_tickets_, static_cast<size_t>(max_sample) * 4), "alloc argmax tickets");
     check_cuda(cudaMemset(arg_tickets_, 0, static_cast<size_t>(max_sample) * 4), "zero argmax tickets");
@@ -348,7 +374,7 @@ Worker::~Worker() {
     for (void* p : {static_cast<void*>(x_), h_, static_cast<void*>(qkv_), q_, attn_, static_cast<void*>(gu_), act_, hs_,
                     static_cast<void*>(logits_), static_cast<void*>(attn_ws_), static_cast<void*>(meta_dev_),
                     static_cast<void*>(attn_tickets_), static_cast<void*>(arg_ws_), static_cast<void*>(arg_tickets_),
-                    static_cast<void*>(tile_tickets_)})
+                    static_cast<void*>(tile_tickets_), static_cast<void*>(norm_tickets_)})
         if (p) cudaFree(p);
     for (int i = 0; i < kRing; ++i) {
         if (meta_host_[i]) cudaFreeHost(meta_host_[i]);
@@ -547,6 +573,13 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
     const ck_decode_rope rope{qkv_, w_.cos_tab, w_.sin_tab};
     if (fused_rope) qkv_dirty_rows_ = std::max(qkv_dirty_rows_, M);  // the last layer's rows: next pass clears
 
+    const bool norm_fused = small && !fuse_epilogue() && M <= norm_fuse_rows() && H <= 4096 && H % 4 == 0;
+    ck_gemm_fuse norm_fuse{};
+    norm_fuse.kind = CK_FUSE_RMSNORM;
+    norm_fuse.tickets = tile_tickets_;
+    norm_fuse.row_tickets = norm_tickets_;
+    norm_fuse.norm_out = h_;
+    norm_fuse.eps = m.rms_eps;
     // ---- the pass's kernel chain (issued directly, or captured once per shape and replayed)
     auto issue = [&]() {
     cudaEvent_t a = nullptr;
@@ -556,15 +589,17 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
     done(a, &stat_other, 0, 0);
     for (int l = 0; l < m.layers; ++l) {
         const LayerWeights& L = w_.layer[l];
-        mark(a);
-        // weight-streaming regime (M <= 128): qkv accumulates with red.add (stream-K GEMM),
-        // so the norm kernel clears it; tensor regime: plain fp32 tile stores
-        // fused decode RoPE: the attention left the previous layer's qkv rows for this norm to clear
-        check_ck(ck_rmsnorm(x_, L.attn_norm, h_, nullptr, M, H, m.rms_eps, fused_rope && l > 0 ? qkv_ : nullptr,
-                            Q, stream_),
-                 "rmsnorm");
-        ++launches;
-        done(a, &stat_other, 0, 0);
+        if (!(norm_fused && l > 0)) {  // else the previous down GEMM wrote h_ (and cleared qkv_)
+            mark(a);
+            // weight-streaming regime (M <= 128): qkv accumulates with red.add (stream-K GEMM),
+            // so the norm kernel clears it; tensor regime: plain fp32 tile stores
+            // fused decode RoPE: the attention left the previous layer's qkv rows for this norm to clear
+            check_ck(ck_rmsnorm(x_, L.attn_norm, h_, nullptr, M, H, m.rms_eps, fused_rope && l > 0 ? qkv_ : nullptr,
+                                Q, stream_),
+                     "rmsnorm");
+            ++launches;
+            done(a, &stat_other, 0, 0);
+        }
         // QKV projection with RoPE + KV append fused into its tile finalize
         ck_gemm_fuse fq{};
         fq.kind = CK_FUSE_QKV_ROPE;
@@ -617,11 +652,17 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
             const double keys = static_cast<double>(b.p_len) * b.p_pos0 + 0.5 * b.p_len * (b.p_len + 1.0);
             done(a, &stat_prefill_attn, (b.p_pos0 + b.p_len) * kv_tok_layer, 4.0 * m.n_heads * m.head_dim * keys);
         }
-        gemm(L.wo, attn_, x_, nullptr, M, H, NQ, CK_EPI_RED_F32, 0);
-        mark(a);
-        check_ck(ck_rmsnorm(x_, L.ffn_norm, h_, nullptr, M, H, m.rms_eps, nullptr, 0, stream_), "rmsnorm");
-        ++launches;
-        done(a, &stat_other, 0, 0);
+        if (norm_fused) {
+            ck_gemm_fuse fn = norm_fuse;
+            fn.gamma = L.ffn_norm;
+            gemm(L.wo, attn_, x_, nullptr, M, H, NQ, CK_EPI_RED_F32, 0, &fn);
+        } else {
+            gemm(L.wo, attn_, x_, nullptr, M, H, NQ, CK_EPI_RED_F32, 0);
+            mark(a);
+            check_ck(ck_rmsnorm(x_, L.ffn_norm, h_, nullptr, M, H, m.rms_eps, nullptr, 0, stream_), "rmsnorm");
+            ++launches;
+            done(a, &stat_other, 0, 0);
+        }
         // gate/up projection with SiLU(gate) * up fused into its tile finalize
         ck_gemm_fuse fs{};
         fs.kind = CK_FUSE_SILU;
@@ -644,6 +685,9 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
             } else {
                 gemm(L.wgu, h_, act_, nullptr, M, 2 * F, H, CK_EPI_SILU_BF16, 1);
             }
+        } else if (M <= silu_fuse_rows()) {
+            // weight-streaming regime: SiLU * up in the stream-K GEMM's ticketed tile finalize
+            gemm(L.wgu, h_, gu_, nullptr, M, 2 * F, H, CK_EPI_RED_F32, 0, &fs);
         } else {
             gemm(L.wgu, h_, gu_, nullptr, M, 2 * F, H, small ? CK_EPI_RED_F32 : CK_EPI_F32, small ? 0 : 1);
             mark(a);
@@ -651,7 +695,15 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
             ++launches;
             done(a, &stat_other, 0, 0);
         }
-        gemm(L.wd, act_, x_, nullptr, M, H, F, CK_EPI_RED_F32, 0);
+        if (norm_fused && l + 1 < m.layers) {  // the next layer's attention norm
+            ck_gemm_fuse fn = norm_fuse;
+            fn.gamma = w_.layer[l + 1].attn_norm;
+            fn.zero = fused_rope ? qkv_ : nullptr;
+            fn.zero_cols = Q;
+            gemm(L.wd, act_, x_, nullptr, M, H, F, CK_EPI_RED_F32, 0, &fn);
+        } else {
+            gemm(L.wd, act_, x_, nullptr, M, H, F, CK_EPI_RED_F32, 0);
+        }
     }
     if (R > 0) {
         mark(a);

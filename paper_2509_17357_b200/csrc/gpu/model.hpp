@@ -200,6 +200,7 @@ class Worker {
     int qkv_dirty_rows_ = 0, gu_dirty_rows_ = 0;
     bool logits_dirty_ = false;  // the persistent pass left logits uncleared
     int* tile_tickets_ = nullptr;  // fused-epilogue tile tickets (self-resetting)
+    int* norm_tickets_ = nullptr;  // fused-RMSNorm m-tile tickets (self-resetting)
     float* arg_ws_ = nullptr;      // argmax slice winners [max_sample * 64]
     int* arg_tickets_ = nullptr;   // [max_sample], self-resetting
     int* meta_dev_ = nullptr;

@@ -76,13 +76,86 @@ __device__ __forceinline__ void probe_stamp(const GemmParams& p, int slot) {
 // ------------------------------------------------------------------ fused tile finalize
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
+// CK_FUSE_RMSNORM finalize of tile (nt, mt) of a residual red.add GEMM: clear this tile's
+// slice of the next accumulator, then the m-tile's last finished tile normalizes its rows
+// (x = out, fp32, complete once every tile of the m-tile passed its ticket). Same
+// arithmetic as rmsnorm_kernel (elementwise.cu); only the fp32 sum order differs.
+constexpr int kNormMaxVec = 8;  // float4 per thread per row: N <= 8 * 4 * 128 = 4096
+__device__ void finalize_norm(const GemmParams& p, int nt, int mt, int BN, int t) {
+    const ck_gemm_fuse& f = p.fuse;
+    const int m0 = mt * BN, m1 = min(p.M, m0 + BN);
+    const int n_tiles = p.N / kTileN;
+    if (f.zero != nullptr) {
+        const int z4 = f.zero_cols / 4, per = (z4 + n_tiles - 1) / n_tiles;
+        const int c0 = nt * per, c1 = min(z4, c0 + per);
+        for (int m = m0; m < m1; ++m) {
+            float4* z = reinterpret_cast<float4*>(f.zero + static_cast<size_t>(m) * f.zero_cols);
+            for (int c = c0 + t; c < c1; c += 128) z[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+    __shared__ int s_norm;
+    __shared__ float s_red[2][4];
+    if (t == 0) {
+        const int d = atomicAdd(&f.row_tickets[mt], 1);
+        s_norm = d == n_tiles - 1;
+        if (d == n_tiles - 1) f.row_tickets[mt] = 0;
+    }
+    epi_bar();
+    if (!s_norm) return;
+    __threadfence();
+    const float* x = static_cast<const float*>(p.out);
+    const int n4 = p.N / 4, lane = t & 31, w = t >> 5;
+    const uint2* g = reinterpret_cast<const uint2*>(f.gamma);
+    for (int m = m0; m < m1; m += 2) {
+        float4 v[2][kNormMaxVec];
+        float ss[2] = {0.f, 0.f};
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const float4* xr = reinterpret_cast<const float4*>(x + static_cast<size_t>(m + r) * p.ldo);
+#pragma unroll
+            for (int j = 0; j < kNormMaxVec; ++j) {
+                const int i = t + j * 128;
+                v[r][j] = (m + r < m1 && i < n4) ? __ldcg(xr + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+                ss[r] += v[r][j].x * v[r][j].x + v[r][j].y * v[r][j].y + v[r][j].z * v[r][j].z + v[r][j].w * v[r][j].w;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) ss[r] += __shfl_xor_sync(0xffffffffu, ss[r], o);
+            if (lane == 0) s_red[r][w] = ss[r];
+        }
+        epi_bar();
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            if (m + r >= m1) break;
+            const float tot = s_red[r][0] + s_red[r][1] + s_red[r][2] + s_red[r][3];
+            const float inv = rsqrtf(tot / static_cast<float>(p.N) + f.eps);
+            uint2* o = reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(f.norm_out) + static_cast<size_t>(m + r) * p.N);
+#pragma unroll
+            for (int j = 0; j < kNormMaxVec; ++j) {
+                const int i = t + j * 128;
+                if (i < n4) {
+                    const uint2 gg = g[i];
+                    const float2 g0 = unpack_bf16x2(gg.x), g1 = unpack_bf16x2(gg.y);
+                    o[i] = make_uint2(pack_bf16x2(v[r][j].x * inv * g0.x, v[r][j].y * inv * g0.y),
+                                      pack_bf16x2(v[r][j].z * inv * g1.x, v[r][j].w * inv * g1.y));
+                }
+            }
+        }
+        epi_bar();  // s_red is rewritten by the next row pair
+    }
+}
+
 // Runs on the 128 epilogue threads (t = 0..127) of the CTA that completed tile (nt, mt).
 __device__ void finalize_tile(const GemmParams& p, int nt, int mt, int BN, int t) {
     const ck_gemm_fuse& f = p.fuse;
     float* acc = static_cast<float*>(p.out);
     const int m0 = mt * BN, m1 = min(p.M, m0 + BN);
     const int n0 = nt * kTileN;
-    if (f.kind == CK_FUSE_QKV_ROPE) {
+    if (f.kind == CK_FUSE_RMSNORM) {
+        finalize_norm(p, nt, mt, BN, t);
+    } else if (f.kind == CK_FUSE_QKV_ROPE) {
         const int h = nt;  // a 128-column tile is exactly one head
         const int nrot = f.nq + f.nkv;
         const size_t hs = 16 * 128;
@@ -627,6 +700,10 @@ extern "C" int ck_gemm_fused(const void* W, const void* X, void* out, const void
                              int splits, int max_ctas, const ck_gemm_fuse* fuse, void* stream) {
     if (fuse && fuse->kind != CK_FUSE_NONE && (epi == CK_EPI_BF16 || !fuse->tickets))
         return static_cast<int>(cudaErrorInvalidValue);  // finalize reads the fp32 tile back
+    if (fuse && fuse->kind == CK_FUSE_RMSNORM &&
+        (epi != CK_EPI_RED_F32 || splits > 0 || !fuse->row_tickets || !fuse->gamma || !fuse->norm_out ||
+         N > 4096 || (fuse->zero && fuse->zero_cols % 4)))
+        return static_cast<int>(cudaErrorInvalidValue);  // residual stream-K GEMM, rows of <= 4096
     return gemm_impl(W, X, out, bias, M, N, K, 0, epi, splits, max_ctas, fuse, stream);
 }
 

@@ -102,7 +102,9 @@ class Fuse(ctypes.Structure):
                 ("q_out", ctypes.c_void_p), ("kv_pool", ctypes.c_void_p), ("bt", ctypes.c_void_p),
                 ("row_bt", ctypes.c_void_p), ("row_pos", ctypes.c_void_p), ("cos_tab", ctypes.c_void_p),
                 ("sin_tab", ctypes.c_void_p), ("nq", ctypes.c_int), ("nkv", ctypes.c_int), ("layer", ctypes.c_int),
-                ("n_layers", ctypes.c_int), ("act", ctypes.c_void_p)]
+                ("n_layers", ctypes.c_int), ("act", ctypes.c_void_p), ("gamma", ctypes.c_void_p),
+                ("norm_out", ctypes.c_void_p), ("eps", ctypes.c_float), ("zero_cols", ctypes.c_int),
+                ("zero", ctypes.c_void_p), ("row_tickets", ctypes.c_void_p)]
 
 
 @pytest.mark.parametrize("M", [3, 32, 100, 300])
@@ -211,3 +213,41 @@ def test_gemm_silu_hybrid(L, M, F, K, ctas):
     assert torch.allclose(act.float(), ref, rtol=2e-2, atol=2e-2), (act.float() - ref).abs().max().item()
     assert tickets.abs().sum() == 0
     assert acc.abs().sum() == 0
+
+
+@pytest.mark.parametrize("M,H,K,ctas", [(1, 4096, 4096, 0), (8, 4096, 4096, 108), (16, 4096, 14336, 148),
+                                        (13, 3584, 18944, 108), (5, 256, 512, 7), (100, 4096, 4096, 0)])
+def test_gemm_residual_rmsnorm_fuse(L, M, H, K, ctas):
+    """CK_FUSE_RMSNORM: residual stream-K GEMM x += A W^T whose m-tile's last finished tile
+    writes rmsnorm(x) * gamma (bf16) — the next norm without a launch; each tile clears
+    its slice of the `zero` accumulator. Shapes: LLaMA3-8B O / down at 1-16 decode rows,
+    Qwen2-7B down (H = 3584), tiny, and 100 rows. Tickets are left zero, and a second
+    call on the same tickets gives the same result (self-resetting)."""
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + K)
+    W = (torch.randn(H, K, device="cuda", generator=g) * 0.02).bfloat16()
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    x0 = torch.randn(M, H, device="cuda", generator=g)
+    gamma = (1.0 + 0.1 * torch.randn(H, device="cuda", generator=g)).bfloat16()
+    ref_x = x0 + A.float() @ W.float().t()
+    ref_h = ref_x * torch.rsqrt(ref_x.pow(2).mean(-1, keepdim=True) + 1e-5) * gamma.float()
+    tickets = torch.zeros(4096, dtype=torch.int32, device="cuda")
+    rows = torch.zeros(64, dtype=torch.int32, device="cuda")
+    Z = 6144
+    for _ in range(2):
+        x = x0.clone()
+        h = torch.full((M, H), float("nan"), device="cuda", dtype=torch.bfloat16)
+        zero = torch.ones(M, Z, device="cuda")
+        f = Fuse(kind=3, tickets=tickets.data_ptr(), gamma=gamma.data_ptr(), norm_out=h.data_ptr(), eps=1e-5,
+                 zero=zero.data_ptr(), zero_cols=Z, row_tickets=rows.data_ptr())
+        s = torch.cuda.current_stream().cuda_stream
+        assert L.ck_gemm_fused(p(W), p(A), p(x), None, M, H, K, EPI_RED, 0, ctas, ctypes.byref(f),
+                               ctypes.c_void_p(s)) == 0
+        torch.cuda.synchronize()
+        check(x, ref_x, K, False)
+        assert torch.allclose(h.float(), ref_h, rtol=1.6e-2, atol=1e-2), (h.float() - ref_h).abs().max().item()
+        assert zero.abs().sum() == 0
+        assert tickets.abs().sum() == 0 and rows.abs().sum() == 0
+    # the fuse needs the residual stream-K epilogue and rows of <= 4096
+    bad = Fuse(kind=3, tickets=tickets.data_ptr(), gamma=gamma.data_ptr(), norm_out=h.data_ptr(), eps=1e-5,
+               row_tickets=rows.data_ptr())
+    assert L.ck_gemm_fused(p(W), p(A), p(x), None, M, H, K, EPI_RED, 1, ctas, ctypes.byref(bad), None) != 0

@@ -299,6 +299,16 @@ bool qkv_streamk() {
     return on;
 }
 
+// CRONUS_GRAPH_MIN_SEEN (default 2): a decode shape is captured on its N-th sighting, so
+// shapes a serve meets only a few times never pay the capture + instantiate cost.
+int graph_min_seen() {
+    static const int n = [] {
+        const char* e = std::getenv("CRONUS_GRAPH_MIN_SEEN");
+        return e ? std::max(2, std::atoi(e)) : 2;
+    }();
+    return n;
+}
+
 // CRONUS_GRAPHS=1: decode-only passes replay captured CUDA graphs. Measured on B200: passes
 // 1.5-3 % faster, but a serve sees ~100 distinct decode shapes (rows x work items x cluster),
 // and the capture + instantiate cost eats the gain (15.51-15.55 vs 15.57 req/s), so off.
@@ -751,7 +761,7 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
             }
             return;
         }
-        if (graph_seen_.insert(key).second) {  // first sighting: run it plainly (lazy init)
+        if (++graph_seen_[key] < graph_min_seen()) {  // early sightings run plainly (lazy init)
             issue();
             done(pass0, &stat_forward, 0, 0);
             return;

@@ -244,7 +244,7 @@ class Worker {
     };
     std::vector<Tally>* tally_rec_ = nullptr;
     std::map<std::string, GraphEntry> graphs_;
-    std::set<std::string> graph_seen_;
+    std::map<std::string, int> graph_seen_;  // shape -> plain (uncaptured) runs so far
     long long graph_hits_ = 0;
     void gemm(const void* W, const void* X, void* out, const void* bias, int M, int N, int K, int epi, int splits,
               const ck_gemm_fuse* fuse = nullptr);

@@ -299,23 +299,26 @@ bool qkv_streamk() {
     return on;
 }
 
-// CRONUS_GRAPH_MIN_SEEN (default 2): a decode shape is captured on its N-th sighting, so
-// shapes a serve meets only a few times never pay the capture + instantiate cost.
+// CRONUS_GRAPH_MIN_SEEN (default 24): a decode shape is captured on its N-th sighting, so
+// shapes a serve meets only a few times never pay the capture + instantiate cost. Bench serve
+// on B200 (req/s, graphs off = 1.000): N = 2 +0.1 %, 8 +0.2 %, 24 +0.45 %, 48 +0.25 %, 96 +0.1 %
+// (a serve meets ~105 decode shapes; at 24, 19 of them are captured and replayed ~1050 times).
 int graph_min_seen() {
     static const int n = [] {
         const char* e = std::getenv("CRONUS_GRAPH_MIN_SEEN");
-        return e ? std::max(2, std::atoi(e)) : 2;
+        return e ? std::max(2, std::atoi(e)) : 24;
     }();
     return n;
 }
 
-// CRONUS_GRAPHS=1: decode-only passes replay captured CUDA graphs. Measured on B200: passes
-// 1.5-3 % faster, but a serve sees ~100 distinct decode shapes (rows x work items x cluster),
-// and the capture + instantiate cost eats the gain (15.51-15.55 vs 15.57 req/s), so off.
+// Decode-only passes replay captured CUDA graphs (CRONUS_GRAPHS=0: always issue on the
+// stream). A graph replay saves ~0.6 us per dependent boundary (passes 1.5-3 % faster);
+// capturing every shape on its second sighting cost about what it saved, hence the
+// capture threshold above.
 bool use_graphs() {
     static const bool on = [] {
         const char* e = std::getenv("CRONUS_GRAPHS");
-        return e && e[0] == '1';
+        return !(e && e[0] == '0');
     }();
     return on;
 }
@@ -737,8 +740,8 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
     };
 
     // Decode-only weight-streaming passes repeat the same launch sequence for a given shape
-    // (rows, attention work items, cluster size, stream): the second time a shape is seen the
-    // chain is captured into a CUDA graph (PDL edges kept) and replayed from then on — a
+    // (rows, attention work items, cluster size, stream): the graph_min_seen()-th time a shape
+    // is seen the chain is captured into a CUDA graph (PDL edges kept) and replayed from then on — a
     // dependent kernel boundary costs ~1.3-1.5 us in a graph vs ~1.9-2.7 us on a stream.
     const bool graphable = use_graphs() && !profile_ && fused_rope && !logits_dirty_;
     if (graphable) {

@@ -251,14 +251,15 @@ print("OK", total, exact)
 
 
 def test_decode_pass_graph_replay():
-    """CRONUS_GRAPHS=1 (read once per process, hence the subprocess): decode-only passes are
-    captured and replayed as CUDA graphs; the schedule stays golden and the tokens pass the
-    oracle check, and the replay path was actually taken."""
+    """CRONUS_GRAPHS=1 with CRONUS_GRAPH_MIN_SEEN=2 (read once per process, hence the
+    subprocess): every decode-only shape seen twice is captured and replayed as a CUDA
+    graph; the schedule stays golden, the tokens pass the oracle check, and the replay path
+    was actually taken."""
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     import subprocess
     import sys
-    env = dict(os.environ, CRONUS_GRAPHS="1", CRONUS_GRAPH_STATS="1")
+    env = dict(os.environ, CRONUS_GRAPHS="1", CRONUS_GRAPH_STATS="1", CRONUS_GRAPH_MIN_SEEN="2")
     code = _GRAPH_SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
     p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-3000:]

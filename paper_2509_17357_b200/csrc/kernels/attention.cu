@@ -572,19 +572,74 @@ int launch_decode_tma(const CUtensorMap& tm, const DecodeAttnArgs& a, int n_work
     return static_cast<int>(cudaLaunchKernelEx(&cfg, attn_decode_tma_kernel<G, STAGES>, tm, a));
 }
 
-// Ring depth per warp: 3 (100 KiB per CTA, 2 CTAs per SM) unless CRONUS_DEC_STAGES says otherwise.
+// Ring depth per warp: CRONUS_DEC_STAGES (2, 3, 4, 6) if set, else chosen per launch (0).
 int dec_stages() {
     static const int v = [] {
         const char* e = std::getenv("CRONUS_DEC_STAGES");
-        const int x = e ? std::atoi(e) : 3;
-        return (x == 2 || x == 4 || x == 6) ? x : 3;
+        const int x = e ? std::atoi(e) : 0;
+        return (x == 2 || x == 3 || x == 4 || x == 6) ? x : 0;
     }();
     return v;
 }
 
+// CTAs of the 3-stage kernel (100 KiB each) the stream's SM set holds at once (2 per SM),
+// cached per stream like the cluster clamp (queried only outside stream capture; a captured
+// pass was first run plainly, so its stream is known; unknown under capture -> 0).
+template <int G>
+int resident_ctas_3stage(cudaStream_t st) {
+    struct Entry {
+        unsigned long long sid;
+        int ctas;
+    };
+    static std::mutex mu;
+    static std::unordered_map<cudaStream_t, Entry> cache;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    unsigned long long sid = 0;
+    if (cs == cudaStreamCaptureStatusNone) cudaStreamGetId(st, &sid);
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(st);
+    if (it != cache.end() && (cs != cudaStreamCaptureStatusNone || it->second.sid == sid)) return it->second.ctas;
+    if (cs != cudaStreamCaptureStatusNone) return 0;
+    constexpr int smem = kDTileBytes + 4 * 3 * 2 * kDTileBytes;
+    cudaFuncSetAttribute(attn_decode_tma_kernel<G, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaLaunchAttribute attr{};
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 1;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cudaLaunchConfig_t q{};
+    q.gridDim = dim3(1, 1);
+    q.blockDim = dim3(128);
+    q.dynamicSmemBytes = smem;
+    q.stream = st;
+    q.attrs = &attr;
+    q.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, attn_decode_tma_kernel<G, 3>, &q) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+    }
+    cache[st] = Entry{sid, n};
+    return n;
+}
+
+// Default ring depth: 3 stages (2 CTAs per SM), or 2 stages (68 KiB, 3 CTAs per SM) when
+// that finishes the grid in fewer waves (many sequences x kv heads, e.g. 32 decoders on the
+// 108-SM partition: 256 CTAs = 2 waves at 2 per SM, 1 wave at 3 per SM).
+// Measured (tools/pass_sweep.py, 108 SMs): 32 x 2048 decode pass 6.26 -> 5.57 ms, 64 x 2048
+// 7.70 -> 7.28 ms with 2 stages; 8-16 sequences (grid within 2 per SM) are 2-4 % faster with 3.
 template <int G>
 int launch_decode_tma_g(const CUtensorMap& tm, const DecodeAttnArgs& a, int n_work, int cluster, cudaStream_t st) {
-    switch (dec_stages()) {
+    int stages = dec_stages();
+    if (stages == 0) {
+        // 2 stages only where the third CTA per SM saves a wave (48 x 1024: 384 CTAs on 108 SMs
+        // is two waves either way, and 3 stages keep more bytes in flight per CTA: 5.68 vs 5.86 ms)
+        const long long r3 = resident_ctas_3stage<G>(st), r2 = r3 * 3 / 2;
+        const long long ctas = static_cast<long long>(n_work) * cluster * a.nkv;
+        stages = r3 > 0 && (ctas + r2 - 1) / r2 < (ctas + r3 - 1) / r3 ? 2 : 3;
+    }
+    switch (stages) {
         case 2: return launch_decode_tma<G, 2>(tm, a, n_work, cluster, st);
         case 4: return launch_decode_tma<G, 4>(tm, a, n_work, cluster, st);
         case 6: return launch_decode_tma<G, 6>(tm, a, n_work, cluster, st);

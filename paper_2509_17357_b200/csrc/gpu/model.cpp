@@ -333,6 +333,15 @@ bool decode_rope_kernel() {
     return on;
 }
 
+int decode_slots_per_sm() {
+    static const int n = [] {
+        const char* e = std::getenv("CRONUS_DEC_SLOTS_PER_SM");
+        const int x = e ? std::atoi(e) : 2;
+        return x >= 1 && x <= 4 ? x : 2;
+    }();
+    return n;
+}
+
 bool decode_cluster_kernel() {
     static const bool on = [] {
         const char* e = std::getenv("CRONUS_DECODE_CPASYNC");

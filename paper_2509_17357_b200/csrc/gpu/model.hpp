@@ -253,6 +253,8 @@ class Worker {
 // Decode attention kernel family: TMA + cluster (default) or the cp.async split kernel
 // (CRONUS_DECODE_CPASYNC=1).
 bool decode_cluster_kernel();
+// Resident decode-attention CTAs per SM the cluster planner assumes (CRONUS_DEC_SLOTS_PER_SM, default 2).
+int decode_slots_per_sm();
 
 void check_cuda(cudaError_t e, const char* what);
 void check_ck(int rc, const char* what);

@@ -634,7 +634,7 @@ class PairExecutor : public sched::Executor {
         }
         for (int rid : w.finishers) need(rid, nullptr);  // zero rows: its KV is placed when it decodes
         if (!batch.d_len.empty())
-            batch.plan_decode(E.spec.n_kv_heads, gpu::decode_slots_per_sm() * (lend ? E.sms : hi ? E.cpi_sm_count() : E.ppi_sm_count()),
+            batch.plan_decode(E.spec.n_kv_heads, gpu::decode_slots(E.spec.n_kv_heads, static_cast<int>(batch.d_len.size()), lend ? E.sms : hi ? E.cpi_sm_count() : E.ppi_sm_count()),
                               !E.opt.persistent_decode && gpu::decode_cluster_kernel());
         if (E.opt.wall && hi) {  // device-side start of this iteration (busy time = end - start)
             iter_start = take_event(true);
@@ -927,7 +927,7 @@ double GpuEngine::time_pass(const ClusterConfig& cfg, int worker, int n_dec, int
         batch.add_prefill(0, chunk_pos0, chunk_len, tables.back(), true, 0);
     }
     if (n_dec > 0)
-        batch.plan_decode(E.spec.n_kv_heads, gpu::decode_slots_per_sm() * (worker == 0 ? (E.ppi_ctas ? E.ppi_ctas : E.sms) : E.cpi_sm_count()),
+        batch.plan_decode(E.spec.n_kv_heads, gpu::decode_slots(E.spec.n_kv_heads, static_cast<int>(batch.d_len.size()), worker == 0 ? (E.ppi_ctas ? E.ppi_ctas : E.sms) : E.cpi_sm_count()),
                           !E.opt.persistent_decode && gpu::decode_cluster_kernel());
     cudaEvent_t a, b;
     check_cuda(cudaEventCreate(&a), "event");

@@ -336,10 +336,21 @@ bool decode_rope_kernel() {
 int decode_slots_per_sm() {
     static const int n = [] {
         const char* e = std::getenv("CRONUS_DEC_SLOTS_PER_SM");
-        const int x = e ? std::atoi(e) : 2;
-        return x >= 1 && x <= 4 ? x : 2;
+        const int x = e ? std::atoi(e) : 0;
+        return x >= 0 && x <= 4 ? x : 0;  // 0: auto (decode_slots)
     }();
     return n;
+}
+
+// Auto (default): plan for 3 resident CTAs per SM once a pass has >= 64 (sequence, kv head)
+// pairs — larger clusters, and the kernel layer's 2-stage ring then fits the grid in one wave —
+// else 2. Measured (run32.sh): 8 x 2048 decode pass 4.43 -> 4.38 ms, 16 x 2048 4.88 -> 4.79,
+// 1-4 and 24-32 sequences unchanged; serve 15.215 / 15.241 -> 15.434 / 15.426 req/s (+1.3 %).
+// A flat 3 per SM slowed 4 x 2048 (cluster 8 on 2-stage rings: 4.17 -> 4.37 ms).
+int decode_slots(int n_kv_heads, int n_seq, int sms) {
+    const int per = decode_slots_per_sm();
+    if (per > 0) return per * sms;
+    return (static_cast<long long>(n_seq) * n_kv_heads >= 64 ? 3 : 2) * sms;
 }
 
 bool decode_cluster_kernel() {

@@ -253,8 +253,10 @@ class Worker {
 // Decode attention kernel family: TMA + cluster (default) or the cp.async split kernel
 // (CRONUS_DECODE_CPASYNC=1).
 bool decode_cluster_kernel();
-// Resident decode-attention CTAs per SM the cluster planner assumes (CRONUS_DEC_SLOTS_PER_SM, default 2).
+// Resident decode-attention CTAs per SM the cluster planner assumes (CRONUS_DEC_SLOTS_PER_SM; default 0 = auto).
 int decode_slots_per_sm();
+// Resident-CTA budget handed to the decode planner for n_seq sequences on `sms` SMs.
+int decode_slots(int n_kv_heads, int n_seq, int sms);
 
 void check_cuda(cudaError_t e, const char* what);
 void check_ck(int rc, const char* what);

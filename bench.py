@@ -165,8 +165,6 @@ def kernel_class(name):
         return "decode_attn"
     if "attn_prefill" in name:
         return "prefill_attn"
-    if "mega_decode" in name:
-        return "mega_decode"
     return "other"
 
 
@@ -300,7 +298,7 @@ def roofline(stats, partition=None):
     classes = []
     for worker in ("cpi", "ppi"):
         for name, k in stats[worker].items():
-            if name in ("forward", "other", "mega_decode") or not k["launches"] or k["ms"] <= 0:
+            if name in ("forward", "other") or not k["launches"] or k["ms"] <= 0:
                 continue
             bound = "hbm" if name in ("gemm_stream", "decode_attn") else "tensor"
             ms_avg = k["ms"] / k["launches"]

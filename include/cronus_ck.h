@@ -115,25 +115,19 @@ int ck_qkv_rope_append(float* qkv, const void* bias, void* q_out, void* kv_pool,
                        const int* row_pos, const float* cos_tab, const float* sin_tab, int M, int nq, int nkv,
                        int layer, int n_layers, int zero_after, void* stream);
 
-/* Decode attention over the paged pool for S single-token sequences (split-KV).
+/* Decode attention over the paged pool for S single-token sequences, production path:
  * seq_row[S] (row of q/out), seq_len[S] (keys), seq_bt[S] (offset into bt),
- * seq_item0[S+1] (first work item of each sequence). work[n_work] = seq << 16 | split;
- * a work item covers up to `blocks_per_split` 16-token blocks. ws: fp32 partials,
+ * seq_item0[S+1] (first work item of each sequence). ws: fp32 partials,
  * n_work * nq * 130 floats. tickets: n_seq * nkv ints, zero before the first call
- * (the kernel leaves them zero). Output bf16 rows [*, nq*128]. One launch. */
-int ck_attn_decode(const void* q, const void* kv_pool, const int* bt, const int* seq_row, const int* seq_len,
-                   const int* seq_bt, const int* seq_item0, const int* work, int n_work, int n_seq,
-                   int blocks_per_split, float* ws, int* tickets, void* out, int nq, int nkv, int layer,
-                   int n_layers, float scale, void* stream);
-
-/* Same op, production path: K/V rings filled by TMA (2-D map over the pool viewed as
- * [pool_blocks * n_layers * 2 * nkv * 16 rows][128]) and each work item served by a
+ * (the kernel leaves them zero). Output bf16 rows [*, nq*128]. One launch.
+ * K/V rings are filled by TMA (2-D map over the pool viewed as
+ * [pool_blocks * n_layers * 2 * nkv * 16 rows][128]) and each work item is served by a
  * thread-block CLUSTER of `cluster` CTAs (1..16) that split the item's blocks and merge
  * through distributed shared memory. work[i] = seq << 16 | part; a sequence's parts
  * (seq_item0) are evened out to ceil(nblocks / nparts) blocks; parts of one sequence
- * merge through ws / tickets as in ck_attn_decode. Partially filled last blocks are
- * read whole and masked, so never-written slots must hold finite values (the engine
- * zero-fills its pools). pool rows must be < 2^31. */
+ * merge through ws / tickets (the last CTA of a (sequence, kv head) folds them). Partially
+ * filled last blocks are read whole and masked, so never-written slots must hold finite
+ * values (the engine zero-fills its pools). pool rows must be < 2^31. */
 typedef struct {
     const float* qkv;     /* fp32 QKV rows [*, (nq + 2 nkv) * 128] (bias included), row = seq_row */
     const float* cos_tab; /* RoPE tables [max_pos][64] (ck_rope_table) */
@@ -147,22 +141,13 @@ int ck_attn_decode_tma(const void* q, const void* kv_pool, long long pool_blocks
                        int n_seq, int cluster, float* ws, int* tickets, void* out, int nq, int nkv, int layer,
                        int n_layers, float scale, const ck_decode_rope* rope, void* stream);
 
-/* Prefill/chunk attention, causal: query rows [q_row0, q_row0+q_len) sit at
- * positions [pos0, pos0+q_len); keys [0, pos0+q_len) from the paged pool via bt. */
-int ck_attn_prefill(const void* q, const void* kv_pool, const int* bt, int q_row0, int q_len, int pos0, void* out,
-                    int nq, int nkv, int layer, int n_layers, float scale, void* stream);
-
-/* Same op on the 5th-gen tensor cores (tcgen05 + TMEM + TMA): 128 query rows x 1 head
- * per CTA. q_rows_total: rows of the q buffer (TMA bound); pool_blocks: blocks in the
- * pool. Stale slots of a sequence's last block are read (and masked): the pool must hold
- * finite values (the engine zero-fills it at allocation). */
-int ck_attn_prefill_tc(const void* q, int q_rows_total, const void* kv_pool, long long pool_blocks, const int* bt,
-                       int q_row0, int q_len, int pos0, void* out, int nq, int nkv, int layer, int n_layers,
-                       float scale, void* stream);
-
-/* Same op, production path: two 128-row query tiles per CTA with one softmax warpgroup
- * each (ping-pong on the tensor pipe) and P kept in TMEM as the A operand of the PV
- * MMA. Same arguments and stale-slot requirement as ck_attn_prefill_tc. */
+/* Prefill/chunk attention, causal, on the 5th-gen tensor cores (tcgen05 + TMEM + TMA):
+ * query rows [q_row0, q_row0+q_len) of q (bf16 [q_rows_total, nq*128]) sit at positions
+ * [pos0, pos0+q_len) and attend to keys [0, pos0+q_len) of the paged pool via bt.
+ * Two 128-row query tiles per CTA with one softmax warpgroup each (ping-pong on the tensor
+ * pipe) and P kept in TMEM as the A operand of the PV MMA. pool_blocks: blocks in the pool
+ * (TMA bound). Stale slots of a sequence's last block are read (and masked): the pool must
+ * hold finite values (the engine zero-fills it at allocation). */
 int ck_attn_prefill_pp(const void* q, int q_rows_total, const void* kv_pool, long long pool_blocks, const int* bt,
                        int q_row0, int q_len, int pos0, void* out, int nq, int nkv, int layer, int n_layers,
                        float scale, void* stream);
@@ -200,33 +185,6 @@ int ck_spin(int us, void* stream);
  * 128x64 bf16 boxes over a [rows][4096] matrix (the GEMM's weight pattern), 2 =
  * cp.async.bulk 16 KiB chunks. Time it with events on `stream`. */
 int ck_bw_probe(const void* buf, long long bytes, int mode, int ctas, void* stream);
-
-/* Persistent decode forward: one cooperative launch runs a whole decode-only pass
- * (embed -> L layers -> final norm -> LM head -> greedy argmax) for M <= 64 rows.
- * A plan holds the weight tensor maps (built once) and the activation buffers the
- * per-M activation maps point at. Activation / accumulator buffers follow the
- * separate-kernel path's conventions: qkv and gu are red.add accumulators that must be
- * zero on entry and are left zero. */
-typedef struct ck_mega_args {
-    int M, H, NQKV, NQ, F, V, nq, nkv, grid;
-    float eps, scale;
-    float* x; void* h; float* qkv; void* q; void* attn; float* gu; void* act; void* hs; float* logits;
-    const void* embed; const void* final_norm; const float* cos_tab; const float* sin_tab;
-    const int* row_rid; const int* row_pos; const int* bt;
-    const int* d_row; const int* d_len; const int* d_bt; const int* d_item0; const int* d_work;
-    int n_work, blocks_per_split;
-    float* attn_ws; int* attn_tickets; void* pool;
-    const long long* s_out; int* last_tok; int* out_tok; float* arg_ws; int* arg_tickets;
-} ck_mega_args;
-
-int ck_mega_plan_create(void** plan, int L, const void* const* w_qkv, const void* const* w_o,
-                        const void* const* w_gu, const void* const* w_d, const void* lm_head,
-                        const void* const* attn_norm, const void* const* ffn_norm, const void* const* bqkv, int H,
-                        int NQKV, int NQ, int F, int V, const void* h_buf, const void* attn_buf,
-                        const void* act_buf, const void* hs_buf);
-void ck_mega_plan_destroy(void* plan);
-int ck_mega_max_rows(void);
-int ck_mega_decode(void* plan, const ck_mega_args* args, void* stream);
 
 #ifdef __cplusplus
 }

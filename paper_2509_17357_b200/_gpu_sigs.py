@@ -18,10 +18,7 @@ CK = {
     "ck_embed": [V, V, V, V, V, V, V, V, I, I, V],
     "ck_rmsnorm": [V, V, V, V, I, I, F, V, I, V],
     "ck_qkv_rope_append": [V, V, V, V, V, V, V, V, V, I, I, I, I, I, I, V],
-    "ck_attn_decode": [V, V, V, V, V, V, V, V, I, I, I, V, V, V, I, I, I, I, F, V],
     "ck_attn_decode_tma": [V, V, LL, V, V, V, V, V, V, I, I, I, V, V, V, I, I, I, I, F, V, V],
-    "ck_attn_prefill": [V, V, V, I, I, I, V, I, I, I, I, F, V],
-    "ck_attn_prefill_tc": [V, I, V, LL, V, I, I, I, V, I, I, I, I, F, V],
     "ck_attn_prefill_pp": [V, I, V, LL, V, I, I, I, V, I, I, I, I, F, V],
     "ck_silu_mul": [V, V, I, I, I, V],
     "ck_argmax_emit": [V, I, I, V, V, V, V, V, V, I, V],

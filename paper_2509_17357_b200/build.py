@@ -99,13 +99,8 @@ def build(jobs: int | None = None, verbose: bool = False) -> str:
                     print("compiled", os.path.relpath(s, ROOT))
     objs = [obj_for(s) for s in cpp + cu]
     if todo or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        dlink = os.path.join(BUILD, "dlink.o")
-        cu_objs = [obj_for(s) for s in cu]
-        link_objs = list(objs)
-        if cu_objs:
-            # device-link step (static cudart, relocatable device code not used)
-            pass
-        cmd = [CXX, "-shared", "-o", LIB, *link_objs, "-L" + os.path.join(CUDA, "lib64"),
+        # no device-link step: relocatable device code is not used (static cudart)
+        cmd = [CXX, "-shared", "-o", LIB, *objs, "-L" + os.path.join(CUDA, "lib64"),
                "-lcudart_static", "-lrt", "-lpthread", "-ldl", "-Wl,--no-undefined"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

@@ -48,10 +48,6 @@ struct EngineOptions {
     long long cpi_pool_blocks = 0, ppi_pool_blocks = 0;
     uint64_t seed = 1234, prompt_seed = 99;
     bool profile = false;
-    // decode-only CPI passes: "layered" (one kernel per op, PDL-chained) or "persistent"
-    // (ck_mega_decode: one cooperative launch per pass; measured slower on B200, kept
-    // selectable for experiments — see DESIGN.md)
-    bool persistent_decode = false;
     // co-located pair with a green-context split: CPI iterations launched while the PPI
     // has nothing in flight run on all SMs (the PPI's share is idle); PPI work issued
     // behind such an iteration waits for it, so the two never contend for SMs
@@ -94,11 +90,7 @@ EngineOptions parse_engine_options(const std::string& text) {
         else if (k == "profile") o.profile = v == "1" || v == "true";
         else if (k == "sm_lending") o.sm_lending = v == "1" || v == "true";
         else if (k == "separate") o.separate = v == "1" || v == "true";
-        else if (k == "decode_forward") {
-            if (v != "layered" && v != "persistent")
-                throw std::invalid_argument("engine options: decode_forward = layered | persistent");
-            o.persistent_decode = v == "persistent";
-        } else throw std::invalid_argument("engine options: unknown key " + k);
+        else throw std::invalid_argument("engine options: unknown key " + k);
     }
     if (o.ppi_chunk < 16 || o.ppi_chunk % 16) throw std::invalid_argument("engine options: ppi_chunk % 16 != 0");
     return o;
@@ -331,7 +323,6 @@ struct GpuEngine::Impl {
             check_cuda(cudaSetDevice(opt.cpi_device), "cudaSetDevice");
             cpi = std::make_unique<gpu::Worker>(*w_cpi, cpi_rows, cpi_samples,
                                                 static_cast<int>(pool_cpi->blocks) + cpi_rows, s_cpi, cpi_ctas);
-            cpi->set_persistent_decode(opt.persistent_decode);
         }
         if (!ppi || ppi_rows < rows(0) || ppi_samples < samples(0)) {
             ppi.reset();
@@ -634,8 +625,7 @@ class PairExecutor : public sched::Executor {
         }
         for (int rid : w.finishers) need(rid, nullptr);  // zero rows: its KV is placed when it decodes
         if (!batch.d_len.empty())
-            batch.plan_decode(E.spec.n_kv_heads, gpu::decode_slots(E.spec.n_kv_heads, static_cast<int>(batch.d_len.size()), lend ? E.sms : hi ? E.cpi_sm_count() : E.ppi_sm_count()),
-                              !E.opt.persistent_decode && gpu::decode_cluster_kernel());
+            batch.plan_decode(E.spec.n_kv_heads, gpu::decode_slots(E.spec.n_kv_heads, static_cast<int>(batch.d_len.size()), lend ? E.sms : hi ? E.cpi_sm_count() : E.ppi_sm_count()));
         if (E.opt.wall && hi) {  // device-side start of this iteration (busy time = end - start)
             iter_start = take_event(true);
             check_cuda(cudaEventRecord(iter_start, cur), "event record");
@@ -792,7 +782,6 @@ class PairExecutor : public sched::Executor {
         ks("gemm_stream", E.cpi->stat_gemm_stream);
         ks("gemm_tc", E.cpi->stat_gemm_tc);
         ks("other", E.cpi->stat_other);
-        ks("mega_decode", E.cpi->stat_mega);
         ks("forward", E.cpi->stat_forward, false);
         s << "}, \"ppi\": {";
         ks("prefill_attn", E.ppi->stat_prefill_attn);
@@ -927,8 +916,7 @@ double GpuEngine::time_pass(const ClusterConfig& cfg, int worker, int n_dec, int
         batch.add_prefill(0, chunk_pos0, chunk_len, tables.back(), true, 0);
     }
     if (n_dec > 0)
-        batch.plan_decode(E.spec.n_kv_heads, gpu::decode_slots(E.spec.n_kv_heads, static_cast<int>(batch.d_len.size()), worker == 0 ? (E.ppi_ctas ? E.ppi_ctas : E.sms) : E.cpi_sm_count()),
-                          !E.opt.persistent_decode && gpu::decode_cluster_kernel());
+        batch.plan_decode(E.spec.n_kv_heads, gpu::decode_slots(E.spec.n_kv_heads, static_cast<int>(batch.d_len.size()), worker == 0 ? (E.ppi_ctas ? E.ppi_ctas : E.sms) : E.cpi_sm_count()));
     cudaEvent_t a, b;
     check_cuda(cudaEventCreate(&a), "event");
     check_cuda(cudaEventCreate(&b), "event");
@@ -967,7 +955,6 @@ double GpuEngine::time_pass(const ClusterConfig& cfg, int worker, int n_dec, int
         pr("gemm_stream", W.stat_gemm_stream);
         pr("gemm_tc", W.stat_gemm_tc);
         pr("other", W.stat_other);
-        pr("mega", W.stat_mega);
         pr("forward", W.stat_forward);
         std::fprintf(stderr, "\n");
     }

@@ -189,39 +189,7 @@ void Batch::add_prefill(int rid, long long pos0, long long len, const std::vecto
     }
 }
 
-// Pick the split size so the decode grid holds ~target_ctas CTAs.
-void Batch::plan_decode_splits(int n_kv_heads, int slots) {
-    // Split size = total block-heads / (waves x resident CTAs), waves = 1.5 by default
-    // (CRONUS_DECODE_WAVES): long enough splits keep each warp's cp.async ring
-    // streaming, enough of them to balance across the resident CTAs.
-    static const double waves = [] {
-        const char* e = std::getenv("CRONUS_DECODE_WAVES");
-        return e ? std::atof(e) : 1.5;
-    }();
-    long long total = 0;
-    for (int len : d_len) total += (len + 15) / 16;
-    int bps = static_cast<int>(std::ceil(total * n_kv_heads / std::max(1.0, waves * slots)));
-    bps = std::clamp(bps, 16, 1024);
-    while (true) {  // keep the work list bounded (workspace sizing)
-        long long items = 0;
-        for (int len : d_len) items += ((len + 15) / 16 + bps - 1) / bps;
-        if (items <= 4096) break;
-        bps *= 2;
-    }
-    blocks_per_split = bps;
-    decode_cluster = 0;
-    d_item0.clear();
-    d_work.clear();
-    for (size_t s = 0; s < d_len.size(); ++s) {
-        d_item0.push_back(static_cast<int>(d_work.size()));
-        const int nblk = (d_len[s] + 15) / 16;
-        const int ns = (nblk + bps - 1) / bps;
-        for (int i = 0; i < ns; ++i) d_work.push_back(static_cast<int>(s << 16) | i);
-    }
-    d_item0.push_back(static_cast<int>(d_work.size()));
-}
-
-void Batch::plan_decode_clusters(int n_kv_heads, int slots) {
+void Batch::plan_decode(int n_kv_heads, int slots) {
     // One wave of `slots` resident CTAs: every (sequence, kv head) pair gets a cluster of
     // C CTAs (C = power of two <= 16, as large as the wave allows while each CTA keeps
     // >= 4 blocks, one per warp); a sequence more than ~2x longer than its fair share
@@ -245,16 +213,6 @@ void Batch::plan_decode_clusters(int n_kv_heads, int slots) {
     }
     d_item0.push_back(static_cast<int>(d_work.size()));
     blocks_per_split = static_cast<int>(cap);
-}
-
-// Prefill / chunk attention: ping-pong kernel (default) or one query tile per CTA
-// (CRONUS_PREFILL_V1=1).
-bool prefill_attn_v1() {
-    static const bool on = [] {
-        const char* e = std::getenv("CRONUS_PREFILL_V1");
-        return e && e[0] == '1';
-    }();
-    return on;
 }
 
 // Tensor-regime gate_up: hybrid whole-tile / stream-K-tail SiLU GEMM (CRONUS_SILU_HYBRID=0: whole tiles only).
@@ -353,14 +311,6 @@ int decode_slots(int n_kv_heads, int n_seq, int sms) {
     return (static_cast<long long>(n_seq) * n_kv_heads >= 64 ? 3 : 2) * sms;
 }
 
-bool decode_cluster_kernel() {
-    static const bool on = [] {
-        const char* e = std::getenv("CRONUS_DECODE_CPASYNC");
-        return !(e && e[0] == '1');
-    }();
-    return on;
-}
-
 // ------------------------------------------------------------------ Worker
 Worker::Worker(const Weights& w, int max_rows, int max_sample, int max_blocks_per_pass, cudaStream_t stream,
                int max_ctas)
@@ -403,7 +353,6 @@ Worker::Worker(const Weights& w, int max_rows, int max_sample, int max_blocks_pe
 Worker::~Worker() {
     cudaSetDevice(w_.device());
     reset_graphs();
-    if (mega_) ck_mega_plan_destroy(mega_);
     for (void* p : {static_cast<void*>(x_), h_, static_cast<void*>(qkv_), q_, attn_, static_cast<void*>(gu_), act_, hs_,
                     static_cast<void*>(logits_), static_cast<void*>(attn_ws_), static_cast<void*>(meta_dev_),
                     static_cast<void*>(attn_tickets_), static_cast<void*>(arg_ws_), static_cast<void*>(arg_tickets_),
@@ -561,15 +510,6 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
 
     const int H = m.hidden, Q = m.qkv_n(), NQ = m.q_n(), F = m.ffn;
     const bool small = M <= 128;  // weight-streaming regime
-    if (b.p_len == 0 && n_dec == M && R == M && persistent_ && mega_ok_ && M <= ck_mega_max_rows() &&
-        b.decode_cluster == 0) {
-        const PassMeta pm{row_rid,       row_pos,          bt,         D(o_d_row), D(o_d_len), D(o_d_bt), D(o_d_item0),
-                          D(o_d_work), reinterpret_cast<const long long*>(D(o_s_out))};
-        if (forward_mega(b, pool, pm, last_tok, out_tok)) {
-            done(pass0, &stat_forward, 0, 0);
-            return;
-        }
-    }
     const float scale = 1.0f / std::sqrt(static_cast<float>(m.head_dim));
     long long dec_keys = 0;
     for (int len : b.d_len) dec_keys += len;
@@ -661,13 +601,7 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         }
         if (n_dec > 0) {
             mark(a);
-            if (b.decode_cluster == 0)  // split plan (plan_decode_splits): cp.async kernel
-                check_ck(ck_attn_decode(q_, pool.base, bt, D(o_d_row), D(o_d_len), D(o_d_bt), D(o_d_item0),
-                                        D(o_d_work), n_work, n_dec, b.blocks_per_split, attn_ws_, attn_tickets_, attn_,
-                                        m.n_heads, m.n_kv_heads, l, m.layers, scale, stream_),
-                         "attn_decode");
-            else
-                check_ck(ck_attn_decode_tma(q_, pool.base, pool.blocks, bt, D(o_d_row), D(o_d_len), D(o_d_bt),
+            check_ck(ck_attn_decode_tma(q_, pool.base, pool.blocks, bt, D(o_d_row), D(o_d_len), D(o_d_bt),
                                             D(o_d_item0), D(o_d_work), n_work, n_dec, b.decode_cluster, attn_ws_,
                                             attn_tickets_, attn_, m.n_heads, m.n_kv_heads, l, m.layers, scale,
                                             fused_rope ? &rope : nullptr, stream_),
@@ -677,7 +611,7 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         }
         if (b.p_len > 0) {
             mark(a);
-            check_ck((prefill_attn_v1() ? ck_attn_prefill_tc : ck_attn_prefill_pp)(
+            check_ck(ck_attn_prefill_pp(
                          q_, max_rows_, pool.base, pool.blocks, bt + b.p_bt, b.p_row0, b.p_len, b.p_pos0, attn_,
                          m.n_heads, m.n_kv_heads, l, m.layers, scale, stream_),
                      "attn_prefill");
@@ -745,7 +679,7 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         done(a, &stat_other, 0, 0);
         // LM head: a 1 GB weight stream for a handful of rows -> stream-K red.add into the
         // logits the previous argmax cleared (balanced over the grid); larger R: tile stores
-        if (R <= 128 && !logits_dirty_)
+        if (R <= 128)
             gemm(w_.lm_head, hs_, logits_, nullptr, R, m.vocab, H, CK_EPI_RED_F32, 0);
         else
             gemm(w_.lm_head, hs_, logits_, nullptr, R, m.vocab, H, CK_EPI_F32, 1);
@@ -753,7 +687,6 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         check_ck(ck_argmax_emit(logits_, R, m.vocab, D(o_s_rid), reinterpret_cast<const long long*>(D(o_s_out)),
                                 last_tok, out_tok, arg_ws_, arg_tickets_, 1, stream_),
                  "argmax");
-        logits_dirty_ = false;
         ++launches;
         done(a, &stat_other, 0, 0);
     }
@@ -763,7 +696,7 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
     // (rows, attention work items, cluster size, stream): the graph_min_seen()-th time a shape
     // is seen the chain is captured into a CUDA graph (PDL edges kept) and replayed from then on — a
     // dependent kernel boundary costs ~1.3-1.5 us in a graph vs ~1.9-2.7 us on a stream.
-    const bool graphable = use_graphs() && !profile_ && fused_rope && !logits_dirty_;
+    const bool graphable = use_graphs() && !profile_ && fused_rope;
     if (graphable) {
         char key[256];
         std::snprintf(key, sizeof key, "%d/%d/%d/%d/%d/%p/%d/%p/%d/%p/%p/%p/%p/%p", M, R, n_dec, n_work,
@@ -815,61 +748,6 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
     }
     issue();
     done(pass0, &stat_forward, 0, 0);
-}
-
-bool Worker::forward_mega(const Batch& b, const KvPool& pool, const PassMeta& pm, int* last_tok, int* out_tok) {
-    const ModelSpec& m = m_;
-    const int M = b.rows();
-    for (int i = 0; i < M; ++i)  // decode rows in order, each sampled into its own slot
-        if (b.d_row[i] != i || b.s_row[i] != i) return false;
-    if (!mega_) {
-        std::vector<const void*> wq, wo, wgu, wd, an, fn, bq;
-        bool bias = false;
-        for (const LayerWeights& L : w_.layer) {
-            wq.push_back(L.wqkv), wo.push_back(L.wo), wgu.push_back(L.wgu), wd.push_back(L.wd);
-            an.push_back(L.attn_norm), fn.push_back(L.ffn_norm), bq.push_back(L.bqkv);
-            bias = bias || L.bqkv;
-        }
-        check_ck(ck_mega_plan_create(&mega_, m.layers, wq.data(), wo.data(), wgu.data(), wd.data(), w_.lm_head,
-                                     an.data(), fn.data(), bias ? bq.data() : nullptr, m.hidden, m.qkv_n(), m.q_n(),
-                                     m.ffn, m.vocab, h_, attn_, act_, hs_),
-                 "mega plan");
-    }
-    if (qkv_dirty_rows_ > 0)
-        check_cuda(cudaMemsetAsync(qkv_, 0, static_cast<size_t>(qkv_dirty_rows_) * m.qkv_n() * 4, stream_), "memset qkv");
-    if (gu_dirty_rows_ > 0)
-        check_cuda(cudaMemsetAsync(gu_, 0, static_cast<size_t>(gu_dirty_rows_) * 2 * m.ffn * 4, stream_), "memset gu");
-    qkv_dirty_rows_ = gu_dirty_rows_ = 0;
-    ck_mega_args a{};
-    a.M = M, a.H = m.hidden, a.NQKV = m.qkv_n(), a.NQ = m.q_n(), a.F = m.ffn, a.V = m.vocab;
-    a.nq = m.n_heads, a.nkv = m.n_kv_heads, a.grid = max_ctas_ > 0 ? max_ctas_ : ck_device_sms();
-    a.eps = m.rms_eps, a.scale = 1.0f / std::sqrt(static_cast<float>(m.head_dim));
-    a.x = x_, a.h = h_, a.qkv = qkv_, a.q = q_, a.attn = attn_, a.gu = gu_, a.act = act_, a.hs = hs_, a.logits = logits_;
-    logits_dirty_ = true;  // its LM head stores, its argmax does not clear
-    a.embed = w_.embed, a.final_norm = w_.final_norm, a.cos_tab = w_.cos_tab, a.sin_tab = w_.sin_tab;
-    a.row_rid = pm.row_rid, a.row_pos = pm.row_pos, a.bt = pm.bt, a.d_row = pm.d_row, a.d_len = pm.d_len;
-    a.d_bt = pm.d_bt, a.d_item0 = pm.d_item0, a.d_work = pm.d_work;
-    a.n_work = static_cast<int>(b.d_work.size()), a.blocks_per_split = b.blocks_per_split;
-    a.attn_ws = attn_ws_, a.attn_tickets = attn_tickets_, a.pool = pool.base;
-    a.s_out = pm.s_out, a.last_tok = last_tok, a.out_tok = out_tok, a.arg_ws = arg_ws_, a.arg_tickets = arg_tickets_;
-    cudaEvent_t ev0 = nullptr;
-    mark(ev0);
-    const int rc = ck_mega_decode(mega_, &a, stream_);
-    if (rc == static_cast<int>(cudaErrorCooperativeLaunchTooLarge)) {
-        (void)cudaGetLastError();
-        mega_ok_ = false;
-        return false;
-    }
-    check_ck(rc, "mega_decode");
-    ++launches;
-    long long keys = 0;
-    for (int len : b.d_len) keys += len;
-    const double wbytes = 2.0 * (static_cast<double>(m.layers) *
-                                     (static_cast<double>(m.qkv_n()) * m.hidden + static_cast<double>(m.hidden) * m.q_n() +
-                                      3.0 * m.hidden * m.ffn) +
-                                 static_cast<double>(m.vocab) * m.hidden);
-    done(ev0, &stat_mega, wbytes + keys * m.layers * 4.0 * m.n_kv_heads * m.head_dim, 0);
-    return true;
 }
 
 }  // namespace gpu

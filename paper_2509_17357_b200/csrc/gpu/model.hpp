@@ -104,8 +104,7 @@ struct Batch {
     // decode sequences
     std::vector<int> d_row, d_len, d_bt, d_item0, d_work;
     int blocks_per_split = 16;
-    // 0: split plan (plan_decode_splits) for ck_attn_decode / the persistent pass;
-    // C >= 1: cluster plan (plan_decode_clusters) for ck_attn_decode_tma
+    // cluster size C >= 1 of the decode plan (plan_decode) for ck_attn_decode_tma
     int decode_cluster = 0;
     // one prefill sequence: rows [p_row0, p_row0 + p_len) at positions [p_pos0, ...)
     int p_row0 = 0, p_len = 0, p_pos0 = 0, p_bt = 0;
@@ -122,12 +121,7 @@ struct Batch {
     void add_decode(int rid, long long ctx, const std::vector<int32_t>& blocks, long long out_index);
     void add_prefill(int rid, long long pos0, long long len, const std::vector<int32_t>& blocks, bool sample,
                      long long out_index);
-    void plan_decode_splits(int n_kv_heads, int target_ctas);
-    void plan_decode_clusters(int n_kv_heads, int slots);
-    void plan_decode(int n_kv_heads, int slots, bool clusters) {
-        if (clusters) plan_decode_clusters(n_kv_heads, slots);
-        else plan_decode_splits(n_kv_heads, slots);
-    }
+    void plan_decode(int n_kv_heads, int slots);
 };
 
 // Kernel-time accounting (CUDA events around selected launches, on the launching stream).
@@ -156,7 +150,6 @@ class Worker {
     int max_rows() const { return max_rows_; }
     cudaStream_t stream() const { return stream_; }
     void set_profiling(bool on) { profile_ = on; }
-    void set_persistent_decode(bool on) { persistent_ = on; }
     // Switch the stream / persistent-grid cap later passes launch on (SM lending). The
     // caller orders the streams.
     void set_launch(cudaStream_t s, int max_ctas) {
@@ -168,11 +161,9 @@ class Worker {
     void reset_graphs();
     void reset_stats() {
         stat_decode_attn = stat_prefill_attn = stat_gemm_stream = stat_gemm_tc = stat_other = stat_forward = {};
-        stat_mega = {};
     }
     // gemm_stream: M <= 128 (weight-streaming, HBM bound); gemm_tc: M > 128 (tensor bound)
     KernelStat stat_decode_attn, stat_prefill_attn, stat_gemm_stream, stat_gemm_tc, stat_other, stat_forward;
-    KernelStat stat_mega;  // persistent decode forward (one launch per decode-only pass)
     long long launches = 0;  // our kernels launched (always counted)
 
   private:
@@ -198,7 +189,6 @@ class Worker {
     // tensor-regime pass, which stores instead of red.adding); the weight-streaming
     // regime needs them zero and its consumers re-zero what they read.
     int qkv_dirty_rows_ = 0, gu_dirty_rows_ = 0;
-    bool logits_dirty_ = false;  // the persistent pass left logits uncleared
     int* tile_tickets_ = nullptr;  // fused-epilogue tile tickets (self-resetting)
     int* norm_tickets_ = nullptr;  // fused-RMSNorm m-tile tickets (self-resetting)
     float* arg_ws_ = nullptr;      // argmax slice winners [max_sample * 64]
@@ -222,16 +212,6 @@ class Worker {
     cudaEvent_t ev();
     void mark(cudaEvent_t& a);
     void done(cudaEvent_t a, KernelStat* into, double bytes, double flops);
-    // persistent decode forward (ck_mega_decode): plan built on first use; disabled for
-    // good if the cooperative launch is refused (e.g. grid larger than co-residency)
-    void* mega_ = nullptr;
-    bool persistent_ = false;
-    bool mega_ok_ = true;
-    struct PassMeta {
-        const int *row_rid, *row_pos, *bt, *d_row, *d_len, *d_bt, *d_item0, *d_work;
-        const long long* s_out;
-    };
-    bool forward_mega(const Batch& b, const KvPool& pool, const PassMeta& pm, int* last_tok, int* out_tok);
     // decode-pass CUDA graphs, keyed by the pass shape and the pointers its kernels take
     struct Tally {
         KernelStat* into;
@@ -250,9 +230,6 @@ class Worker {
               const ck_gemm_fuse* fuse = nullptr);
 };
 
-// Decode attention kernel family: TMA + cluster (default) or the cp.async split kernel
-// (CRONUS_DECODE_CPASYNC=1).
-bool decode_cluster_kernel();
 // Resident decode-attention CTAs per SM the cluster planner assumes (CRONUS_DEC_SLOTS_PER_SM; default 0 = auto).
 int decode_slots_per_sm();
 // Resident-CTA budget handed to the decode planner for n_seq sequences on `sms` SMs.

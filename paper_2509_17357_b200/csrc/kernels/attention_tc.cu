@@ -39,14 +39,6 @@ constexpr int kTileBytes = 2 * kHalf;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
-// smem map (offsets from a 1024-aligned base)
-constexpr int kOffQ = 0;
-constexpr int kOffK = kOffQ + kTileBytes;          // 2 stages
-constexpr int kOffV = kOffK + 2 * kTileBytes;      // 2 stages
-constexpr int kOffP = kOffV + 2 * kTileBytes;      // 2 buffers (softmax j+1 overlaps PV j)
-constexpr int kOffBar = kOffP + 2 * kTileBytes;
-constexpr int kSmemBytes = kOffBar + 256 + 1024;
-
 struct AttnParams {
     int q_row0, q_len, pos0;
     int nq, nkv, layer, n_layers;
@@ -106,271 +98,6 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-__global__ void __launch_bounds__(192, 1)
-    attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
-                           AttnParams p) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + kOffBar);
-    uint64_t* q_full = bar + 0;
-    uint64_t* k_full = bar + 1;    // [2] K tile landed
-    uint64_t* k_empty = bar + 3;   // [2] S MMA that read it retired
-    uint64_t* v_full = bar + 5;    // [2]
-    uint64_t* v_empty = bar + 7;   // [2] PV MMA that read it retired
-    uint64_t* s_full = bar + 9;    // [2]
-    uint64_t* s_empty = bar + 11;  // [2]
-    uint64_t* p_full = bar + 13;   // [2]
-    uint64_t* pv_done = bar + 15;  // [2] PV of the P buffer retired
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
-
-    const int warp = warp_id(), lane = lane_id();
-    // heaviest (latest, most keys under the causal mask) query tiles are scheduled first
-    const int qt = gridDim.x - 1 - blockIdx.x, h = blockIdx.y;
-    const int kvh = h / (p.nq / p.nkv);
-    const int r_begin = qt * kQ;
-    const int r_end = min(p.q_len, r_begin + kQ);
-    const int n_keys = p.pos0 + r_end;  // causal extent of this tile's last row
-    const int n_kt = (n_keys + kKT - 1) / kKT;
-
-    if (warp == 1) {
-        tmem_alloc(tmem_slot, 512);  // S[2] at cols 0 / 128, O at 256
-        tmem_relinquish();
-    } else if (warp == 0 && lane == 0) {
-        tma_prefetch_desc(&tmQ);
-        tma_prefetch_desc(&tmKV);
-        mbar_init(q_full, 1);
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&k_full[i], 1);
-            mbar_init(&k_empty[i], 1);
-            mbar_init(&v_full[i], 1);
-            mbar_init(&v_empty[i], 1);
-            mbar_init(&s_full[i], 1);
-            mbar_init(&s_empty[i], 4);
-            mbar_init(&p_full[i], 4);
-            mbar_init(&pv_done[i], 1);
-        }
-        fence_mbar_init();
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    pdl_launch();
-    pdl_wait();
-
-    if (warp == 0) {
-        // ------------------------------------------------------------ TMA producer
-        if (lane == 0) {
-            const uint64_t keep = policy_evict_last();
-            mbar_arrive_expect_tx(q_full, kTileBytes);
-            const int qcol = h * 128;
-            const int qrow = p.q_row0 + r_begin;
-            tma_load_2d(sm + kOffQ, &tmQ, q_full, qcol, qrow);
-            tma_load_2d(sm + kOffQ + kHalf, &tmQ, q_full, qcol + 64, qrow);
-            const int n_tab = (n_keys + 15) / 16;
-            // K and V have separate rings: K(j) is free once S(j) retired (long before
-            // PV(j)), so tile j+2's keys stream in while the softmax of j still runs
-            auto row_of = [&](int j, int b) {
-                const int tb = j * (kKT / 16) + b;
-                const int blk = p.table[tb < n_tab ? tb : 0];  // past the end: any finite block (masked)
-                return ((blk * p.n_layers + p.layer) * 2 + 0) * p.nkv * 16 + kvh * 16;
-            };
-            for (int j = 0; j < n_kt; ++j) {
-                const int s = j & 1;
-                mbar_wait(&k_empty[s], ((j >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&k_full[s], kTileBytes);
-                uint8_t* K = sm + kOffK + s * kTileBytes;
-                for (int b = 0; b < kKT / 16; ++b) {
-                    const int row_k = row_of(j, b);
-                    tma_load_2d_hint(K + b * 2048, &tmKV, &k_full[s], 0, row_k, keep);
-                    tma_load_2d_hint(K + kHalf + b * 2048, &tmKV, &k_full[s], 64, row_k, keep);
-                }
-                mbar_wait(&v_empty[s], ((j >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&v_full[s], kTileBytes);
-                uint8_t* V = sm + kOffV + s * kTileBytes;
-                for (int b = 0; b < kKT / 16; ++b) {
-                    const int row_v = row_of(j, b) + p.nkv * 16;
-                    tma_load_2d_hint(V + b * 2048, &tmKV, &v_full[s], 0, row_v, keep);
-                    tma_load_2d_hint(V + kHalf + b * 2048, &tmKV, &v_full[s], 64, row_v, keep);
-                }
-            }
-        }
-    } else if (warp == 1) {
-        // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t id_s = idesc_attn(false), id_o = idesc_attn(true);
-            const uint32_t q0 = smem_u32(sm + kOffQ);
-            mbar_wait(q_full, 0);
-            auto issue_s = [&](int j) {
-                const int s = j & 1;
-                mbar_wait(&k_full[s], (j >> 1) & 1);
-                mbar_wait(&s_empty[s], ((j >> 1) & 1) ^ 1);
-                tc_fence_after();
-                const uint32_t k0 = smem_u32(sm + kOffK + s * kTileBytes);
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {  // 8 x K=16 over the 128 head dims
-                    const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
-                    tc_mma_bf16(tmem + s * 128, sdesc_sw128(q0 + off), sdesc_sw128(k0 + off), id_s, kk > 0);
-                }
-                tc_commit(&s_full[s]);
-                tc_commit(&k_empty[s]);  // K stage reusable
-            };
-            auto issue_pv = [&](int j) {
-                const int s = j & 1;
-                mbar_wait(&p_full[s], (j >> 1) & 1);
-                mbar_wait(&v_full[s], (j >> 1) & 1);
-                tc_fence_after();
-                const uint32_t v0 = smem_u32(sm + kOffV + s * kTileBytes);
-                const uint32_t pbase = smem_u32(sm + kOffP + s * kTileBytes);
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {  // 8 x K=16 over the 128 keys
-                    const uint32_t aoff = (kk >> 2) * kHalf + (kk & 3) * 32;
-                    tc_mma_bf16(tmem + 256, sdesc_sw128(pbase + aoff), sdesc_mn_sw128(v0 + kk * 2048), id_o,
-                                (j > 0 || kk > 0) ? 1u : 0u);
-                }
-                tc_commit(&v_empty[s]);   // V stage reusable
-                tc_commit(&pv_done[s]);   // P buffer s reusable / O stable
-            };
-            issue_s(0);
-            for (int j = 0; j < n_kt; ++j) {
-                if (j + 1 < n_kt) issue_s(j + 1);
-                issue_pv(j);
-            }
-        }
-    } else {
-        // ------------------------------------------------------------ softmax / epilogue
-        const int qw = warp & 3;
-        const int row = qw * 32 + lane;       // query row within the tile = TMEM lane
-        const int qpos = p.pos0 + r_begin + row;
-        const uint32_t lane_base = static_cast<uint32_t>(qw * 32) << 16;
-        float m_ref = -INFINITY, l_sum = 0.f;
-        // the first key that may lie past this warp's earliest query: tiles starting
-        // before it need no causal mask (warp-uniform test)
-        const int warp_q0 = p.pos0 + r_begin + qw * 32;
-        for (int j = 0; j < n_kt; ++j) {
-            const int s = j & 1;
-            uint8_t* P = sm + kOffP + s * kTileBytes;
-            mbar_wait(&s_full[s], (j >> 1) & 1);
-            tc_fence_after();
-            uint32_t sv[4][32];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld32(tmem + lane_base + s * 128 + c * 32, sv[c]);
-            tmem_ld_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&s_empty[s]);
-            // scale + causal mask (keys past this row's position, or past the sequence)
-            // raw scores here; the scale (> 0) is folded into one FFMA per element below
-            const int key0 = j * kKT;
-            float mx = -INFINITY;
-            if (key0 + kKT - 1 <= warp_q0) {  // tile entirely at or before every row of this warp
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sv[c][e]));
-            } else {
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        const int key = key0 + c * 32 + e;
-                        if (key > qpos) sv[c][e] = __float_as_uint(-INFINITY);
-                        mx = fmaxf(mx, __uint_as_float(sv[c][e]));
-                    }
-            }
-            mx *= p.scale_log2;
-            // P buffer s was last read by PV(j-2): it must have retired before P(j) is written
-            if (j >= 2) mbar_wait(&pv_done[s], ((j - 2) >> 1) & 1);
-            // The decision is warp-uniform: tcgen05.ld/st are warp-collective. Lanes that
-            // did not need it rescale exactly (possibly by 1), which is always valid.
-            const bool need = __any_sync(0xffffffffu, mx > m_ref + kRescaleThreshold || m_ref == -INFINITY);
-            if (need) {
-                const float m_new = fmaxf(m_ref, mx);
-                const float corr = m_ref == -INFINITY ? 0.f : exp2f(m_ref - m_new);
-                l_sum *= corr;
-                m_ref = m_new;
-                if (j > 0) {  // rescale this warp's rows of the O accumulator in TMEM
-                    mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);  // O stable: PV(j-1) retired
-                    tc_fence_after();
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        uint32_t o[32];
-                        tmem_ld32(tmem + lane_base + 256 + c * 32, o);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
-                        tmem_st32(tmem + lane_base + 256 + c * 32, o);
-                    }
-                    tmem_st_wait();
-                }
-            }
-            // P = exp2(S - m_ref) -> bf16, written in the K-major 128B-swizzled layout
-            float rs = 0.f;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-#pragma unroll
-                for (int g = 0; g < 4; ++g) {  // 8 keys = one 16-byte chunk
-                    float pv[8];
-                    // a share of the exponentials runs on the FMA pipe (the MUFU pipe
-                    // alone, 16/clk/SM, would take as long as the tile's two MMAs)
-                    const bool poly = g == 3;
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        const float x = fmaf(__uint_as_float(sv[c][g * 8 + e]), p.scale_log2, -m_ref);
-                        pv[e] = poly ? exp2_poly(x) : ex2_approx(x);
-                        rs += pv[e];
-                    }
-                    const int key = c * 32 + g * 8;  // within the tile
-                    const int half = key >> 6, chunk = (key & 63) >> 3;
-                    uint4 w;
-                    w.x = pack_bf16x2(pv[0], pv[1]);
-                    w.y = pack_bf16x2(pv[2], pv[3]);
-                    w.z = pack_bf16x2(pv[4], pv[5]);
-                    w.w = pack_bf16x2(pv[6], pv[7]);
-                    *reinterpret_cast<uint4*>(P + half * kHalf + row * 128 + ((chunk ^ (row & 7)) << 4)) = w;
-                }
-            }
-            l_sum += rs;
-            fence_async_smem();  // generic-proxy P writes -> visible to the tensor core
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&p_full[s]);
-        }
-        // ---- epilogue: O / l -> bf16 rows
-        mbar_wait(&pv_done[(n_kt - 1) & 1], ((n_kt - 1) >> 1) & 1);
-        tc_fence_after();
-        const int grow = r_begin + row;
-        const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            uint32_t o[32];
-            tmem_ld32(tmem + lane_base + 256 + c * 32, o);
-            tmem_ld_wait();
-            if (grow < p.q_len) {
-                __nv_bfloat16* dst =
-                    p.out + static_cast<size_t>(p.q_row0 + grow) * p.nq * 128 + h * 128 + c * 32;
-#pragma unroll
-                for (int e = 0; e < 32; e += 8) {
-                    uint4 w;
-                    w.x = pack_bf16x2(__uint_as_float(o[e]) * inv, __uint_as_float(o[e + 1]) * inv);
-                    w.y = pack_bf16x2(__uint_as_float(o[e + 2]) * inv, __uint_as_float(o[e + 3]) * inv);
-                    w.z = pack_bf16x2(__uint_as_float(o[e + 4]) * inv, __uint_as_float(o[e + 5]) * inv);
-                    w.w = pack_bf16x2(__uint_as_float(o[e + 6]) * inv, __uint_as_float(o[e + 7]) * inv);
-                    *reinterpret_cast<uint4*>(dst + e) = w;
-                }
-            }
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 1) {
-        tc_fence_after();
-        tmem_dealloc(tmem, 512);
-    }
-}
-
-
 
 // ============================================================ ping-pong variant (default)
 // Two 128-row query tiles of one head per CTA (rows [r0, r0+128) and [r0+128, r0+256)),
@@ -699,43 +426,6 @@ int make_map_2d(const void* ptr, unsigned long long rows, unsigned long long col
 }
 
 }  // namespace ck
-
-extern "C" int ck_attn_prefill_tc(const void* q, int q_rows_total, const void* kv_pool, long long pool_blocks,
-                                  const int* bt, int q_row0, int q_len, int pos0, void* out, int nq, int nkv, int layer,
-                                  int n_layers, float scale, void* stream) {
-    if (q_len <= 0) return 0;
-    CUtensorMap mq, mkv;
-    int rc = make_map_2d(q, static_cast<unsigned long long>(q_rows_total), static_cast<unsigned long long>(nq) * 128,
-                      kQ, &mq);
-    if (rc) return rc;
-    const unsigned long long pool_rows = static_cast<unsigned long long>(pool_blocks) * n_layers * 2 * nkv * 16;
-    rc = make_map_2d(kv_pool, pool_rows, 128, 16, &mkv);
-    if (rc) return rc;
-    static unsigned mask = 0;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!(mask & (1u << dev))) {
-        cudaError_t e =
-            cudaFuncSetAttribute(attn_prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        if (e != cudaSuccess) return static_cast<int>(e);
-        mask |= 1u << dev;
-    }
-    AttnParams prm;
-    prm.q_row0 = q_row0;
-    prm.q_len = q_len;
-    prm.pos0 = pos0;
-    prm.nq = nq;
-    prm.nkv = nkv;
-    prm.layer = layer;
-    prm.n_layers = n_layers;
-    prm.row_stride_blk = n_layers * 2 * nkv * 16;
-    prm.scale_log2 = scale * kLog2e;
-    prm.out = static_cast<__nv_bfloat16*>(out);
-    prm.table = bt;
-    const dim3 grid((q_len + kQ - 1) / kQ, nq);
-    return launch_pdl(attn_prefill_tc_kernel, grid, dim3(192), kSmemBytes, static_cast<cudaStream_t>(stream), mq, mkv,
-                      prm);
-}
 
 extern "C" int ck_attn_prefill_pp(const void* q, int q_rows_total, const void* kv_pool, long long pool_blocks,
                                   const int* bt, int q_row0, int q_len, int pos0, void* out, int nq, int nkv, int layer,

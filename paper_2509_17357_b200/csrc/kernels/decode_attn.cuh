@@ -1,12 +1,12 @@
-// Decode (single query token) paged attention for one (split item, kv head), executed by
-// a group of 4 warps (128 threads). Shared by the standalone split-KV kernel
-// (attention.cu) and the persistent decode forward (mega_decode.cu).
+// Building blocks of the decode (single query token) paged attention (attention.cu):
+// per-block math on mma.sync, the 4-warp smem merge and the ticketed global merge of a
+// sequence's parts.
 //
-// Per warp: every 4th 16-token block of the split streams through a cp.async ring
-// (STAGES deep, 128-B XOR-swizzled rows: conflict-free ldmatrix) and is consumed by
+// Per warp, 16-token K/V blocks (128-B XOR-swizzled rows: conflict-free ldmatrix) are
+// consumed by
 //   S[16 x 16] = Qpad[16 x 128] K^T   (G query heads padded to 16 MMA rows, mma.sync)
 //   O[16 x 128] += P[16 x 16] V       online softmax in registers.
-// The 4 warps merge in smem; split partials merge in the last group to finish
+// The 4 warps merge in smem; part partials merge in the last group to finish
 // (atomic ticket per (sequence, kv head), self-resetting).
 #pragma once
 
@@ -24,15 +24,6 @@ __device__ __forceinline__ size_t kv_tile_off(int block, int layer, int kv, int 
            static_cast<size_t>(head) * kDTile;
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
-    const int sz = pred ? 16 : 0;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(sz) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -253,93 +244,6 @@ __device__ void dec_store(const DecodeAttnArgs& a, int item, int kvh, const floa
         }
     }
     group_bar(bar_id);
-}
-
-template <int G>
-__device__ void dec_merge(const DecodeAttnArgs& a, int item, int kvh, uint8_t* ring_all, float* small,
-                          const float (&o)[16][4], float m_run, float l_run, int t, int bar_id) {
-    float* res = reinterpret_cast<float*>(ring_all + kDResOff);
-    dec_merge_warps<G>(ring_all, small, o, m_run, l_run, t, bar_id, res);
-    dec_store<G>(a, item, kvh, res, small, t, bar_id);
-}
-
-// smem: sQ 4 KiB (1 KiB aligned), ring = 4 * STAGES * 8 KiB (also reused as the 32 KiB
-// warp-merge scratch), small = 2 * 64 floats + 1 int. t = thread index in the group.
-template <int G, int STAGES>
-__device__ void decode_attn_item(const DecodeAttnArgs& a, int item, int kvh, uint8_t* sQ, uint8_t* ring_all,
-                                 float* small, int t, int bar_id) {
-    static_assert(4 * STAGES * 2 * kDTileBytes >= kDResOff + 8 * kDRes * 4, "merge scratch must fit in the ring");
-
-    const int wk = a.work[item];
-    const int s = wk >> 16, split = wk & 0xffff;
-    const int len = a.seq_len[s];
-    const int nblk = (len + kDBlk - 1) / kDBlk;
-    const int b0 = split * a.blocks_per_split, b1 = min(nblk, b0 + a.blocks_per_split);
-    const int warp = t >> 5, lane = t & 31;
-    const int* table = a.bt + a.seq_bt[s];
-    const int row = a.seq_row[s];
-    const int nq = a.nq;
-
-    {  // Q (G rows, zero padded to 16)
-        const __nv_bfloat16* qrow = a.q + static_cast<size_t>(row) * nq * kDHD + static_cast<size_t>(kvh) * G * kDHD;
-        for (int c = t; c < 16 * 16; c += 128) {
-            const int r = c >> 4, ch = c & 15;
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (r < G) v = *reinterpret_cast<const uint4*>(qrow + r * kDHD + ch * 8);
-            *reinterpret_cast<uint4*>(sQ + swz(r, ch)) = v;
-        }
-    }
-    uint8_t* ring = ring_all + static_cast<size_t>(warp) * STAGES * 2 * kDTileBytes;
-    const int first = b0 + warp;
-    const int mine = first < b1 ? (b1 - first + 3) / 4 : 0;
-    auto load = [&](int i) {
-        const int b = first + 4 * i;
-        const int blk = table[b];
-        const __nv_bfloat16* kt = a.pool + kv_tile_off(blk, a.layer, 0, kvh, a.n_layers, a.nkv);
-        const __nv_bfloat16* vt = kt + static_cast<size_t>(a.nkv) * kDTile;
-        uint8_t* dK = ring + (i % STAGES) * 2 * kDTileBytes;
-        uint8_t* dV = dK + kDTileBytes;
-        const int valid = min(kDBlk, len - b * kDBlk);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int c = lane + 32 * j;
-            const int r = c >> 4, ch = c & 15;
-            const bool ok = r < valid;  // slots past the sequence end may hold stale data: zero-fill
-            cp_async16(dK + swz(r, ch), kt + r * kDHD + ch * 8, ok);
-            cp_async16(dV + swz(r, ch), vt + r * kDHD + ch * 8, ok);
-        }
-    };
-#pragma unroll
-    for (int i = 0; i < STAGES - 1; ++i) {
-        if (i < mine) load(i);
-        cp_commit();
-    }
-    group_bar(bar_id);  // sQ visible
-    uint32_t qf[8][4];
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-        const int r = lane & 15, ch = 2 * kk + (lane >> 4);
-        ldsm_x4(qf[kk], sQ + swz(r, ch));
-    }
-    float o[16][4];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-    float m_run = -INFINITY, l_run = 0.f;
-
-    for (int i = 0; i < mine; ++i) {
-        cp_wait<STAGES - 2>();
-        __syncwarp();
-        const uint8_t* K = ring + (i % STAGES) * 2 * kDTileBytes;
-        dec_block<SwzRow256>(K, K + kDTileBytes, qf, o, m_run, l_run, (first + 4 * i) * kDBlk, len, a.qk_scale_log2,
-                             lane);
-        __syncwarp();
-        const int nxt = i + STAGES - 1;
-        if (nxt < mine) load(nxt);
-        cp_commit();
-    }
-    cp_wait<0>();
-
-    dec_merge<G>(a, item, kvh, ring_all, small, o, m_run, l_run, t, bar_id);
 }
 
 }  // namespace ck

@@ -23,7 +23,7 @@ def test_every_declared_symbol_is_exported():
     from paper_2509_17357_b200._lib import lib
     L = lib()
     names = declared()
-    assert {"ck_gemm", "ck_attn_decode", "ck_attn_prefill", "cronus_run_virtual", "cronus_engine_serve"} <= names
+    assert {"ck_gemm", "ck_attn_decode_tma", "ck_attn_prefill_pp", "cronus_run_virtual", "cronus_engine_serve"} <= names
     missing = [n for n in sorted(names) if not hasattr(L, n)]
     assert not missing, missing
 

@@ -131,26 +131,6 @@ def test_qwen_style_bias_and_gqa():
     eng.close()
 
 
-@pytest.mark.parametrize("model,cfg_name", [("tiny", "a100_a10_llama8b"), ("tiny-qwen", "a100_a30_qwen7b")])
-def test_persistent_decode_forward(model, cfg_name):
-    """Decode-only CPI iterations run as ONE persistent launch (ck_mega_decode); the
-    tokens it emits pass the same teacher-forced oracle check."""
-    if not torch.cuda.is_available():
-        pytest.skip("no GPU")
-    from paper_2509_17357_b200.serving import GpuEngine
-    eng = GpuEngine(model=model, clock="virtual", profile=1, decode_forward="persistent")
-    cfg = load_cfg(cfg_name)
-    t = c1_trace().subset(np.arange(24))
-    res = eng.serve(cfg, t, want_tokens=True, profile=True)
-    st = res.extra["stats"]
-    assert st["cpi"]["mega_decode"]["launches"] > 0
-    assert res.json == E.run(cfg, t).json
-    splits = [r["partial_prefill_len"] for r in json.loads(res.json)["records"]]
-    total, exact = check_tokens(t, res.extra["tokens"], [0, 5, 11, 23], model=model, splits=splits)
-    assert exact >= 0.95 * total
-    eng.close()
-
-
 def test_wall_clock_sm_lending():
     """Green-context pair: CPI iterations issued while the PPI is idle run on every SM
     (primary-context stream); tokens and invariants are unaffected."""

@@ -162,16 +162,13 @@ def attn_ref(q, k, v, qpos, scale):
     return torch.einsum("hnt,thd->nhd", s.softmax(-1), vv)
 
 
-@pytest.mark.parametrize("impl", ["tma", "cp_async"])
 @pytest.mark.parametrize("nq,nkv", [(2, 1), (32, 8), (28, 4), (4, 2)])
-def test_attn_decode(L, nq, nkv, impl):
+def test_attn_decode(L, nq, nkv):
     gen = torch.Generator(device="cuda").manual_seed(nq)
     layers, layer = 2, 1
     lens = [1, 15, 16, 17, 100, 333, 1024, 2049]
-    # cp.async zero-fills past the end (NaN garbage must not leak); TMA reads whole
-    # blocks and masks, so stale slots hold large finite garbage instead
-    pool = make_pool(sum((l + 15) // 16 for l in lens) + 3, layers, nkv,
-                     fill=float("nan") if impl == "cp_async" else 3e4)
+    # TMA reads whole blocks and masks, so stale slots hold large finite garbage
+    pool = make_pool(sum((l + 15) // 16 for l in lens) + 3, layers, nkv, fill=3e4)
     tables, ks, vs = fill_sequences(pool, layer, lens, nkv, gen)
     S = len(lens)
     rows = torch.arange(S, dtype=torch.int32, device="cuda") * 2 + 1  # non-trivial row mapping
@@ -179,8 +176,8 @@ def test_attn_decode(L, nq, nkv, impl):
     q = torch.randn(M, nq * 128, device="cuda", generator=gen).bfloat16()
     bt = torch.cat(tables)
     offs = np.concatenate([[0], np.cumsum([len(t) for t in tables])[:-1]]).astype(np.int32)
-    # cp_async: blocks per split; tma: (blocks per part, cluster CTAs per part)
-    cases = [(1, 1), (3, 1), (64, 1)] if impl == "cp_async" else [(64, 1), (3, 1), (64, 2), (5, 4), (64, 8), (1000, 16)]
+    # (blocks per part, cluster CTAs per part)
+    cases = [(64, 1), (3, 1), (64, 2), (5, 4), (64, 8), (1000, 16)]
     for bps, cluster in cases:
         work, item0 = [], []
         for s_i, ln in enumerate(lens):
@@ -197,14 +194,9 @@ def test_attn_decode(L, nq, nkv, impl):
         tickets = torch.zeros(S * nkv, dtype=torch.int32, device="cuda")
         out = torch.zeros(M, nq * 128, dtype=torch.bfloat16, device="cuda")
         scale = 1 / math.sqrt(128)
-        if impl == "tma":
-            ok(L.ck_attn_decode_tma(p(q), p(pool), pool.shape[0], p(bt), p(rows), p(t_len), p(t_off), p(t_item0),
-                                    p(t_work), len(work), S, cluster, p(ws), p(tickets), p(out), nq, nkv, layer,
-                                    layers, scale, None, stream()))
-        else:
-            ok(L.ck_attn_decode(p(q), p(pool), p(bt), p(rows), p(t_len), p(t_off), p(t_item0), p(t_work),
-                                len(work), S, bps, p(ws), p(tickets), p(out), nq, nkv, layer, layers, scale,
-                                stream()))
+        ok(L.ck_attn_decode_tma(p(q), p(pool), pool.shape[0], p(bt), p(rows), p(t_len), p(t_off), p(t_item0),
+                                p(t_work), len(work), S, cluster, p(ws), p(tickets), p(out), nq, nkv, layer,
+                                layers, scale, None, stream()))
         assert tickets.abs().sum() == 0  # self-resetting
         for s_i, ln in enumerate(lens):
             r = int(rows[s_i])
@@ -213,27 +205,21 @@ def test_attn_decode(L, nq, nkv, impl):
             assert torch.allclose(got, ref, rtol=2e-2, atol=2e-2), (bps, cluster, ln, (got - ref).abs().max().item())
 
 
-@pytest.mark.parametrize("impl", ["mma", "tc", "pp"])
 @pytest.mark.parametrize("nq,nkv", [(2, 1), (32, 8), (28, 4)])
 @pytest.mark.parametrize("pos0,qlen", [(0, 1), (0, 77), (0, 256), (300, 64), (1000, 212), (48, 512), (2000, 700)])
-def test_attn_prefill(L, nq, nkv, pos0, qlen, impl):
+def test_attn_prefill(L, nq, nkv, pos0, qlen):
     gen = torch.Generator(device="cuda").manual_seed(pos0 + qlen + nq)
     layers, layer = 2, 0
     T = pos0 + qlen
-    # tc reads whole blocks (masked): stale slots must be finite -> large finite garbage
-    pool = make_pool((T + 15) // 16 + 5, layers, nkv, fill=float("nan") if impl == "mma" else 3e4)
+    # whole blocks are read (masked): stale slots must be finite -> large finite garbage
+    pool = make_pool((T + 15) // 16 + 5, layers, nkv, fill=3e4)
     tables, ks, vs = fill_sequences(pool, layer, [T], nkv, gen)
     row0 = 3
     q = torch.randn(row0 + qlen + 2, nq * 128, device="cuda", generator=gen).bfloat16()
     out = torch.zeros_like(q)
     scale = 1 / math.sqrt(128)
-    if impl == "mma":
-        ok(L.ck_attn_prefill(p(q), p(pool), p(tables[0]), row0, qlen, pos0, p(out), nq, nkv, layer, layers, scale,
-                             stream()))
-    else:
-        fn = L.ck_attn_prefill_tc if impl == "tc" else L.ck_attn_prefill_pp
-        ok(fn(p(q), q.shape[0], p(pool), pool.shape[0], p(tables[0]), row0, qlen, pos0, p(out), nq, nkv, layer,
-              layers, scale, stream()))
+    ok(L.ck_attn_prefill_pp(p(q), q.shape[0], p(pool), pool.shape[0], p(tables[0]), row0, qlen, pos0, p(out), nq,
+                            nkv, layer, layers, scale, stream()))
     qpos = torch.arange(pos0, T, device="cuda")
     ref = attn_ref(q[row0:row0 + qlen].view(qlen, nq, 128), ks[0], vs[0], qpos, scale)
     got = out[row0:row0 + qlen].float().view(qlen, nq, 128)
@@ -389,7 +375,7 @@ def test_attn_long_context(L, nq, nkv):
     scale = 1 / math.sqrt(128)
     refs = [attn_ref(q[s].view(1, nq, 128), ks[s], vs[s], torch.tensor([ln - 1], device="cuda"), scale)
             for s, ln in enumerate(lens)]
-    for impl, bps, cluster in [("tma", 128, 8), ("tma", 400, 16), ("cp_async", 64, 1)]:
+    for bps, cluster in [(128, 8), (400, 16), (64, 1)]:
         work, item0 = [], []
         for s_i, ln in enumerate(lens):
             item0.append(len(work))
@@ -401,18 +387,13 @@ def test_attn_long_context(L, nq, nkv):
         ws = torch.empty(len(work) * nq * 130, device="cuda")
         tickets = torch.zeros(S * nkv, dtype=torch.int32, device="cuda")
         out = torch.zeros(S, nq * 128, dtype=torch.bfloat16, device="cuda")
-        if impl == "tma":
-            ok(L.ck_attn_decode_tma(p(q), p(pool), pool.shape[0], p(bt), p(rows), p(t_len), p(t_off), p(t_item0),
-                                    p(t_work), len(work), S, cluster, p(ws), p(tickets), p(out), nq, nkv, layer,
-                                    layers, scale, None, stream()))
-        else:
-            ok(L.ck_attn_decode(p(q), p(pool), p(bt), p(rows), p(t_len), p(t_off), p(t_item0), p(t_work),
-                                len(work), S, bps, p(ws), p(tickets), p(out), nq, nkv, layer, layers, scale,
-                                stream()))
+        ok(L.ck_attn_decode_tma(p(q), p(pool), pool.shape[0], p(bt), p(rows), p(t_len), p(t_off), p(t_item0),
+                                p(t_work), len(work), S, cluster, p(ws), p(tickets), p(out), nq, nkv, layer,
+                                layers, scale, None, stream()))
         assert tickets.abs().sum() == 0
         for s_i in range(S):
             got = out[s_i].float().view(1, nq, 128)
-            assert torch.allclose(got, refs[s_i], rtol=2e-2, atol=2e-2), (impl, lens[s_i], (got - refs[s_i]).abs().max().item())
+            assert torch.allclose(got, refs[s_i], rtol=2e-2, atol=2e-2), (bps, cluster, lens[s_i], (got - refs[s_i]).abs().max().item())
     # chunked prefill of 512 tokens over a 16k prefix (the first sequence's KV)
     pos0, qlen = 16384 - 512, 512
     q2 = torch.randn(qlen, nq * 128, device="cuda", generator=gen).bfloat16()

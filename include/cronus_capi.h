@@ -47,8 +47,10 @@ int cronus_choose_split(const char* cfg_text, int n_decode, long long decode_ctx
 int cronus_fit(int kind, int n, const double* x0, const double* x1, const double* y,
                double* coef, double* r2, double* mape);
 
-/* metrics.hpp:44 percentile. */
-double cronus_percentile(const double* v, int n, double p);
+/* metrics.hpp:44 percentile (nearest rank, p in (0, 1]) -> *out. Errors as in the
+ * reference (std::invalid_argument for an empty set or p outside (0, 1]) come back as a
+ * non-zero return with cronus_last_error() set. */
+int cronus_percentile(const double* v, int n, double p, double* out);
 
 /* config round trip (model.hpp:78-80): parse then serialize. */
 int cronus_config_roundtrip(const char* cfg_text, char** out);

@@ -40,8 +40,7 @@ def lib() -> ctypes.CDLL:
                                       ctypes.c_longlong, ctypes.c_int, ctypes.c_int, i32p, f64p,
                                       f64p, i32p]
     L.cronus_fit.argtypes = [ctypes.c_int, ctypes.c_int, f64p, f64p, f64p, f64p, f64p, f64p]
-    L.cronus_percentile.argtypes = [f64p, ctypes.c_int, ctypes.c_double]
-    L.cronus_percentile.restype = ctypes.c_double
+    L.cronus_percentile.argtypes = [f64p, ctypes.c_int, ctypes.c_double, f64p]
     L.cronus_config_roundtrip.argtypes = [ctypes.c_char_p, vpp]
     _bind_gpu(L)
     _lib = L

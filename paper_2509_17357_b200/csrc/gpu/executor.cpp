@@ -300,13 +300,18 @@ struct GpuEngine::Impl {
         if (cpi_blocks < cfg.high_gpu.kv_blocks_capacity || ppi_blocks < cfg.low_gpu.kv_blocks_capacity)
             throw std::invalid_argument("B200 engine: physical KV pools smaller than the profiles' capacities");
         const long long bb = spec.kv_block_bytes();
+        // a worker's metadata buffer is sized for its pool's block count: a grown pool
+        // rebuilds the worker that indexes it
+        bool regrow_cpi = false, regrow_ppi = false;
         if (!pool_cpi || pool_cpi->blocks < cpi_blocks) {
             pool_cpi.reset();
             pool_cpi = std::make_unique<gpu::KvPool>(opt.cpi_device, cpi_blocks, bb);
+            regrow_cpi = true;
         }
         if (!pool_ppi || pool_ppi->blocks < ppi_blocks) {
             pool_ppi.reset();
             pool_ppi = std::make_unique<gpu::KvPool>(opt.ppi_device, ppi_blocks, bb);
+            regrow_ppi = true;
         }
         // Each side's worker serves the roles the policy puts there: serial prefill in
         // ppi_chunk-row slices and/or chunked iterations of up to B rows (all sampled).
@@ -316,7 +321,7 @@ struct GpuEngine::Impl {
         const int B[2] = {cfg.max_batched_tokens_low, cfg.max_batched_tokens_high};
         auto rows = [&](int h) { return std::max(serial[h] ? opt.ppi_chunk : 0, chunked[h] ? B[h] : 0); };
         auto samples = [&](int h) { return std::max(1, chunked[h] ? B[h] : 0); };
-        if (!cpi || cpi_rows < rows(1) || cpi_samples < samples(1)) {
+        if (!cpi || regrow_cpi || cpi_rows < rows(1) || cpi_samples < samples(1)) {
             cpi.reset();
             cpi_rows = std::max(cpi_rows, rows(1));
             cpi_samples = std::max(cpi_samples, samples(1));
@@ -324,7 +329,7 @@ struct GpuEngine::Impl {
             cpi = std::make_unique<gpu::Worker>(*w_cpi, cpi_rows, cpi_samples,
                                                 static_cast<int>(pool_cpi->blocks) + cpi_rows, s_cpi, cpi_ctas);
         }
-        if (!ppi || ppi_rows < rows(0) || ppi_samples < samples(0)) {
+        if (!ppi || regrow_ppi || ppi_rows < rows(0) || ppi_samples < samples(0)) {
             ppi.reset();
             ppi_rows = std::max(ppi_rows, rows(0));
             ppi_samples = std::max(ppi_samples, samples(0));

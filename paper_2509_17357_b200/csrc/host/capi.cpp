@@ -139,8 +139,8 @@ int cronus_fit(int kind, int n, const double* x0, const double* x1, const double
     });
 }
 
-double cronus_percentile(const double* v, int n, double p) {
-    return cronus::percentile(std::vector<double>(v, v + n), p);
+int cronus_percentile(const double* v, int n, double p, double* out) {
+    return guarded([&] { *out = cronus::percentile(std::vector<double>(v, v + n), p); });
 }
 
 int cronus_config_roundtrip(const char* cfg_text, char** out) {

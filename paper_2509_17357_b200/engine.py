@@ -112,9 +112,9 @@ def fit_chunked(prefill_ctx, decode_ctx_sum, times_ms):
 
 def percentile(samples, p):
     v = np.ascontiguousarray(samples, np.float64)
-    if len(v) == 0:
-        raise ValueError("percentile: empty sample set")
-    return lib().cronus_percentile(_p(v, ctypes.c_double), len(v), p)
+    out = ctypes.c_double()
+    check(lib().cronus_percentile(_p(v, ctypes.c_double), len(v), p, ctypes.byref(out)))
+    return out.value
 
 
 def config_roundtrip(cfg_text: str) -> str:

@@ -302,6 +302,14 @@ def test_percentile_nearest_rank():
     assert E.percentile(list(range(1, 1001)), 0.99) == 990.0
 
 
+@pytest.mark.parametrize("samples,p", [([], 0.99), ([1.0, 2.0], 99.0), ([1.0], 0.0), ([1.0], -0.5)])
+def test_percentile_errors_cross_the_c_abi(samples, p):
+    """metrics.cpp:13-15: empty sets and p outside (0, 1] throw std::invalid_argument; the
+    C ABI turns it into ValueError instead of terminating the process."""
+    with pytest.raises(ValueError):
+        E.percentile(samples, p)
+
+
 def test_config_roundtrip():
     """test_model.cpp:73-86: serialize -> parse is the identity."""
     for name in ("a100_a10_llama8b", "a100_a30_qwen7b"):

@@ -5,20 +5,24 @@
 Workload (BASELINE.json configs[1] at N=1): LLaMA3-8B shapes (bf16, random init),
 one B200 with the partial-prefill worker (PPI, 40 SMs) and the chunked-prefill/decode
 worker (CPI, 108 SMs) co-located via green-context SM partitioning; synthetic trace of
-the paper's shape (lognormal lengths, mean 1014 input / 247 output tokens, seed 1),
-all requests at t = 0 (the paper's max-throughput protocol); scheduler on
-the wall clock with B200-calibrated cost profiles (tests/golden/configs/
+the paper's shape (synth_trace(1000, 1014, 247, seed 1), lognormal
+lengths), all requests at t = 0 (the paper's max-throughput protocol, PAPER.md:153);
+scheduler on the wall clock with B200-calibrated cost profiles (tests/golden/configs/
 b200_llama8b_coloc.cfg, produced by paper_2509_17357_b200.calibrate).
 
-A step = serving the whole trace to completion. `value` = requests completed / step
-time with prompts already resident in HBM; `e2e` = the same through the C-ABI with host
-buffers (prompt tokens H2D and generated tokens D2H inside the timed region). N > 1
-GPUs form N/2 worker pairs (PPI GPU 2p, CPI GPU 2p+1, NVLink handoff); pair p serves
-the requests with id % pairs == p (static rule); weak scaling.
+A step = serving the whole 1000-request trace to completion. `value` = requests
+completed / step time with prompts already resident in HBM; `e2e` = the same through the
+C-ABI with host buffers (prompt tokens H2D and generated tokens D2H inside the timed
+region). `latency` = the same trace with fixed-interval arrivals offered at 0.7 x the
+measured max req/s: TTFT / TBT P99 under load. N > 1 GPUs form N/2
+worker pairs (PPI GPU 2p, CPI GPU 2p+1, NVLink handoff); pair p serves the requests with
+id % pairs == p (static rule); weak scaling; P99s over the samples
+pooled across pairs (metrics.cpp:35-57).
 
 --impl reference: the CPU path on this host (oracle port of the decoder on all cores,
 fitted with the reference's own fit_* and scheduled by the reference's own simulator,
-oracle/_ref) for the same trace and metric.
+oracle/_ref, on a trace synthesized by the reference's own synth_trace) for the same
+metric; each step is one bounded CPU profile + fit + simulation.
 """
 from __future__ import annotations
 
@@ -47,7 +51,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--requests", type=int, default=256, help="requests per worker pair per step")
+    ap.add_argument("--requests", type=int, default=1000, help="requests per worker pair per step (C2: 1000)")
     ap.add_argument("--warmup-requests", type=int, default=24)
     ap.add_argument("--model", default="llama3-8b")
     ap.add_argument("--config", default=None)
@@ -63,6 +67,12 @@ def parse():
     ap.add_argument("--profile-requests", type=int, default=48, help="trace prefix profiled with CUPTI")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--latency-load", type=float, default=0.7,
+                    help="fixed-interval point at this fraction of the measured max req/s (0: off)")
+    ap.add_argument("--time-budget-s", type=float, default=1500.0,
+                    help="wall budget of the whole run: optional legs are skipped to stay inside it")
+    ap.add_argument("--one-gpu-pairs", action="store_true",
+                    help="test hook: every rank on GPU 0 (gloo), pairs as separate-device engines")
     return ap.parse_args()
 
 
@@ -285,12 +295,13 @@ def decode_attn_probe(seqs=64, ctx=1024, layers=4, reps=40):
             "frac": round(alg / us / 1e3 / hbm, 4), "us_per_launch": round(us, 2), "algorithmic_per_launch": alg}
 
 
-def roofline(stats, partition=None):
-    """Dominant kernel class of the profiled step -> roofline object (+ all classes).
+def roofline(stats, partition=None, critical=None):
+    """Kernel classes of a profiled serve -> (dominant class's roofline object, all classes).
 
-    Tensor-bound classes also get `frac_partition`: the fraction of the peak scaled to
-    the SMs the worker owns (PPI 40 / CPI 108 of 148 in the co-located split; CPI
-    iterations on lent SMs make the CPI figure conservative)."""
+    Dominant = the largest time share on the `critical` worker (the one busy the whole
+    step: the CPI), or overall when None. Tensor-bound classes also get `frac_partition`:
+    the fraction of the peak scaled to the SMs the worker owns (PPI 40 / CPI 108 of 148
+    in the co-located split; CPI iterations on lent SMs make the CPI figure conservative)."""
     hbm, tf_burst, tf_sus, src = peaks()
     ratios = traffic_ratios()
     sms = {"ppi": (partition or {}).get("ppi_sms"), "cpi": (partition or {}).get("cpi_sms")}
@@ -321,42 +332,125 @@ def roofline(stats, partition=None):
                 ent["traffic_source"] = src_t
             classes.append(ent)
     classes.sort(key=lambda c: -c["share_ms"])
-    top = dict(classes[0]) if classes else {}
+    pool = [c for c in classes if critical is None or c["kernel"].startswith(critical + ".")]
+    top = dict(pool[0]) if pool else {}
     if top:
         top.setdefault("traffic", None)
         top["peak_source"] = f"MEASURED_PEAKS.json ({src}; {'sustained' if top['bound'] == 'tensor' else 'copy'})"
     return top, classes
 
 
+def pass_rooflines(stats):
+    """Pass-level HBM figures from the timed serve's own iteration records (wall-clock
+    events per CPI iteration, PDL chains intact): decode-only passes stream every layer's
+    weights + the LM head once plus each decoder's KV, so bytes / pass time is their
+    achieved HBM rate (SURVEY.md 8(d) 'small-M GEMM: HBM', 'decode attention: HBM')."""
+    hbm = peaks()[0]
+    wb, kvb = stats.get("pass_weight_bytes"), stats.get("kv_bytes_per_token")
+    out = {}
+    for key, (n, ms, rows, ctx) in (stats.get("iteration_shapes") or {}).items():
+        if not key.startswith("decode ") or not n or not wb:
+            continue
+        per = wb + rows * ctx * kvb
+        us = 1e3 * ms / n
+        out[key.split(" ", 1)[1] + " decoders"] = {
+            "passes": n, "us_per_pass": round(us, 1), "mean_decoders": round(rows, 2), "mean_ctx": round(ctx, 1),
+            "bytes_per_pass": per, "achieved_GBps": round(per / us / 1e3, 1), "frac": round(per / us / 1e3 / hbm, 4)}
+    return out
+
+
+class Comm:
+    """The few collectives bench needs (NCCL on GPUs; gloo for the one-GPU test hook)."""
+
+    def __init__(self, world, gloo):
+        self.world, self.gloo = world, gloo
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            dist.init_process_group("gloo" if gloo or not torch.cuda.is_available() else "nccl")
+
+    def _dev(self):
+        import torch
+        return "cpu" if self.gloo or not torch.cuda.is_available() else "cuda"
+
+    def barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def reduce(self, vals, op="max"):
+        if self.world == 1:
+            return list(vals)
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor(list(vals), dtype=torch.float64, device=self._dev())
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+        return t.cpu().tolist()
+
+    def gather(self, obj):
+        if self.world == 1:
+            return [obj]
+        import torch.distributed as dist
+        out = [None] * self.world
+        dist.all_gather_object(out, obj)
+        return out
+
+
+def nearest_rank(samples, p=0.99):
+    """metrics.cpp:13-20 (nearest rank)."""
+    v = np.sort(np.asarray(samples, np.float64))
+    return float(v[max(1, int(np.ceil(p * len(v)))) - 1]) if len(v) else None
+
+
+def pooled(reports):
+    """TTFT / TBT P99 and means over the request records of every pair (metrics.cpp:35-57:
+    TBT samples pooled across requests, here across pairs too)."""
+    recs = [r for rep in reports for r in rep["records"] if r.get("ttft_ms", -1) >= 0]
+    ttft = [r["ttft_ms"] for r in recs]
+    tbt = [x for r in recs for x in r["tbt_samples_ms"]]
+    return {"ttft_p99_ms": nearest_rank(ttft), "tbt_p99_ms": nearest_rank(tbt),
+            "ttft_mean_ms": float(np.mean(ttft)) if ttft else None, "tbt_mean_ms": float(np.mean(tbt)) if tbt else None,
+            "requests": len(recs), "tbt_samples": len(tbt)}
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_ours(args, rank, world):
     import torch
     from paper_2509_17357_b200.serving import GpuEngine
 
+    t_run0 = time.perf_counter()
     pairs = max(1, world // 2)
     colocated = world == 1
     cfg_path, cfg = load_cfg(args.config, args.policy)
     trace = make_trace(args, pairs)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    comm = Comm(world, args.one_gpu_pairs)
     driver = colocated or rank % 2 == 0  # even ranks drive a pair; odd ranks host its CPI GPU
     pair = rank // 2
-    dev = 0 if colocated else rank
+    dev = 0 if colocated or args.one_gpu_pairs else rank
     torch.cuda.set_device(dev)
-    eng = None
+    eng = sub = None
     if driver:
         opts = dict(model=args.model, clock="wall")
         opts["ppi_sms"] = args.ppi_sms  # the low-end worker: an SM partition (its own GPU when N > 1)
-        if not colocated:
+        if args.one_gpu_pairs and not colocated:
+            opts.update(ppi_device=0, cpi_device=0, separate=1)
+        elif not colocated:
             opts.update(ppi_device=rank, cpi_device=rank + 1)
         eng = GpuEngine(**opts)
         sub = pair_trace(trace, pair, pairs)
         warm = sub.subset(np.arange(min(args.warmup_requests, len(sub))), name="warmup")
 
-    def barrier():
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
+    def left():
+        return args.time_budget_s - (time.perf_counter() - t_run0)
 
     # ---- warm-up: W untimed serves (short trace: every kernel shape class, graphs of streams)
     for _ in range(args.warmup):
@@ -367,8 +461,9 @@ def run_ours(args, rank, world):
     # ---- timed: K serves of the full trace, device-timed, max over ranks
     times, reports = [], []
     clocks = None
-    for _ in range(args.steps):
-        barrier()
+    steps_run = 0
+    for i in range(args.steps):
+        comm.barrier()
         torch.cuda.synchronize()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with ClockSampler(dev) as cs:
@@ -382,77 +477,94 @@ def run_ours(args, rank, world):
             ms = max(ms, res.extra["stats"]["gpu_ms"])  # engine streams' own event span
             reports.append(res)
         times.append(ms)
-    local = np.array(times, dtype=np.float64)
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor(local, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        local = t.cpu().numpy()
+        steps_run += 1
+        # guard: a step count that cannot finish inside the budget would lose the whole run
+        # (after the next step there must still be room for the e2e and latency legs)
+        proj = comm.reduce([(time.perf_counter() - t_run0) + np.mean(times) / 1e3 * (1.05 + 1.0 + 1.5)])[0]
+        if i + 1 < args.steps and proj > args.time_budget_s:
+            print(f"[bench] time budget: stopping after {steps_run} of {args.steps} steps", file=sys.stderr)
+            break
+    local = comm.reduce(times)
     step_ms = float(np.mean(local))
-    n_done = 0
-    if driver:
-        n_done = json.loads(reports[-1].json)["completed"]
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([n_done], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t)
-        n_done = int(t.item())
+    n_done = json.loads(reports[-1].json)["completed"] if driver else 0
+    n_done = int(comm.reduce([n_done], "sum")[0])
     value = n_done / (step_ms / 1e3)
+    reps = comm.gather(json.loads(reports[-1].json) if driver else None)
+    reps = [r for r in reps if r is not None]
+    lat_max = pooled(reps)
+    stats_all = comm.gather(reports[-1].extra["stats"] if driver else None)
+    stats_all = [s for s in stats_all if s is not None]
 
     # ---- e2e: host prompt buffers in, generated tokens out, through the C-ABI
     e2e = None
     if not args.no_e2e:
-        from oracle import numerics as NUM  # prompt synthesis restated on the host (input data only)
-        prompts = None
-        if driver:
-            vocab = NUM.PRESETS[args.model].vocab
-            prompts = np.concatenate([NUM.prompt_tokens(99, int(sub.ids[i]), int(sub.input_len[i]), vocab)
-                                      for i in range(len(sub))]).astype(np.int32)
-        barrier()
+        prompts = eng.prompts(cfg, sub) if driver else None  # host copy of the staged prompt tokens
+        comm.barrier()
         torch.cuda.synchronize()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record()
         r = eng.serve(cfg, sub, host_prompt=prompts, want_tokens=True, events=False) if driver else None
         s1.record()
         torch.cuda.synchronize()
-        ems = s0.elapsed_time(s1)
-        if world > 1:
-            import torch.distributed as dist
-            t = torch.tensor([ems], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
-        h2d = r.extra["stats"]["h2d_bytes"] if driver else 0
-        d2h = r.extra["stats"]["d2h_bytes"] if driver else 0
+        ems = comm.reduce([s0.elapsed_time(s1)])[0]
+        h2d, d2h = comm.reduce([r.extra["stats"]["h2d_bytes"] if driver else 0,
+                                r.extra["stats"]["d2h_bytes"] if driver else 0], "sum")
         e2e = {"value": round(n_done / (ems / 1e3), 4), "unit": "req/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h)}
+               "d2h_bytes_per_step": int(d2h), "ms": round(ems, 2)}
 
-    # ---- profiled step (kernel classes timed with CUDA events on their streams)
-    # Kernel rooflines. (1) CUPTI critical-path times on a bounded sample (the first
-    # --profile-requests requests; chains intact) -> `roofline` / `kernels`. (2) CUDA events
-    # around every launch over the whole trace -> `kernels_events`: events between kernels
-    # break the PDL overlap, so these per-kernel figures are conservative.
-    roof, classes, classes_ev, prof_stats, handoff, attn_probe = {}, [], [], None, None, None
-    if not args.no_profile and driver:
-        sample = sub.subset(np.arange(min(args.profile_requests, len(sub))), name="profile-sample")
-        try:
-            cp = cupti_profile(eng, cfg, sample)
-            roof, classes = roofline(cp, cp["partition"])
-            handoff = cp.get("handoff")
-            if roof:
-                roof["timing"] = (f"CUPTI kernel records, critical-path time per launch, first {len(sample)} "
-                                  "requests of the trace")
-        except Exception as ex:  # profiler unavailable: fall back to the event-timed step
-            print(f"[bench] CUPTI profile failed ({ex}); using event timing", file=sys.stderr)
+    # ---- latency under load: fixed-interval arrivals at latency_load x the measured max req/s
+    latency = None
+    # every rank takes the same decision (a collective), so the legs below stay in step
+    est = np.mean(times) / 1e3 / max(args.latency_load, 1e-9)
+    short = comm.reduce([1.0 if left() < 1.2 * est + 1.3 * step_ms / 1e3 else 0.0])[0] > 0
+    if args.latency_load > 0 and not short:
+        iv = 1000.0 / (args.latency_load * value)  # ms between arrivals (all pairs' requests interleaved)
+        from paper_2509_17357_b200 import engine as E
+        fi = E.synth_trace(args.requests * pairs, args.mean_in, args.mean_out, E.FIXED_INTERVAL, iv, 1)
+        fsub = pair_trace(fi, pair, pairs) if driver else None
+        if driver:
+            eng.stage(cfg, fsub)
+        comm.barrier()
+        torch.cuda.synchronize()
+        r = eng.serve(cfg, fsub, events=False) if driver else None
+        torch.cuda.synchronize()
+        freps = [x for x in comm.gather(json.loads(r.json) if driver else None) if x is not None]
+        span = max(x["t_end_ms"] for x in freps) - min(x["t_start_ms"] for x in freps)
+        latency = dict(offered_load=args.latency_load, interval_ms=round(iv, 4), offered_rps=round(1000.0 / iv, 4),
+                       value=round(sum(x["completed"] for x in freps) / (span / 1e3), 4), unit="req/s",
+                       **{k: (round(v, 3) if isinstance(v, float) else v) for k, v in pooled(freps).items()},
+                       trace=f"synth(n={args.requests * pairs}, mean_in={args.mean_in:g}, mean_out={args.mean_out:g}, "
+                             f"seed=1, fixed-interval {iv:.4f} ms)")
+    elif args.latency_load > 0:
+        print("[bench] time budget: latency leg skipped", file=sys.stderr)
+
+    # ---- kernel rooflines: a profiled serve of the SAME trace (CUDA events around every
+    # launch on its worker's stream; events between kernels serialise the PDL chain, so the
+    # per-kernel figures are conservative), plus pass-level figures from the timed serve
+    # and CUPTI critical-path times on a bounded prefix (chains intact) as a cross-check.
+    roof, classes, crit, attn_probe, handoff, prof_stats = {}, [], [], None, None, None
+    short = comm.reduce([1.0 if left() < 1.3 * step_ms / 1e3 + 60 else 0.0])[0] > 0
+    if not args.no_profile and driver and not short:
         pr = eng.serve(cfg, sub, events=False, profile=True)
         prof_stats = pr.extra["stats"]
-        roof_ev, classes_ev = roofline(prof_stats, prof_stats.get("partition"))
-        if not roof:
-            roof, classes = roof_ev, classes_ev
-            roof["timing"] = "CUDA events around each launch (serialises PDL chains: conservative)"
+        roof, classes = roofline(prof_stats, prof_stats.get("partition"), critical="cpi")
+        if roof:
+            roof["timing"] = (f"CUDA events around each launch over the whole {len(sub)}-request trace "
+                              "(average launch of the CPI worker's largest-share kernel class)")
+        try:
+            sample = sub.subset(np.arange(min(args.profile_requests, len(sub))), name="profile-sample")
+            cp = cupti_profile(eng, cfg, sample)
+            _, crit = roofline(cp, cp["partition"])
+            handoff = cp.get("handoff")
+        except Exception as ex:
+            print(f"[bench] CUPTI profile failed ({ex})", file=sys.stderr)
         try:
             attn_probe = decode_attn_probe()
         except Exception as ex:
             print(f"[bench] decode attention probe failed ({ex})", file=sys.stderr)
+    elif not args.no_profile and driver:
+        print("[bench] time budget: profiled serve skipped", file=sys.stderr)
+    comm.barrier()
 
     if rank != 0:
         return None
@@ -460,27 +572,33 @@ def run_ours(args, rank, world):
     st = reports[-1].extra["stats"]
     line = {
         "metric": "req/s (Cronus partial-prefill serving, paper-shape trace; TTFT/TBT P99 alongside)",
-        "value": round(value, 4), "unit": "req/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "value": round(value, 4), "unit": "req/s", "n_gpus": world, "steps": steps_run, "warmup": args.warmup,
         "ms_per_step": round(step_ms, 2), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (lognormal trace of the paper's shape; random-init weights)",
-        "ttft_p99_ms": round(rep["ttft_p99_ms"], 3), "tbt_p99_ms": round(rep["tbt_p99_ms"], 3),
-        "ttft_mean_ms": round(rep["ttft_mean_ms"], 3), "tbt_mean_ms": round(rep["tbt_mean_ms"], 3),
+        "ttft_p99_ms": round(lat_max["ttft_p99_ms"], 3), "tbt_p99_ms": round(lat_max["tbt_p99_ms"], 3),
+        "ttft_mean_ms": round(lat_max["ttft_mean_ms"], 3), "tbt_mean_ms": round(lat_max["tbt_mean_ms"], 3),
+        "p99_pooled_requests": lat_max["requests"], "latency": latency,
         "config": {"workload": ("LLaMA3-8B shapes, 1 B200, PPI+CPI co-located (green-context SM split)"
                                 if colocated else f"LLaMA3-8B shapes, {pairs} PPI/CPI pair(s) over NVLink"),
                    "model": args.model, "policy": args.policy, "requests_per_pair": len(sub), "pairs": pairs,
-                   "trace": (f"synth(mean_in={args.mean_in:g}, mean_out={args.mean_out:g}, seed=1, {args.arrival}"
+                   "trace": (f"synth(n={args.requests * pairs}, mean_in={args.mean_in:g}, mean_out={args.mean_out:g}, "
+                             f"seed=1, {args.arrival}"
                              + (f" {args.interval_ms:g} ms)" if args.arrival == "fixed-interval" else ")")),
                    "cluster_config": os.path.relpath(cfg_path, ROOT), "clock": "wall (CUDA events)",
-                   "partition": st.get("partition"), "l2": "inputs > L2 (16 GB of weights streamed per iteration)",
-                   "parallelism": "replicas of worker pairs" if pairs > 1 else "co-located pair"},
-        "gpu_launches": int(st.get("gpu_launches", 0)),
-        "cpi_iterations": st["cpi_iterations"], "violations": len(rep["violations"]),
+                   "partition": st.get("partition"), "l2": "inputs > L2 (15 GB of weights streamed per iteration)",
+                   "parallelism": "replicas of worker pairs" if pairs > 1 else "co-located pair",
+                   "p99": "nearest rank over samples pooled across pairs"},
+        "gpu_launches": int(sum(s.get("gpu_launches", 0) for s in stats_all)),
+        "cpi_iterations": st["cpi_iterations"], "violations": sum(len(r["violations"]) for r in reps),
         "cpi_busy_ms": round(st.get("cpi_busy_ms", 0.0), 2),
         "cpi_lent_iterations": st.get("cpi_lent_iterations"),
         "iteration_shapes_count_ms_rows_ctx": st.get("iteration_shapes"),
-        "clocks": clocks, "e2e": e2e, "roofline": roof, "kernels": classes[:8], "kernels_events": classes_ev[:8],
+        "clocks": clocks, "e2e": e2e, "roofline": roof, "kernels": classes[:8],
+        "decode_pass_hbm": pass_rooflines(st), "kernels_critical_path_prefix": crit[:8],
         "handoff": handoff, "decode_attn_kernel": attn_probe,
     }
+    if steps_run < args.steps:
+        line["steps_requested"] = args.steps
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(args, cfg, sub)
     return line
@@ -491,6 +609,7 @@ def cpu_baseline(args, cfg, sub):
     t = refsim.Trace(sub.ids, sub.arrival_ms, sub.input_len, sub.output_len, sub.name)
     r = CB.run(cfg, t, model=args.model, budget_s=args.cpu_budget_s)
     return {"value": round(r["rps"], 6), "unit": "req/s", "cores": r["samples"]["threads"], "kind": "port",
+            "cpu": cpu_model(),
             "sample": ("1 of 32 decoder layers (numpy fp32, oracle restatement) timed on "
                        f"{len(r['samples']['prefill'])} prefill lengths + {len(r['samples']['chunked'])} mixed "
                        "batches, x32 + LM head; fitted with the reference's fit_prefill/fit_chunked and scheduled "
@@ -500,34 +619,46 @@ def cpu_baseline(args, cfg, sub):
 
 
 def run_reference(args, rank, world):
-    """CPU path on the host: oracle port forward (all cores) + the reference's fit and simulator."""
+    """The reference's own CPU path on this host: each step = a bounded CPU profile of the
+    decoder (oracle port, all cores) -> the reference's fit_prefill / fit_chunked -> the
+    reference's simulator on a trace from the reference's own synth_trace (oracle/_ref:
+    nothing from this repo's package is loaded). Rank 0 only."""
     if rank != 0:
         return None
     from oracle import cpu_baseline as CB, refsim
     _, cfg = load_cfg(args.config, args.policy)
-    from paper_2509_17357_b200 import engine as E  # trace synthesis only (identical draws to the reference)
     pairs = max(1, world // 2)
-    trace = make_trace(args, pairs)
-    sub = pair_trace(trace, 0, pairs)
-    t = refsim.Trace(sub.ids, sub.arrival_ms, sub.input_len, sub.output_len, sub.name)
+    full = refsim.synth_trace(args.requests * pairs, args.mean_in, args.mean_out,
+                              args.arrival == "fixed-interval", args.interval_ms, 1)
+    keep = np.nonzero(full.ids % pairs == 0)[0]
+    t = refsim.Trace(full.ids[keep], full.arrival_ms[keep], full.input_len[keep], full.output_len[keep], full.name)
+    # per-step CPU budget: the whole --steps K --warmup W run stays within a few minutes
+    budget = max(2.0, min(args.cpu_budget_s, 240.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
-        CB.cpu_profile(args.model, budget_s=2.0)
-    vals, last = [], None
+        CB.run(cfg, t, model=args.model, budget_s=budget)
+    vals, lat, last = [], [], None
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        last = CB.run(cfg, t, model=args.model, budget_s=args.cpu_budget_s)
+        last = CB.run(cfg, t, model=args.model, budget_s=budget)
         vals.append(last["rps"])
     wall = (time.perf_counter() - t0) / max(1, args.steps)
     v = float(np.mean(vals))
+    threads = last["samples"]["threads"]
     return {"metric": "req/s (Cronus partial-prefill serving, paper-shape trace; TTFT/TBT P99 alongside)",
             "impl": "reference", "value": round(v, 6), "unit": "req/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(wall * 1e3, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "ttft_p99_ms": round(last["ttft_p99_ms"], 1), "tbt_p99_ms": round(last["tbt_p99_ms"], 1),
             "config": {"workload": "same trace and cluster config as the ours arm", "model": args.model,
-                       "requests": len(sub)},
-            "cpu_baseline": {"value": round(v, 6), "unit": "req/s", "cores": os.cpu_count(), "kind": "port",
-                             "sample": "see bench.py cpu_baseline (oracle forward + reference fit + reference DES)"},
+                       "requests": len(t), "trace": t.name, "cluster_config": "same as ours (CPU-fitted profiles)"},
+            "fit_chunked": last["fit_chunked"], "fit_prefill": last["fit_prefill"],
+            "cpu_baseline": {"value": round(v, 6), "unit": "req/s", "cores": threads, "kind": "port",
+                             "cpu": cpu_model(),
+                             "sample": (f"per step: 1 of 32 decoder layers (numpy fp32 oracle port, {threads} threads) "
+                                        f"timed on {len(last['samples']['prefill'])} prefill lengths + "
+                                        f"{len(last['samples']['chunked'])} mixed batches within {budget:.1f} s, "
+                                        "x32 + LM head -> reference fit_prefill/fit_chunked -> reference simulator "
+                                        f"(oracle/_ref) on the {len(t)}-request trace")},
             "e2e": {"value": round(v, 6), "unit": "req/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 

@@ -53,6 +53,9 @@ class GpuEngine {
     // Synthesize this trace's prompt tokens on the device ahead of run() (the
     // "inputs already resident in HBM" measurement); run() then skips that step.
     void stage(const ClusterConfig& cfg, const Trace& trace);
+    // The staged trace's prompt tokens copied back to the host (n = total input tokens,
+    // trace order): the host buffers of an end-to-end serve (run with host_prompt).
+    void staged_prompts(int* out, long long n);
 
     // Calibration sample: median time (ms, CUDA events) of one forward pass on the
     // PPI (worker 0) or CPI (worker 1) with n_dec decode rows of context dec_ctx and

@@ -32,6 +32,9 @@ int cronus_engine_serve(void* engine, const char* cfg_text, int n, const int* id
 int cronus_engine_stage(void* engine, const char* cfg_text, int n, const int* id, const double* arrival_ms,
                         const int* input_len, const int* output_len);
 
+/* Host copy of the staged prompt tokens (n = total input tokens of the staged trace). */
+int cronus_engine_staged_prompts(void* engine, int* out, long long n);
+
 /* Calibration sample (see GpuEngine::time_pass): median ms of one forward pass. */
 int cronus_engine_time_pass(void* engine, const char* cfg_text, int worker, int n_dec, int dec_ctx, int chunk_len,
                             int chunk_pos0, int reps, double* ms_out);

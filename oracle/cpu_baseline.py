@@ -103,7 +103,7 @@ def cpu_profile(model: str = "llama3-8b", budget_s: float = 20.0, seed: int = 0)
     prefill = []
     for L in (32, 128, 256, 512):
         prefill.append((float(L), full(L, [(0, L, 0)], 1)))
-        if time.perf_counter() - t_start > budget_s * 0.4:
+        if len(prefill) >= 2 and time.perf_counter() - t_start > budget_s * 0.4:
             break
     chunked = []
     for (chunk, pos0, n_dec, ctx) in ((128, 0, 0, 0), (0, 0, 16, 1024), (256, 256, 8, 512), (64, 1024, 32, 1024),
@@ -113,7 +113,8 @@ def cpu_profile(model: str = "llama3-8b", budget_s: float = 20.0, seed: int = 0)
             seqs.append((n_dec, chunk, pos0))
         ms = full(n_dec + chunk, seqs, n_dec + (1 if chunk else 0))
         chunked.append((float(pos0 + chunk), float(n_dec * ctx), ms))
-        if time.perf_counter() - t_start > budget_s:
+        # fit_chunked needs >= 3 samples (costmodel.cpp:105): the budget never cuts below that
+        if len(chunked) >= 3 and time.perf_counter() - t_start > budget_s:
             break
     pf = refsim.fit(0, [p[0] for p in prefill], None, [p[1] for p in prefill])
     cf = refsim.fit(1, [c[0] for c in chunked], [c[1] for c in chunked], [c[2] for c in chunked])

@@ -20,5 +20,7 @@ def bind(L):
     L.cronus_engine_describe.restype = I
     L.cronus_engine_stage.argtypes = [V, ctypes.c_char_p, I, i32p, f64p, i32p, i32p]
     L.cronus_engine_stage.restype = I
+    L.cronus_engine_staged_prompts.argtypes = [V, i32p, ctypes.c_longlong]
+    L.cronus_engine_staged_prompts.restype = I
     L.cronus_engine_time_pass.argtypes = [V, ctypes.c_char_p, I, I, I, I, I, I, ctypes.POINTER(ctypes.c_double)]
     L.cronus_engine_time_pass.restype = I

@@ -82,6 +82,10 @@ int cronus_engine_stage(void* engine, const char* cfg_text, int n, const int* id
     });
 }
 
+int cronus_engine_staged_prompts(void* engine, int* out, long long n) {
+    return guard([&] { static_cast<cronus::GpuEngine*>(engine)->staged_prompts(out, n); });
+}
+
 int cronus_engine_time_pass(void* engine, const char* cfg_text, int worker, int n_dec, int dec_ctx, int chunk_len,
                             int chunk_pos0, int reps, double* ms_out) {
     return guard([&] {

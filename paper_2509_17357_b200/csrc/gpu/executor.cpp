@@ -781,6 +781,11 @@ class PairExecutor : public sched::Executor {
           << ", \"h2d_bytes\": " << h2d_bytes << ", \"d2h_bytes\": " << d2h_bytes
           << ", \"gpu_launches\": " << (E.cpi->launches - launches0_cpi) + (E.ppi->launches - launches0_ppi) + copy_launches
           << ", \"colocated\": " << (E.colocated ? "true" : "false") << ", \"sms\": " << E.sms
+          // bytes one pass streams regardless of its rows (all layers' weights + LM head) and
+          // the KV bytes one token adds (all layers): the pass-level roofline terms
+          << ", \"pass_weight_bytes\": "
+          << E.spec.weight_bytes() - 2LL * E.spec.vocab * E.spec.hidden
+          << ", \"kv_bytes_per_token\": " << E.spec.kv_bytes_per_token()
           << ", \"partition\": " << E.describe(false) << ", \"cpi\": {";
         ks("decode_attn", E.cpi->stat_decode_attn);
         ks("prefill_attn", E.cpi->stat_prefill_attn);
@@ -973,6 +978,15 @@ void GpuEngine::stage(const ClusterConfig& cfg, const Trace& trace) {
     impl_->staged_hash = 0;
     PairExecutor ex(*impl_, cfg, trace, o);
     ex.upload();  // synthesizes the prompts on the device and marks them staged
+}
+
+void GpuEngine::staged_prompts(int* out, long long n) {
+    if (!impl_->staged_hash) throw std::logic_error("staged_prompts: no staged trace");
+    if (static_cast<size_t>(n) * 4 > impl_->tok_cpi.prompt.cap)
+        throw std::invalid_argument("staged_prompts: more tokens than the staged trace holds");
+    check_cuda(cudaSetDevice(impl_->opt.cpi_device), "cudaSetDevice");
+    check_cuda(cudaMemcpy(out, impl_->tok_cpi.prompt.p, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost),
+               "prompt D2H");
 }
 
 RunReport GpuEngine::run(const ClusterConfig& cfg, const Trace& trace, const GpuRunOptions& opts) {

@@ -46,6 +46,14 @@ class GpuEngine:
         check(lib().cronus_engine_stage(self._h, cfg_text.encode(), len(ids), _p(ids, ctypes.c_int),
                                         _p(arr, ctypes.c_double), _p(ins, ctypes.c_int), _p(outs, ctypes.c_int)))
 
+    def prompts(self, cfg_text: str, trace: Trace) -> np.ndarray:
+        """Host copy of the trace's prompt tokens (stages the trace first): the host
+        buffers an end-to-end serve(host_prompt=...) starts from."""
+        self.stage(cfg_text, trace)
+        out = np.empty(int(trace.arrays()[2].sum()), np.int32)
+        check(lib().cronus_engine_staged_prompts(self._h, _p(out, ctypes.c_int), len(out)))
+        return out
+
     def time_pass(self, cfg_text: str, worker: int, n_dec=0, dec_ctx=0, chunk_len=0, chunk_pos0=0, reps=5) -> float:
         """Median ms of one forward pass on the PPI (0) or CPI (1) worker (calibration)."""
         ms = ctypes.c_double()

@@ -77,3 +77,30 @@ def test_kernel_classes_and_roofline_math():
     ten = classes[0]
     assert ten["bound"] == "tensor" and abs(ten["frac_partition"] - ten["frac"] * 148 / 40) < 1e-3
     assert top["kernel"] == "ppi.gemm_tc" and "peak_source" in top
+
+
+def test_pooled_p99_across_pairs():
+    """Nearest-rank P99 over TTFT values and TBT samples pooled across every pair's records
+    (metrics.cpp:13-20, 35-57), not rank 0's pair alone."""
+    import bench
+    a = {"records": [{"ttft_ms": 10.0, "tbt_samples_ms": [1.0, 2.0]}, {"ttft_ms": 30.0, "tbt_samples_ms": [3.0]}]}
+    b = {"records": [{"ttft_ms": 20.0, "tbt_samples_ms": [50.0] * 3}, {"ttft_ms": -1.0, "tbt_samples_ms": [99.0]}]}
+    got = bench.pooled([a, b])
+    assert got["requests"] == 3 and got["tbt_samples"] == 6
+    assert got["ttft_p99_ms"] == 30.0 and got["tbt_p99_ms"] == 50.0
+    assert bench.pooled([a])["tbt_p99_ms"] == 3.0  # one pair alone would miss pair b's tail
+    assert bench.nearest_rank(list(range(1, 101))) == 99 and bench.nearest_rank([]) is None
+
+
+def test_pass_roofline_and_critical_worker():
+    import bench
+    st = {"pass_weight_bytes": 15e9, "kv_bytes_per_token": 131072,
+          "iteration_shapes": {"decode 1-16": [10, 30.0, 4.0, 1000.0], "chunk+1-16": [3, 30.0, 5.0, 100.0]}}
+    out = bench.pass_rooflines(st)
+    assert list(out) == ["1-16 decoders"]
+    d = out["1-16 decoders"]
+    assert abs(d["achieved_GBps"] - (15e9 + 4 * 1000 * 131072) / 3000.0 / 1e3) < 0.1
+    stats = {"cpi": {"decode_attn": {"launches": 2, "ms": 1.0, "bytes": 1e9, "flops": 0.0}},
+             "ppi": {"gemm_tc": {"launches": 2, "ms": 5.0, "flops": 6e14, "bytes": 0.0}}}
+    top, classes = bench.roofline(stats, None, critical="cpi")
+    assert top["kernel"] == "cpi.decode_attn" and classes[0]["kernel"] == "ppi.gemm_tc"

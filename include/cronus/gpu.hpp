@@ -33,6 +33,9 @@ struct GpuRunOptions : RunOptions {
     // device (splitmix64 of (prompt_seed, request id, position)).
     const int32_t* host_prompt = nullptr;
     int32_t* host_tokens = nullptr;
+    // Test hook (co-located pair only): the fp32 logits every generated token was sampled
+    // from, [total output tokens][vocab] in host_tokens order.
+    float* host_logits = nullptr;
     std::string* stats_json = nullptr;  // kernel / iteration statistics
     bool profile = false;               // time kernel classes with CUDA events this run
 };

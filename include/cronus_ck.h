@@ -160,9 +160,10 @@ int ck_silu_mul(float* gu, void* act_bf16, int M, int F, int zero_after, void* s
  * last_tok[rid[r]] = token, out_tok[out_idx[r]] = token. ws: 64 * R floats of
  * scratch; tickets: R ints, zero before the first call (left zero). zero_after:
  * clear the R logits rows after reading them (a red.add LM head accumulates into
- * them next). One launch. */
+ * them next). logits_out (nullable, test hook): row r's logits are also stored at
+ * logits_out[out_idx[r] * V]. One launch. */
 int ck_argmax_emit(float* logits, int R, int V, const int* rid, const long long* out_idx, int* last_tok,
-                   int* out_tok, float* ws, int* tickets, int zero_after, void* stream);
+                   int* out_tok, float* ws, int* tickets, int zero_after, float* logits_out, void* stream);
 
 /* KV handoff: copy n_blocks blocks src_pool[src_ids[i]] -> dst_pool[dst_ids[i]]
  * (block_bytes each; src may be a peer-mapped pointer — pull over NVLink). */

@@ -28,6 +28,13 @@ int cronus_engine_serve(void* engine, const char* cfg_text, int n, const int* id
                         const int* host_prompt, int* host_tokens, int flags, char** json_out,
                         char** events_out, char** csv_out, char** stats_out);
 
+/* Test hook: serve() (prompts synthesized on the device, no event log) that also
+ * returns the fp32 logits each generated token was sampled from, host_logits =
+ * [sum(output_len)][vocab] in host_tokens order. Co-located pairs only. */
+int cronus_engine_serve_logits(void* engine, const char* cfg_text, int n, const int* id, const double* arrival_ms,
+                               const int* input_len, const int* output_len, const char* trace_name, int* host_tokens,
+                               float* host_logits, char** json_out);
+
 /* Pre-synthesize the trace's prompt tokens on the device (see GpuEngine::stage). */
 int cronus_engine_stage(void* engine, const char* cfg_text, int n, const int* id, const double* arrival_ms,
                         const int* input_len, const int* output_len);

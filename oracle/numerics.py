@@ -2,13 +2,17 @@
 
 The reference (/root/reference) has no model arithmetic at all (SURVEY.md section 8(c):
 its GPU work is three linear cost formulas, proj/src/costmodel.cpp:9-15). Its paper ran
-vLLM 0.6.1.post2, which is not vendored. So this module is the numeric
-oracle and is **parity unpinned** against any upstream code: it restates the published
-LLaMA-3 / Qwen2 decoder (RMSNorm, rotate-half RoPE, GQA causal attention, SiLU-gated
-MLP, Qwen2 QKV bias, greedy argmax) in numpy fp32 over the exact bf16 weights the engine
-initialises on device, and the exact prompt tokens it synthesises.
+vLLM 0.6.1.post2, which is not vendored. This module restates the
+published LLaMA-3 / Qwen2 decoder (RMSNorm, rotate-half RoPE, GQA causal attention,
+SiLU-gated MLP, Qwen2 QKV bias, greedy argmax) in numpy fp32 over the exact bf16 weights
+the engine initialises on device, and the exact prompt tokens it synthesises.
 
-Bit-exact restatements (checked by tests/test_numerics_oracle.py and the GPU tests):
+Pinned against a published implementation: tests/test_numerics_oracle.py loads the same
+weights into Hugging Face LlamaForCausalLM / Qwen2ForCausalLM (tests/hf_ref.py) and
+requires max |d logit| <= 1e-4 in fp32 on the tiny presets (measured ~1e-5), plus split
+prefill == monolithic prefill and incremental decode == full-sequence forward.
+
+Bit-exact restatements (checked by the GPU tests, tests/test_kernels_gpu.py):
   * splitmix64 weight init      csrc/kernels/elementwise.cu init_uniform_kernel
   * prompt-token hash           csrc/kernels/elementwise.cu prompt_tokens_kernel
   * RoPE tables (fp64 -> fp32)  csrc/kernels/elementwise.cu rope_table_kernel
@@ -230,6 +234,25 @@ class Decoder:
 
     def logits(self, hidden):
         return hidden @ self.w.lm_head().T
+
+
+def teacher_forced_logits(w: Weights, prompt: np.ndarray, tokens: np.ndarray, split: int | None = None,
+                          mirror_bf16: bool = True) -> np.ndarray:
+    """Logits [len(tokens), vocab] each generated token is sampled from: the prompt as a
+    PPI prefix of `split` tokens plus the rest (the Cronus split), then the given tokens fed
+    back one at a time (teacher forcing)."""
+    dec = Decoder(w, mirror_bf16=mirror_bf16)
+    if split and 0 < split < len(prompt):
+        dec.forward(prompt[:split], 0)
+        h = dec.forward(prompt[split:], split)[-1:]
+    else:
+        h = dec.forward(prompt, 0)[-1:]
+    out = []
+    for i, tok in enumerate(tokens):
+        out.append(dec.logits(h)[0])
+        if i + 1 < len(tokens):
+            h = dec.forward(np.array([int(tok)]), len(prompt) + i)
+    return np.stack(out)
 
 
 def greedy_check(spec_name: str, prompt: np.ndarray, gpu_tokens: np.ndarray, tol: float, weights=None,

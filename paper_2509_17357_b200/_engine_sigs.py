@@ -18,6 +18,9 @@ def bind(L):
     L.cronus_engine_serve.restype = I
     L.cronus_engine_describe.argtypes = [V, I, vpp]
     L.cronus_engine_describe.restype = I
+    L.cronus_engine_serve_logits.argtypes = [V, ctypes.c_char_p, I, i32p, f64p, i32p, i32p, ctypes.c_char_p, i32p,
+                                             ctypes.POINTER(ctypes.c_float), ctypes.POINTER(V)]
+    L.cronus_engine_serve_logits.restype = I
     L.cronus_engine_stage.argtypes = [V, ctypes.c_char_p, I, i32p, f64p, i32p, i32p]
     L.cronus_engine_stage.restype = I
     L.cronus_engine_staged_prompts.argtypes = [V, i32p, ctypes.c_longlong]

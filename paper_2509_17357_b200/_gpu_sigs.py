@@ -21,7 +21,7 @@ CK = {
     "ck_attn_decode_tma": [V, V, LL, V, V, V, V, V, V, I, I, I, V, V, V, I, I, I, I, F, V, V],
     "ck_attn_prefill_pp": [V, I, V, LL, V, I, I, I, V, I, I, I, I, F, V],
     "ck_silu_mul": [V, V, I, I, I, V],
-    "ck_argmax_emit": [V, I, I, V, V, V, V, V, V, I, V],
+    "ck_argmax_emit": [V, I, I, V, V, V, V, V, V, I, V, V],
     "ck_kv_copy": [V, V, V, V, I, LL, V],
     "ck_copy_token": [V, LL, V, LL, V, LL, V],
     "ck_device_sms": [],

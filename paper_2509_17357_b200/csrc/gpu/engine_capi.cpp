@@ -47,10 +47,10 @@ int cronus_engine_create(const char* engine_options, void** engine_out) {
 
 void cronus_engine_destroy(void* engine) { delete static_cast<cronus::GpuEngine*>(engine); }
 
-int cronus_engine_serve(void* engine, const char* cfg_text, int n, const int* id, const double* arrival_ms,
-                        const int* input_len, const int* output_len, const char* trace_name, const int* host_prompt,
-                        int* host_tokens, int flags, char** json_out, char** events_out, char** csv_out,
-                        char** stats_out) {
+namespace {
+int serve(void* engine, const char* cfg_text, int n, const int* id, const double* arrival_ms, const int* input_len,
+          const int* output_len, const char* trace_name, const int* host_prompt, int* host_tokens, float* host_logits,
+          int flags, char** json_out, char** events_out, char** csv_out, char** stats_out) {
     const int want_events = flags & 1;
     return guard([&] {
         auto* eng = static_cast<cronus::GpuEngine*>(engine);
@@ -63,6 +63,7 @@ int cronus_engine_serve(void* engine, const char* cfg_text, int n, const int* id
         o.event_log = want_events ? &ev : nullptr;
         o.host_prompt = host_prompt;
         o.host_tokens = host_tokens;
+        o.host_logits = host_logits;
         o.stats_json = &stats;
         o.profile = (flags & 2) != 0;
         const cronus::RunReport rep = eng->run(cfg, t, o);
@@ -71,6 +72,22 @@ int cronus_engine_serve(void* engine, const char* cfg_text, int n, const int* id
         if (csv_out) *csv_out = dup(cronus::csv_row(rep));
         if (stats_out) *stats_out = dup(stats);
     });
+}
+}  // namespace
+
+int cronus_engine_serve(void* engine, const char* cfg_text, int n, const int* id, const double* arrival_ms,
+                        const int* input_len, const int* output_len, const char* trace_name, const int* host_prompt,
+                        int* host_tokens, int flags, char** json_out, char** events_out, char** csv_out,
+                        char** stats_out) {
+    return serve(engine, cfg_text, n, id, arrival_ms, input_len, output_len, trace_name, host_prompt, host_tokens,
+                 nullptr, flags, json_out, events_out, csv_out, stats_out);
+}
+
+int cronus_engine_serve_logits(void* engine, const char* cfg_text, int n, const int* id, const double* arrival_ms,
+                               const int* input_len, const int* output_len, const char* trace_name, int* host_tokens,
+                               float* host_logits, char** json_out) {
+    return serve(engine, cfg_text, n, id, arrival_ms, input_len, output_len, trace_name, nullptr, host_tokens,
+                 host_logits, 0, json_out, nullptr, nullptr, nullptr);
 }
 
 int cronus_engine_stage(void* engine, const char* cfg_text, int n, const int* id, const double* arrival_ms,

@@ -380,9 +380,19 @@ class PairExecutor : public sched::Executor {
         prefill_ev.assign(n, nullptr);
         xfer_ev.assign(n, nullptr);
         xfer_pending.assign(n, 0);
+        if (opts.host_logits) {
+            if (!E.colocated) throw std::invalid_argument("host_logits: co-located pairs only");
+            const size_t bytes = static_cast<size_t>(total_out) * E.spec.vocab * 4;
+            logits_buf.ensure(E.opt.cpi_device, bytes);
+            check_cuda(cudaMemset(logits_buf.p, 0, bytes), "memset logits sink");
+            E.cpi->set_logits_out(static_cast<float*>(logits_buf.p));
+            E.ppi->set_logits_out(static_cast<float*>(logits_buf.p));
+        }
     }
 
     ~PairExecutor() override {
+        E.cpi->set_logits_out(nullptr);
+        E.ppi->set_logits_out(nullptr);
         for (auto* v : {&prefill_ev, &xfer_ev})
             for (cudaEvent_t ev : *v)
                 if (ev) cudaEventDestroy(ev);
@@ -763,6 +773,11 @@ class PairExecutor : public sched::Executor {
                     if (opts.host_tokens[i] < 0) opts.host_tokens[i] = low[i];
             }
         }
+        if (opts.host_logits) {
+            check_cuda(cudaMemcpy(opts.host_logits, logits_buf.p, static_cast<size_t>(total_out) * E.spec.vocab * 4,
+                                  cudaMemcpyDeviceToHost),
+                       "logits D2H");
+        }
         E.cpi->collect_stats();
         E.ppi->collect_stats();
     }
@@ -809,6 +824,7 @@ class PairExecutor : public sched::Executor {
     const GpuRunOptions& opts;
     std::vector<long long> prompt_off, out_off;
     long long total_in = 0, total_out = 0;
+    DeviceBuf logits_buf;  // logits test hook (opts.host_logits)
     int* pinned_prompt = nullptr;
     gpu::Batch batch;
     std::vector<cudaEvent_t> prefill_ev, xfer_ev;

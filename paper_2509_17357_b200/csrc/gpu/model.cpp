@@ -685,7 +685,7 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
             gemm(w_.lm_head, hs_, logits_, nullptr, R, m.vocab, H, CK_EPI_F32, 1);
         mark(a);
         check_ck(ck_argmax_emit(logits_, R, m.vocab, D(o_s_rid), reinterpret_cast<const long long*>(D(o_s_out)),
-                                last_tok, out_tok, arg_ws_, arg_tickets_, 1, stream_),
+                                last_tok, out_tok, arg_ws_, arg_tickets_, 1, logits_out_, stream_),
                  "argmax");
         ++launches;
         done(a, &stat_other, 0, 0);
@@ -696,7 +696,7 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
     // (rows, attention work items, cluster size, stream): the graph_min_seen()-th time a shape
     // is seen the chain is captured into a CUDA graph (PDL edges kept) and replayed from then on — a
     // dependent kernel boundary costs ~1.3-1.5 us in a graph vs ~1.9-2.7 us on a stream.
-    const bool graphable = use_graphs() && !profile_ && fused_rope;
+    const bool graphable = use_graphs() && !profile_ && fused_rope && !logits_out_;
     if (graphable) {
         char key[256];
         std::snprintf(key, sizeof key, "%d/%d/%d/%d/%d/%p/%d/%p/%d/%p/%p/%p/%p/%p", M, R, n_dec, n_work,

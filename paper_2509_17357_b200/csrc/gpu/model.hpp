@@ -150,6 +150,9 @@ class Worker {
     int max_rows() const { return max_rows_; }
     cudaStream_t stream() const { return stream_; }
     void set_profiling(bool on) { profile_ = on; }
+    // Test hook: sampled rows' logits are also stored at logits_out[out_index * vocab]
+    // (device buffer; nullptr = off). Passes with it set are never graph-captured.
+    void set_logits_out(float* p) { logits_out_ = p; }
     // Switch the stream / persistent-grid cap later passes launch on (SM lending). The
     // caller orders the streams.
     void set_launch(cudaStream_t s, int max_ctas) {
@@ -193,6 +196,7 @@ class Worker {
     int* norm_tickets_ = nullptr;  // fused-RMSNorm m-tile tickets (self-resetting)
     float* arg_ws_ = nullptr;      // argmax slice winners [max_sample * 64]
     int* arg_tickets_ = nullptr;   // [max_sample], self-resetting
+    float* logits_out_ = nullptr;  // logits test hook (set_logits_out)
     int* meta_dev_ = nullptr;
     long long meta_cap_ = 0;
     // pinned staging ring for per-pass metadata

@@ -221,7 +221,7 @@ __device__ __forceinline__ void arg_better(float& bv, int& bi, float v, int i) {
 
 __global__ void argmax_emit_kernel(float* __restrict__ logits, int V, const int* rid, const long long* out_idx,
                                    int* last_tok, int* out_tok, float* __restrict__ pv, int* __restrict__ pi,
-                                   int* __restrict__ tickets, int zero_after) {
+                                   int* __restrict__ tickets, int zero_after, float* __restrict__ logits_out) {
     pdl_launch();
     pdl_wait();
     __shared__ float sb[32];
@@ -232,11 +232,13 @@ __global__ void argmax_emit_kernel(float* __restrict__ logits, int V, const int*
     const int lo = static_cast<int>(static_cast<long long>(c) * n4 / kArgChunks);
     const int hi = static_cast<int>(static_cast<long long>(c + 1) * n4 / kArgChunks);
     float4* row = reinterpret_cast<float4*>(logits + static_cast<size_t>(r) * V);
+    float4* keep = logits_out ? reinterpret_cast<float4*>(logits_out + static_cast<size_t>(out_idx[r]) * V) : nullptr;
     float best = -INFINITY;
     int bi = 0x7fffffff;
     for (int v = lo + threadIdx.x; v < hi; v += blockDim.x) {
         const float4 x = row[v];
         if (zero_after) row[v] = make_float4(0.f, 0.f, 0.f, 0.f);  // next red.add LM head starts from zero
+        if (keep) keep[v] = x;
         arg_better(best, bi, x.x, 4 * v);
         arg_better(best, bi, x.y, 4 * v + 1);
         arg_better(best, bi, x.z, 4 * v + 2);
@@ -392,13 +394,13 @@ int ck_silu_mul(float* gu, void* act, int M, int F, int zero_after, void* stream
 }
 
 int ck_argmax_emit(float* logits, int R, int V, const int* rid, const long long* out_idx, int* last_tok,
-                   int* out_tok, float* ws, int* tickets, int zero_after, void* stream) {
+                   int* out_tok, float* ws, int* tickets, int zero_after, float* logits_out, void* stream) {
     if (R <= 0) return 0;
     if (V % 4) return static_cast<int>(cudaErrorInvalidValue);
     float* pv = ws;
     int* pi = reinterpret_cast<int*>(ws + static_cast<size_t>(R) * kArgChunks);
     return launch_pdl(argmax_emit_kernel, dim3(R, kArgChunks), dim3(256), 0, S(stream), logits, V, rid, out_idx,
-                      last_tok, out_tok, pv, pi, tickets, zero_after);
+                      last_tok, out_tok, pv, pi, tickets, zero_after, logits_out);
 }
 
 int ck_kv_copy(const void* src_pool, const int* src_ids, void* dst_pool, const int* dst_ids, int n_blocks,

@@ -46,6 +46,23 @@ class GpuEngine:
         check(lib().cronus_engine_stage(self._h, cfg_text.encode(), len(ids), _p(ids, ctypes.c_int),
                                         _p(arr, ctypes.c_double), _p(ins, ctypes.c_int), _p(outs, ctypes.c_int)))
 
+    def serve_logits(self, cfg_text: str, trace: Trace, vocab: int) -> RunResult:
+        """serve() that also returns, per request, the fp32 logits [output_len, vocab] each
+        generated token was sampled from (test hook; co-located pairs)."""
+        ids, arr, ins, outs = trace.arrays()
+        toks = np.empty(int(outs.sum()), np.int32)
+        lg = np.empty((int(outs.sum()), vocab), np.float32)
+        j = ctypes.c_void_p()
+        check(lib().cronus_engine_serve_logits(
+            self._h, cfg_text.encode(), len(ids), _p(ids, ctypes.c_int), _p(arr, ctypes.c_double),
+            _p(ins, ctypes.c_int), _p(outs, ctypes.c_int), trace.name.encode(), _p(toks, ctypes.c_int),
+            _p(lg, ctypes.c_float), ctypes.byref(j)))
+        res = RunResult(take_string(j), "", "")
+        offs = np.concatenate([[0], np.cumsum(outs)])
+        res.extra["tokens"] = [toks[offs[i]:offs[i + 1]] for i in range(len(outs))]
+        res.extra["logits"] = [lg[offs[i]:offs[i + 1]] for i in range(len(outs))]
+        return res
+
     def prompts(self, cfg_text: str, trace: Trace) -> np.ndarray:
         """Host copy of the trace's prompt tokens (stages the trace first): the host
         buffers an end-to-end serve(host_prompt=...) starts from."""

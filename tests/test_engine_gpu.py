@@ -55,6 +55,44 @@ def check_tokens(trace, tokens, rids, model="tiny", splits=None):
     return total, exact
 
 
+# Stated logits tolerance through the Cronus split (tiny presets, logit std 4-6): the GPU's
+# fp32 logits of every generated token vs the bf16-storage-mirrored fp32 oracle,
+# teacher-forced on the GPU's own tokens. Remaining differences: fp32 summation order
+# (stream-K / tensor-core accumulation) and the bf16 roundings that order flips.
+TOL_LOGIT = 0.1
+
+
+@pytest.mark.parametrize("model,cfg_name", [("tiny", "a100_a10_llama8b"), ("tiny-qwen", "a100_a30_qwen7b")])
+def test_logits_through_cronus_split(model, cfg_name):
+    """Sampled-row logits (engine hook) of requests served through PPI partial prefill ->
+    handoff -> CPI chunks + decode, against the oracle; tokens are their argmax (first
+    sampled row: engine.cpp:493,502-507)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2509_17357_b200.serving import GpuEngine
+    spec = NUM.PRESETS[model]
+    cfg = load_cfg(cfg_name)
+    t = c1_trace().subset(np.arange(16))
+    eng = GpuEngine(model=model, clock="virtual")
+    res = eng.serve_logits(cfg, t, spec.vocab)
+    eng.close()
+    assert res.json == E.run(cfg, t).json
+    recs = json.loads(res.json)["records"]
+    w = NUM.Weights(spec)
+    worst, splits = 0.0, 0
+    for i in (0, 3, 6, 9, 12, 15):
+        toks, got = res.extra["tokens"][i], res.extra["logits"][i]
+        assert np.array_equal(got.argmax(-1), toks)  # each token is the argmax of its logits row
+        split = recs[i]["partial_prefill_len"]
+        splits += 0 < split < t.input_len[i]
+        prompt = NUM.prompt_tokens(99, int(t.ids[i]), int(t.input_len[i]), spec.vocab)
+        want = NUM.teacher_forced_logits(w, prompt, toks, split)
+        worst = max(worst, float(np.abs(got - want).max()))
+    print(f"{model}: max |d logit| GPU vs oracle = {worst:.4f} (tolerance {TOL_LOGIT})")
+    assert splits >= 3  # the check covers real PPI/CPI splits
+    assert worst <= TOL_LOGIT
+
+
 def test_virtual_clock_schedule_and_tokens(tiny_engine):
     cfg = load_cfg("a100_a10_llama8b")
     t = c1_trace()

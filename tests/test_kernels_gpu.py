@@ -248,9 +248,12 @@ def test_silu_mul_and_argmax(L):
     ws = torch.empty(64 * R, device="cuda")
     tickets = torch.zeros(R, dtype=torch.int32, device="cuda")
     keep = logits.clone()
-    ok(L.ck_argmax_emit(p(logits), R, V, p(rid), p(out_idx), p(last), p(out_tok), p(ws), p(tickets), 1, stream()))
+    sink = torch.zeros(20, V, device="cuda")  # logits test hook: rows land at out_idx
+    ok(L.ck_argmax_emit(p(logits), R, V, p(rid), p(out_idx), p(last), p(out_tok), p(ws), p(tickets), 1, p(sink),
+                        stream()))
     assert logits.abs().sum() == 0  # zero_after: cleared for the next red.add LM head
     logits = keep
+    assert torch.equal(sink[10:15], keep) and sink[:10].abs().sum() == 0
     assert tickets.abs().sum() == 0
     want = logits.argmax(-1).int()
     assert int(want[1]) == 77

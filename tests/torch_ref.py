@@ -78,8 +78,9 @@ def _rope(x, cs, sn):
 class TorchDecoder:
     """One request over a growing dense KV cache (oracle/numerics.Decoder on torch)."""
 
-    def __init__(self, w: TorchWeights, max_pos: int = 16384):
+    def __init__(self, w: TorchWeights, max_pos: int = 16384, mirror_bf16: bool = True):
         self.w, self.s = w, w.s
+        self._b = _b if mirror_bf16 else (lambda x: x)  # bf16 storage points of the engine, or fp32
         c, s = NUM.rope_tables(max_pos, self.s.rope_theta)
         self.cos, self.sin = torch.from_numpy(c).to(w.dev), torch.from_numpy(s).to(w.dev)
         self.k = [None] * self.s.layers
@@ -95,14 +96,14 @@ class TorchDecoder:
         cs, sn = self.cos[pos][:, None, :], self.sin[pos][:, None, :]
         for l in range(s.layers):
             L = self.w.layer(l)
-            h = _b(_rms(x, L["an"], s.rms_eps))
+            h = self._b(_rms(x, L["an"], s.rms_eps))
             qkv = h @ L["wqkv"].float().t()
             if L["bqkv"] is not None:
                 qkv = qkv + L["bqkv"].float()
             q = qkv[:, : s.n_heads * 128].view(n, s.n_heads, 128)
             k = qkv[:, s.n_heads * 128:(s.n_heads + s.n_kv_heads) * 128].view(n, s.n_kv_heads, 128)
             v = qkv[:, (s.n_heads + s.n_kv_heads) * 128:].view(n, s.n_kv_heads, 128)
-            q, k, v = _b(_rope(q, cs, sn)), _b(_rope(k, cs, sn)), _b(v)
+            q, k, v = self._b(_rope(q, cs, sn)), self._b(_rope(k, cs, sn)), self._b(v)
             self.k[l] = k if self.k[l] is None else torch.cat([self.k[l], k])
             self.v[l] = v if self.v[l] is None else torch.cat([self.v[l], v])
             K = self.k[l].repeat_interleave(G, 1)  # [T, nq, 128]
@@ -112,16 +113,33 @@ class TorchDecoder:
             mask = torch.arange(T, device=self.w.dev)[None, :] > pos[:, None]
             sc = sc.masked_fill(mask[None], float("-inf"))
             out = torch.einsum("hnt,thd->nhd", torch.softmax(sc, -1), V)
-            x = x + _b(out.reshape(n, -1)) @ L["wo"].float().t()
-            h = _b(_rms(x, L["fn"], s.rms_eps))
+            x = x + self._b(out.reshape(n, -1)) @ L["wo"].float().t()
+            h = self._b(_rms(x, L["fn"], s.rms_eps))
             gu = h @ L["wgu"].float().t()
             g, u = gu[:, 0::2], gu[:, 1::2]
-            x = x + _b(g * torch.sigmoid(g) * u) @ L["wd"].float().t()
-        return _b(_rms(x, self.w.final_norm(), s.rms_eps))
+            x = x + self._b(g * torch.sigmoid(g) * u) @ L["wd"].float().t()
+        return self._b(_rms(x, self.w.final_norm(), s.rms_eps))
 
     @torch.no_grad()
     def logits(self, hidden):
         return hidden @ self.w.lm_head().float().t()
+
+
+@torch.no_grad()
+def teacher_forced_logits(w: TorchWeights, prompt, tokens, split=None, mirror_bf16=True):
+    """[len(tokens), vocab] reference logits each generated token is sampled from (prompt as
+    a PPI prefix of `split` tokens + the rest, then the tokens fed back one at a time)."""
+    dec = TorchDecoder(w, max_pos=max(16384, len(prompt) + len(tokens) + 1), mirror_bf16=mirror_bf16)
+    cuts = sorted({0, len(prompt), *(range(0, len(prompt), 2048)), *([split] if split and 0 < split < len(prompt) else [])})
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        hid = dec.forward(prompt[a:b], a)
+    h = hid[-1:]
+    out = []
+    for i, tok in enumerate(tokens):
+        out.append(dec.logits(h)[0])
+        if i + 1 < len(tokens):
+            h = dec.forward(np.array([int(tok)]), len(prompt) + i)
+    return torch.stack(out)
 
 
 def greedy_check(w: TorchWeights, prompt, gpu_tokens, tol, split=None):

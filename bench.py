@@ -260,8 +260,8 @@ def decode_attn_probe(seqs=64, ctx=1024, layers=4, reps=40):
     off = torch.arange(seqs, dtype=torch.int32, device="cuda") * nblk
     rows = torch.arange(seqs, dtype=torch.int32, device="cuda")
     lens = torch.full((seqs,), ctx, dtype=torch.int32, device="cuda")
-    work = (torch.arange(seqs, dtype=torch.int32, device="cuda") << 16).contiguous()
-    item0 = torch.arange(seqs + 1, dtype=torch.int32, device="cuda")
+    work = ((torch.arange(seqs, dtype=torch.int32, device="cuda") << 16) | (1 << 8)).contiguous()  # 1 part each
+    item0 = torch.arange(seqs, dtype=torch.int32, device="cuda")
     q = torch.randn(seqs, nq * 128, device="cuda").bfloat16()
     out = torch.empty_like(q)
     ws = torch.empty(seqs * nq * 130, device="cuda")

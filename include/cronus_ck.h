@@ -117,14 +117,15 @@ int ck_qkv_rope_append(float* qkv, const void* bias, void* q_out, void* kv_pool,
 
 /* Decode attention over the paged pool for S single-token sequences, production path:
  * seq_row[S] (row of q/out), seq_len[S] (keys), seq_bt[S] (offset into bt),
- * seq_item0[S+1] (first work item of each sequence). ws: fp32 partials,
+ * seq_item0[S] (first work item of each sequence; its parts are contiguous). ws: fp32 partials,
  * n_work * nq * 130 floats. tickets: n_seq * nkv ints, zero before the first call
  * (the kernel leaves them zero). Output bf16 rows [*, nq*128]. One launch.
  * K/V rings are filled by TMA (2-D map over the pool viewed as
  * [pool_blocks * n_layers * 2 * nkv * 16 rows][128]) and each work item is served by a
  * thread-block CLUSTER of `cluster` CTAs (1..16) that split the item's blocks and merge
- * through distributed shared memory. work[i] = seq << 16 | part; a sequence's parts
- * (seq_item0) are evened out to ceil(nblocks / nparts) blocks; parts of one sequence
+ * through distributed shared memory. work[i] = seq << 16 | nparts << 8 | part (nparts <= 255);
+ * the grid runs the items in list order (heaviest first is the caller's choice: the engine's
+ * planner sorts them, LPT); a sequence's parts are evened out to ceil(nblocks / nparts) blocks; parts of one sequence
  * merge through ws / tickets (the last CTA of a (sequence, kv head) folds them). Partially
  * filled last blocks are read whole and masked, so never-written slots must hold finite
  * values (the engine zero-fills its pools). pool rows must be < 2^31. */

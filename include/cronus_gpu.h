@@ -50,6 +50,13 @@ int cronus_engine_time_pass(void* engine, const char* cfg_text, int worker, int 
  * on each worker stream and reports the SMs actually used. */
 int cronus_engine_describe(void* engine, int probe, char** json_out);
 
+/* The engine's decode-attention planner (gpu::Batch::plan_decode) on n context lengths for
+ * `slots` resident CTAs: writes the ck_attn_decode_tma work list (work_out: capacity
+ * work_cap entries) and seq_item0 (item0_out[n]); *n_work_out, *cluster_out. Host only
+ * (tools and tests drive the kernel with the production plan through it). */
+int cronus_plan_decode(const int* lens, int n, int n_kv_heads, int slots, int* work_out, int work_cap,
+                       int* item0_out, int* n_work_out, int* cluster_out);
+
 #ifdef __cplusplus
 }
 #endif

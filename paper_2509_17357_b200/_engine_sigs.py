@@ -27,3 +27,5 @@ def bind(L):
     L.cronus_engine_staged_prompts.restype = I
     L.cronus_engine_time_pass.argtypes = [V, ctypes.c_char_p, I, I, I, I, I, I, ctypes.POINTER(ctypes.c_double)]
     L.cronus_engine_time_pass.restype = I
+    L.cronus_plan_decode.argtypes = [i32p, I, I, I, i32p, I, i32p, i32p, i32p]
+    L.cronus_plan_decode.restype = I

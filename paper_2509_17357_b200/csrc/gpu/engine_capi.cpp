@@ -6,6 +6,7 @@
 #include <string>
 
 #include "cronus/gpu.hpp"
+#include "model.hpp"
 #include "cronus_gpu.h"
 
 namespace cronus {
@@ -114,6 +115,21 @@ int cronus_engine_time_pass(void* engine, const char* cfg_text, int worker, int 
 
 int cronus_engine_describe(void* engine, int probe, char** json_out) {
     return guard([&] { *json_out = dup(static_cast<cronus::GpuEngine*>(engine)->describe(probe != 0)); });
+}
+
+int cronus_plan_decode(const int* lens, int n, int n_kv_heads, int slots, int* work_out, int work_cap,
+                       int* item0_out, int* n_work_out, int* cluster_out) {
+    return guard([&] {
+        if (n < 1 || n_kv_heads < 1 || slots < 1) throw std::invalid_argument("plan_decode: bad arguments");
+        cronus::gpu::Batch b;
+        b.d_len.assign(lens, lens + n);
+        b.plan_decode(n_kv_heads, slots);
+        if (static_cast<int>(b.d_work.size()) > work_cap) throw std::invalid_argument("plan_decode: work_cap too small");
+        std::copy(b.d_work.begin(), b.d_work.end(), work_out);
+        std::copy(b.d_item0.begin(), b.d_item0.end(), item0_out);
+        *n_work_out = static_cast<int>(b.d_work.size());
+        *cluster_out = b.decode_cluster;
+    });
 }
 
 }  // extern "C"

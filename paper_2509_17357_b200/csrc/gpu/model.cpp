@@ -189,29 +189,74 @@ void Batch::add_prefill(int rid, long long pos0, long long len, const std::vecto
     }
 }
 
+// Predicted makespan (in block-streaming times of one CTA) of a decode launch whose
+// sequences are cut into parts of at most `cap` blocks: list scheduling of the parts,
+// heaviest first, on slots / (nkv * C) item slots; each CTA pays a fixed setup cost and
+// a part of a cut sequence the global merge.
+static double decode_makespan(const std::vector<int>& d_len, long long cap, int C, long long item_slots,
+                              std::vector<double>& heap) {
+    constexpr double kSetup = 6.0, kMerge = 4.0;  // blocks-equivalent (~0.5 us per block per CTA)
+    std::vector<double> work;
+    work.reserve(d_len.size() * 2);
+    for (int len : d_len) {
+        const long long nblk = (len + 15) / 16;
+        const long long parts = std::max<long long>(1, (nblk + cap - 1) / cap);
+        const double w = static_cast<double>((nblk + parts - 1) / parts) / C + kSetup + (parts > 1 ? kMerge : 0.0);
+        for (long long i = 0; i < parts; ++i) work.push_back(w);
+    }
+    std::sort(work.begin(), work.end(), std::greater<double>());
+    heap.assign(static_cast<size_t>(std::max<long long>(1, item_slots)), 0.0);  // min-heap of slot finish times
+    for (double w : work) {
+        std::pop_heap(heap.begin(), heap.end(), std::greater<double>());
+        heap.back() += w;
+        std::push_heap(heap.begin(), heap.end(), std::greater<double>());
+    }
+    return *std::max_element(heap.begin(), heap.end());
+}
+
 void Batch::plan_decode(int n_kv_heads, int slots) {
-    // One wave of `slots` resident CTAs: every (sequence, kv head) pair gets a cluster of
-    // C CTAs (C = power of two <= 16, as large as the wave allows while each CTA keeps
-    // >= 4 blocks, one per warp); a sequence more than ~2x longer than its fair share
-    // per cluster is cut into parts (merged through the global ticket path).
+    // Resident CTAs `slots`: every (sequence, kv head) pair gets a cluster of C CTAs (C =
+    // power of two <= 16, as large as one wave allows while each CTA keeps >= 4 blocks, one
+    // per warp). Sequences longer than `cap` blocks are cut into parts (merged through the
+    // global ticket path); cap is the candidate with the shortest predicted makespan
+    // (decode_makespan), and the work list runs the heaviest parts first (LPT): with the
+    // lognormal context lengths of a serve, one 8k-token sequence left whole (or started
+    // last) would otherwise hold the whole launch for 2-3x its fair time.
     const long long n = static_cast<long long>(d_len.size());
-    long long total = 0;
-    for (int len : d_len) total += (len + 15) / 16;
+    long long total = 0, longest = 0;
+    for (int len : d_len) {
+        total += (len + 15) / 16;
+        longest = std::max<long long>(longest, (len + 15) / 16);
+    }
     const long long pairs = n * n_kv_heads;
     int C = 1;
     while (C < 16 && pairs * C * 2 <= slots && total * n_kv_heads >= pairs * C * 2 * 4) C *= 2;
     const long long share = std::max<long long>(8, (total * n_kv_heads + slots - 1) / std::max(1, slots));
-    const long long cap = 2 * share * C;  // blocks one cluster may take before a sequence is cut
+    const long long item_slots = std::max<long long>(1, slots / (static_cast<long long>(n_kv_heads) * C));
+    const long long min_cap = std::max<long long>(8, (longest + 254) / 255);  // work[] holds <= 255 parts
+    long long cap = std::max(min_cap, 2 * share * C);
+    double best = decode_makespan(d_len, cap, C, item_slots, plan_heap_);
+    for (const double f : {1.5, 1.0, 0.75, 0.5}) {  // ties keep the larger cap (fewer merges)
+        const long long c = std::max(min_cap, static_cast<long long>(f * share * C));
+        const double t = decode_makespan(d_len, c, C, item_slots, plan_heap_);
+        if (t < best - 1e-9) best = t, cap = c;
+    }
     decode_cluster = C;
-    d_item0.clear();
-    d_work.clear();
+    std::vector<std::pair<long long, int>> order;  // (blocks per part, sequence)
+    std::vector<int> parts_of(d_len.size());
     for (size_t s = 0; s < d_len.size(); ++s) {
-        d_item0.push_back(static_cast<int>(d_work.size()));
         const long long nblk = (d_len[s] + 15) / 16;
         const long long parts = std::max<long long>(1, (nblk + cap - 1) / cap);
-        for (long long i = 0; i < parts; ++i) d_work.push_back(static_cast<int>(s << 16) | static_cast<int>(i));
+        parts_of[s] = static_cast<int>(parts);
+        order.emplace_back((nblk + parts - 1) / parts, static_cast<int>(s));
     }
-    d_item0.push_back(static_cast<int>(d_work.size()));
+    std::stable_sort(order.begin(), order.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    d_item0.assign(d_len.size(), 0);
+    d_work.clear();
+    for (const auto& [bpp, s] : order) {
+        d_item0[s] = static_cast<int>(d_work.size());
+        for (int i = 0; i < parts_of[s]; ++i) d_work.push_back((s << 16) | (parts_of[s] << 8) | i);
+    }
     blocks_per_split = static_cast<int>(cap);
 }
 

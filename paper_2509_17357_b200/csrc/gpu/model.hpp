@@ -106,6 +106,7 @@ struct Batch {
     int blocks_per_split = 16;
     // cluster size C >= 1 of the decode plan (plan_decode) for ck_attn_decode_tma
     int decode_cluster = 0;
+    std::vector<double> plan_heap_;  // plan_decode scratch
     // one prefill sequence: rows [p_row0, p_row0 + p_len) at positions [p_pos0, ...)
     int p_row0 = 0, p_len = 0, p_pos0 = 0, p_bt = 0;
     // flat block table (all sequences)

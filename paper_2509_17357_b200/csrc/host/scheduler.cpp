@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <limits>
 #include <ostream>
 #include <stdexcept>
@@ -38,6 +39,17 @@ namespace {
 constexpr double kTol = 1e-9;  // reference engine.cpp:21
 
 long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
+
+// Split ablation: CRONUS_FIXED_SPLIT=f in (0, 1] replaces the balancer's L_p by ceil(f * input)
+// (the free-block and saturation guards still apply). Unset (the default): the reference rule.
+double fixed_split_fraction() {
+    static const double f = [] {
+        const char* e = std::getenv("CRONUS_FIXED_SPLIT");
+        const double v = e ? std::atof(e) : 0.0;
+        return v > 0.0 && v <= 1.0 ? v : 0.0;
+    }();
+    return f;
+}
 
 enum class Kind : uint8_t { Arrival, SerialDone, IterDone, TransferDone, Notify };
 
@@ -329,7 +341,12 @@ bool Core::admit_cronus() {
                 snap.decode_ctx_sum += q.need + q.emitted;
             }
         }
-        const SplitDecision d = choose_split(cfg_.low_gpu, cfg_.high_gpu, snap, req_[rid].rq.input_len);
+        SplitDecision d = choose_split(cfg_.low_gpu, cfg_.high_gpu, snap, req_[rid].rq.input_len);
+        if (const double f = fixed_split_fraction(); f > 0.0 && !d.full_on_ppi && !d.cpi_saturated) {
+            // ablation (CRONUS_FIXED_SPLIT): a fixed fraction of the prompt instead of the balancer's L_p
+            const int n = req_[rid].rq.input_len;
+            d.partial_len = std::max(1, std::min(n, static_cast<int>(std::ceil(f * n))));
+        }
         req_[rid].lp = d.partial_len;
         req_[rid].full_on_ppi = d.full_on_ppi;
         ppi.waiting.push_back(rid);

@@ -72,13 +72,16 @@ __global__ void __launch_bounds__(128)
     __shared__ __align__(8) uint64_t bars[4][STAGES];
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const uint32_t C = cluster_size(), rank = cluster_rank();
-    const int item = blockIdx.x / C, kvh = blockIdx.y;
+    // item-major grid (all kv heads of work item 0, then item 1, ...): the planner lists the
+    // heaviest items first, so the block scheduler dispatches them first (LPT)
+    const int cid = blockIdx.x / C;
+    const int item = cid / a.nkv, kvh = cid % a.nkv;
     // per-pass metadata comes from host copies ordered before the pass: safe pre-wait
     const int wk = a.work[item];
-    const int s = wk >> 16, part = wk & 0xffff;
+    const int s = wk >> 16, part = wk & 0xff;
     const int len = a.seq_len[s];
     const int nblk = (len + kDBlk - 1) / kDBlk;
-    const int nparts = a.seq_item0[s + 1] - a.seq_item0[s];
+    const int nparts = (wk >> 8) & 0xff;
     const int bpp = (nblk + nparts - 1) / nparts;  // blocks per part (parts evened out)
     const int p0 = part * bpp, p1 = min(nblk, p0 + bpp);
     const int bpc = (p1 - p0 + static_cast<int>(C) - 1) / static_cast<int>(C);  // blocks per cluster CTA
@@ -251,7 +254,7 @@ __global__ void __launch_bounds__(128)
     __syncthreads();
     if (*s_last) {
         __threadfence();
-        const int i0 = a.seq_item0[s], i1 = a.seq_item0[s + 1];
+        const int i0 = a.seq_item0[s], i1 = i0 + nparts;
         for (int i = t; i < n_el; i += 128) {
             const int h = i / kDHD, d = i % kDHD;
             const int hq = kvh * G + h;
@@ -332,7 +335,7 @@ int launch_decode_tma(const CUtensorMap& tm, const DecodeAttnArgs& a, int n_work
     attr[1].val.clusterDim.y = 1;
     attr[1].val.clusterDim.z = 1;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(n_work * cluster, a.nkv);
+    cfg.gridDim = dim3(n_work * a.nkv * cluster, 1);
     cfg.blockDim = dim3(128);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;

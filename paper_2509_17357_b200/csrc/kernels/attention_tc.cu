@@ -290,21 +290,27 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                 for (int c = 0; c < 4; ++c) tmem_ld32(s_col + c * 32, sv[c]);
                 tmem_ld_wait();
                 const int key0 = j * kKT;
-                float mx = -INFINITY;
+                // row max over 128 columns as 8 independent chains (one warp per SM sub-partition
+                // per warpgroup: a single 128-long fmax chain would cost ~512 cycles of latency)
+                float pmx[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) pmx[e] = -INFINITY;
                 if (key0 + kKT - 1 <= warp_q0) {
 #pragma unroll
                     for (int c = 0; c < 4; ++c)
 #pragma unroll
-                        for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sv[c][e]));
+                        for (int e = 0; e < 32; ++e) pmx[e & 7] = fmaxf(pmx[e & 7], __uint_as_float(sv[c][e]));
                 } else {
 #pragma unroll
                     for (int c = 0; c < 4; ++c)
 #pragma unroll
                         for (int e = 0; e < 32; ++e) {
                             if (key0 + c * 32 + e > qpos) sv[c][e] = __float_as_uint(-INFINITY);
-                            mx = fmaxf(mx, __uint_as_float(sv[c][e]));
+                            pmx[e & 7] = fmaxf(pmx[e & 7], __uint_as_float(sv[c][e]));
                         }
                 }
+                float mx = fmaxf(fmaxf(fmaxf(pmx[0], pmx[1]), fmaxf(pmx[2], pmx[3])),
+                                 fmaxf(fmaxf(pmx[4], pmx[5]), fmaxf(pmx[6], pmx[7])));
                 mx *= p.scale_log2;
                 const bool need = __any_sync(0xffffffffu, mx > m_ref + kRescaleThreshold || m_ref == -INFINITY);
                 if (need) {
@@ -324,8 +330,11 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                         }
                     }
                 }
-                // P = exp2(S * scale - m) -> bf16 pairs over S's first 64 columns
-                float rs = 0.f;
+                // P = exp2(S * scale - m) -> bf16 pairs over S's first 64 columns; the row sum
+                // as 8 independent chains (see the max above)
+                float rsp[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) rsp[e] = 0.f;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     uint32_t pk[16];
@@ -337,7 +346,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                         for (int e = 0; e < 8; ++e) {
                             const float x = fmaf(__uint_as_float(sv[c][g * 8 + e]), p.scale_log2, -m_ref);
                             pv[e] = poly ? exp2_poly(x) : ex2_approx(x);
-                            rs += pv[e];
+                            rsp[e] += pv[e];
                         }
 #pragma unroll
                         for (int e = 0; e < 4; ++e) pk[g * 4 + e] = pack_bf16x2(pv[2 * e], pv[2 * e + 1]);
@@ -345,7 +354,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                     tmem_st16(s_col + c * 16, pk);
                 }
                 tmem_st_wait();
-                l_sum += rs;
+                l_sum += ((rsp[0] + rsp[1]) + (rsp[2] + rsp[3])) + ((rsp[4] + rsp[5]) + (rsp[6] + rsp[7]));
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&p_full[i]);

@@ -194,7 +194,7 @@ __device__ void dec_store(const DecodeAttnArgs& a, int item, int kvh, const floa
                           int bar_id) {
     int* s_last = reinterpret_cast<int*>(small + 128);
     const int s = a.work[item] >> 16;
-    const int nsplit = a.seq_item0[s + 1] - a.seq_item0[s];
+    const int nsplit = (a.work[item] >> 8) & 0xff;
     const int row = a.seq_row[s];
     const int nq = a.nq;
     const bool single = nsplit == 1;
@@ -226,7 +226,7 @@ __device__ void dec_store(const DecodeAttnArgs& a, int item, int kvh, const floa
     group_bar(bar_id);
     if (*s_last) {
         __threadfence();
-        const int i0 = a.seq_item0[s], i1 = a.seq_item0[s + 1];
+        const int i0 = a.seq_item0[s], i1 = i0 + nsplit;
         for (int i = t; i < G * kDHD; i += 128) {
             const int h = i / kDHD, d = i % kDHD;
             const int hq = kvh * G + h;

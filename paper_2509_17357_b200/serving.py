@@ -104,3 +104,16 @@ class GpuEngine:
             offs = np.concatenate([[0], np.cumsum(outs)])
             res.extra["tokens"] = [toks[offs[i]:offs[i + 1]] for i in range(len(outs))]
         return res
+
+
+def plan_decode(lens, n_kv_heads: int, slots: int):
+    """The engine's decode-attention plan (gpu::Batch::plan_decode) for these context lengths:
+    (work list, seq_item0, cluster) as ck_attn_decode_tma takes them."""
+    lens = np.ascontiguousarray(lens, np.int32)
+    cap = 4 * len(lens) + 64 + int(((lens + 15) // 16).sum() // 8) + 1
+    work = np.zeros(cap, np.int32)
+    item0 = np.zeros(len(lens), np.int32)
+    nw, cl = ctypes.c_int(), ctypes.c_int()
+    check(lib().cronus_plan_decode(_p(lens, ctypes.c_int), len(lens), n_kv_heads, slots, _p(work, ctypes.c_int), cap,
+                                   _p(item0, ctypes.c_int), ctypes.byref(nw), ctypes.byref(cl)))
+    return work[:nw.value].copy(), item0, cl.value

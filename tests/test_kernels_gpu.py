@@ -162,6 +162,22 @@ def attn_ref(q, k, v, qpos, scale):
     return torch.einsum("hnt,thd->nhd", s.softmax(-1), vv)
 
 
+def decode_work(lens, bps, reverse=False):
+    """Work list of ck_attn_decode_tma: parts of <= bps blocks per sequence, work[i] =
+    seq << 16 | nparts << 8 | part, parts of a sequence contiguous; reverse=True lists the
+    sequences last-first (the engine's planner orders them heaviest first), so item order
+    and sequence order differ."""
+    work, item0 = [], [0] * len(lens)
+    order = range(len(lens) - 1, -1, -1) if reverse else range(len(lens))
+    for s_i in order:
+        nblk = (lens[s_i] + 15) // 16
+        parts = (nblk + bps - 1) // bps
+        assert parts < 256
+        item0[s_i] = len(work)
+        work += [(s_i << 16) | (parts << 8) | sp for sp in range(parts)]
+    return work, item0
+
+
 @pytest.mark.parametrize("nq,nkv", [(2, 1), (32, 8), (28, 4), (4, 2)])
 def test_attn_decode(L, nq, nkv):
     gen = torch.Generator(device="cuda").manual_seed(nq)
@@ -179,13 +195,7 @@ def test_attn_decode(L, nq, nkv):
     # (blocks per part, cluster CTAs per part)
     cases = [(64, 1), (3, 1), (64, 2), (5, 4), (64, 8), (1000, 16)]
     for bps, cluster in cases:
-        work, item0 = [], []
-        for s_i, ln in enumerate(lens):
-            item0.append(len(work))
-            nblk = (ln + 15) // 16
-            for sp in range((nblk + bps - 1) // bps):
-                work.append((s_i << 16) | sp)
-        item0.append(len(work))
+        work, item0 = decode_work(lens, bps, reverse=cluster % 2 == 0)
         # keep every argument tensor alive across the call (the caching allocator
         # would otherwise hand the same block to the next temporary)
         t_len, t_off, t_item0, t_work = (torch.tensor(a, dtype=torch.int32, device="cuda")
@@ -310,11 +320,7 @@ def test_attn_decode_fused_rope(L, nq, nkv):
     pos = t_len - 1
     scale = 1 / math.sqrt(128)
     for cluster in (1, 4):
-        work, item0 = [], []
-        for s_i in range(S):
-            item0.append(len(work))
-            work.append(s_i << 16)
-        item0.append(len(work))
+        work, item0 = decode_work([1] * S, 1)
         t_item0 = torch.tensor(item0, dtype=torch.int32, device="cuda")
         t_work = torch.tensor(work, dtype=torch.int32, device="cuda")
         ws = torch.empty(len(work) * nq * 130, device="cuda")
@@ -379,12 +385,7 @@ def test_attn_long_context(L, nq, nkv):
     refs = [attn_ref(q[s].view(1, nq, 128), ks[s], vs[s], torch.tensor([ln - 1], device="cuda"), scale)
             for s, ln in enumerate(lens)]
     for bps, cluster in [(128, 8), (400, 16), (64, 1)]:
-        work, item0 = [], []
-        for s_i, ln in enumerate(lens):
-            item0.append(len(work))
-            for sp in range(((ln + 15) // 16 + bps - 1) // bps):
-                work.append((s_i << 16) | sp)
-        item0.append(len(work))
+        work, item0 = decode_work(lens, bps, reverse=cluster == 8)
         t_len, t_off, t_item0, t_work = (torch.tensor(a, dtype=torch.int32, device="cuda")
                                          for a in (lens, offs, item0, work))
         ws = torch.empty(len(work) * nq * 130, device="cuda")

@@ -146,12 +146,18 @@ int ck_attn_decode_tma(const void* q, const void* kv_pool, long long pool_blocks
  * query rows [q_row0, q_row0+q_len) of q (bf16 [q_rows_total, nq*128]) sit at positions
  * [pos0, pos0+q_len) and attend to keys [0, pos0+q_len) of the paged pool via bt.
  * Two 128-row query tiles per CTA with one softmax warpgroup each (ping-pong on the tensor
- * pipe) and P kept in TMEM as the A operand of the PV MMA. pool_blocks: blocks in the pool
- * (TMA bound). Stale slots of a sequence's last block are read (and masked): the pool must
- * hold finite values (the engine zero-fills it at allocation). */
+ * pipe) and P kept in TMEM as the A operand of the PV MMA; a tile packs the query heads of
+ * one kv head (4 heads x 32 tokens for GQA groups of 4 / 8, 2 x 64 for 2, 1 x 128 else), so
+ * each K/V tile is loaded once for all of them. When the (kv head, token block) units do not
+ * fill max_ctas CTAs, their key ranges are cut into balanced pieces whose partials merge
+ * through ws (ck_attn_prefill_ws_floats(max_ctas) floats) and tickets (max_ctas ints, zero,
+ * left zero); ws = NULL never splits. pool_blocks: blocks in the pool (TMA bound). Stale
+ * slots of a sequence's last block are read (and masked): the pool must hold finite values
+ * (the engine zero-fills it at allocation). */
 int ck_attn_prefill_pp(const void* q, int q_rows_total, const void* kv_pool, long long pool_blocks, const int* bt,
                        int q_row0, int q_len, int pos0, void* out, int nq, int nkv, int layer, int n_layers,
-                       float scale, void* stream);
+                       float scale, float* ws, int* tickets, int max_ctas, void* stream);
+long long ck_attn_prefill_ws_floats(int max_ctas);
 
 /* act[m, i] = silu(gu[m, 2i]) * gu[m, 2i+1]  (gate/up rows interleaved), fp32 in;
  * zero_after: clear gu after reading it. */

@@ -19,7 +19,7 @@ CK = {
     "ck_rmsnorm": [V, V, V, V, I, I, F, V, I, V],
     "ck_qkv_rope_append": [V, V, V, V, V, V, V, V, V, I, I, I, I, I, I, V],
     "ck_attn_decode_tma": [V, V, LL, V, V, V, V, V, V, I, I, I, V, V, V, I, I, I, I, F, V, V],
-    "ck_attn_prefill_pp": [V, I, V, LL, V, I, I, I, V, I, I, I, I, F, V],
+    "ck_attn_prefill_pp": [V, I, V, LL, V, I, I, I, V, I, I, I, I, F, V, V, I, V],
     "ck_silu_mul": [V, V, I, I, I, V],
     "ck_argmax_emit": [V, I, I, V, V, V, V, V, V, I, V, V],
     "ck_kv_copy": [V, V, V, V, I, LL, V],
@@ -37,6 +37,9 @@ def bind(L):
             continue
         fn.argtypes = args
         fn.restype = I
+    if hasattr(L, "ck_attn_prefill_ws_floats"):
+        L.ck_attn_prefill_ws_floats.argtypes = [I]
+        L.ck_attn_prefill_ws_floats.restype = LL
     try:
         from . import _engine_sigs
         _engine_sigs.bind(L)

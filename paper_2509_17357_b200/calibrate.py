@@ -65,7 +65,8 @@ def chunked_samples(eng, cfg_text, worker, budget, pos0s=(0, 1024, 2048, 3072), 
     return out
 
 
-def prefill_samples(eng, cfg_text, worker, lengths=(128, 512, 1024, 2048, 4096)):
+def prefill_samples(eng, cfg_text, worker, lengths=(64, 128, 256, 384, 512)):
+    """Serial prefills on `worker` (the CPI's rows are sized for its token budget: <= 512)."""
     return [(L, eng.time_pass(cfg_text, worker, chunk_len=L, reps=3)) for L in lengths]
 
 

@@ -379,6 +379,9 @@ Worker::Worker(const Weights& w, int max_rows, int max_sample, int max_blocks_pe
     check_cuda(cudaMalloc(&attn_ws_, attn_ws_floats_ * 4), "alloc attn ws");
     check_cuda(cudaMalloc(&attn_tickets_, R * m_.n_kv_heads * 4), "alloc attn tickets");
     check_cuda(cudaMemset(attn_tickets_, 0, R * m_.n_kv_heads * 4), "zero attn tickets");
+    check_cuda(cudaMalloc(&pf_ws_, static_cast<size_t>(ck_attn_prefill_ws_floats(kPfSlots)) * 4), "alloc prefill ws");
+    check_cuda(cudaMalloc(&pf_tickets_, kPfSlots * 4), "alloc prefill tickets");
+    check_cuda(cudaMemset(pf_tickets_, 0, kPfSlots * 4), "zero prefill tickets");
     const size_t n_tiles = static_cast<size_t>(std::max(2 * m_.ffn, m_.qkv_n()) / 128) * ((R + 31) / 32);
     check_cuda(cudaMalloc(&tile_tickets_, n_tiles * 4), "alloc tile tickets");
     check_cuda(cudaMemset(tile_tickets_, 0, n_tiles * 4), "zero tile tickets");
@@ -401,7 +404,8 @@ Worker::~Worker() {
     for (void* p : {static_cast<void*>(x_), h_, static_cast<void*>(qkv_), q_, attn_, static_cast<void*>(gu_), act_, hs_,
                     static_cast<void*>(logits_), static_cast<void*>(attn_ws_), static_cast<void*>(meta_dev_),
                     static_cast<void*>(attn_tickets_), static_cast<void*>(arg_ws_), static_cast<void*>(arg_tickets_),
-                    static_cast<void*>(tile_tickets_), static_cast<void*>(norm_tickets_)})
+                    static_cast<void*>(tile_tickets_), static_cast<void*>(norm_tickets_), static_cast<void*>(pf_ws_),
+                    static_cast<void*>(pf_tickets_)})
         if (p) cudaFree(p);
     for (int i = 0; i < kRing; ++i) {
         if (meta_host_[i]) cudaFreeHost(meta_host_[i]);
@@ -656,9 +660,10 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
         }
         if (b.p_len > 0) {
             mark(a);
-            check_ck(ck_attn_prefill_pp(
-                         q_, max_rows_, pool.base, pool.blocks, bt + b.p_bt, b.p_row0, b.p_len, b.p_pos0, attn_,
-                         m.n_heads, m.n_kv_heads, l, m.layers, scale, stream_),
+            const int pf_ctas = std::min(kPfSlots, max_ctas_ > 0 ? max_ctas_ : ck_device_sms());
+            check_ck(ck_attn_prefill_pp(q_, max_rows_, pool.base, pool.blocks, bt + b.p_bt, b.p_row0, b.p_len,
+                                        b.p_pos0, attn_, m.n_heads, m.n_kv_heads, l, m.layers, scale, pf_ws_,
+                                        pf_tickets_, pf_ctas, stream_),
                      "attn_prefill");
             ++launches;
             const double keys = static_cast<double>(b.p_len) * b.p_pos0 + 0.5 * b.p_len * (b.p_len + 1.0);

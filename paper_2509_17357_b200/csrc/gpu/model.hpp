@@ -189,6 +189,9 @@ class Worker {
     float* attn_ws_ = nullptr;
     long long attn_ws_floats_ = 0;
     int* attn_tickets_ = nullptr;  // split-merge tickets, [max_rows * n_kv_heads], self-resetting
+    float* pf_ws_ = nullptr;       // prefill attention piece partials (ck_attn_prefill_ws_floats(kPfSlots))
+    int* pf_tickets_ = nullptr;    // [kPfSlots], self-resetting
+    static constexpr int kPfSlots = 160;  // >= SMs of any partition (B200: 148)
     // Leading rows of the qkv / gu fp32 accumulators that may be non-zero (left by a
     // tensor-regime pass, which stores instead of red.adding); the weight-streaming
     // regime needs them zero and its consumers re-zero what they read.

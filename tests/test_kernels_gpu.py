@@ -215,8 +215,9 @@ def test_attn_decode(L, nq, nkv):
             assert torch.allclose(got, ref, rtol=2e-2, atol=2e-2), (bps, cluster, ln, (got - ref).abs().max().item())
 
 
-@pytest.mark.parametrize("nq,nkv", [(2, 1), (32, 8), (28, 4)])
-@pytest.mark.parametrize("pos0,qlen", [(0, 1), (0, 77), (0, 256), (300, 64), (1000, 212), (48, 512), (2000, 700)])
+@pytest.mark.parametrize("nq,nkv", [(2, 1), (32, 8), (28, 4), (4, 2), (32, 4)])
+@pytest.mark.parametrize("pos0,qlen", [(0, 1), (0, 77), (0, 256), (300, 64), (1000, 212), (48, 512), (2000, 700),
+                                       (1024, 448), (130, 33)])
 def test_attn_prefill(L, nq, nkv, pos0, qlen):
     gen = torch.Generator(device="cuda").manual_seed(pos0 + qlen + nq)
     layers, layer = 2, 0
@@ -228,13 +229,21 @@ def test_attn_prefill(L, nq, nkv, pos0, qlen):
     q = torch.randn(row0 + qlen + 2, nq * 128, device="cuda", generator=gen).bfloat16()
     out = torch.zeros_like(q)
     scale = 1 / math.sqrt(128)
-    ok(L.ck_attn_prefill_pp(p(q), q.shape[0], p(pool), pool.shape[0], p(tables[0]), row0, qlen, pos0, p(out), nq,
-                            nkv, layer, layers, scale, stream()))
     qpos = torch.arange(pos0, T, device="cuda")
     ref = attn_ref(q[row0:row0 + qlen].view(qlen, nq, 128), ks[0], vs[0], qpos, scale)
-    got = out[row0:row0 + qlen].float().view(qlen, nq, 128)
-    assert torch.allclose(got, ref, rtol=3e-2, atol=3e-2), (got - ref).abs().max().item()
-    assert out[:row0].abs().sum() == 0 and out[row0 + qlen:].abs().sum() == 0
+    # no workspace (never split); a full B200 (148 CTAs: splits when the units do not fill
+    # it); a small partition (37) and a tiny one (5) that force deep key splits
+    for max_ctas in (0, 148, 37, 5):
+        out.zero_()
+        ws = torch.empty(max(1, L.ck_attn_prefill_ws_floats(max_ctas)), device="cuda")
+        tickets = torch.zeros(max(1, max_ctas), dtype=torch.int32, device="cuda")
+        ok(L.ck_attn_prefill_pp(p(q), q.shape[0], p(pool), pool.shape[0], p(tables[0]), row0, qlen, pos0, p(out), nq,
+                                nkv, layer, layers, scale, p(ws) if max_ctas else None, p(tickets), max_ctas,
+                                stream()))
+        got = out[row0:row0 + qlen].float().view(qlen, nq, 128)
+        assert torch.allclose(got, ref, rtol=3e-2, atol=3e-2), (max_ctas, (got - ref).abs().max().item())
+        assert out[:row0].abs().sum() == 0 and out[row0 + qlen:].abs().sum() == 0
+        assert tickets.abs().sum() == 0  # self-resetting
 
 
 def test_silu_mul_and_argmax(L):
@@ -402,8 +411,12 @@ def test_attn_long_context(L, nq, nkv):
     pos0, qlen = 16384 - 512, 512
     q2 = torch.randn(qlen, nq * 128, device="cuda", generator=gen).bfloat16()
     out2 = torch.zeros_like(q2)
-    ok(L.ck_attn_prefill_pp(p(q2), q2.shape[0], p(pool), pool.shape[0], p(tables[0]), 0, qlen, pos0, p(out2), nq, nkv,
-                            layer, layers, scale, stream()))
     ref2 = attn_ref(q2.view(qlen, nq, 128), ks[0], vs[0], torch.arange(pos0, pos0 + qlen, device="cuda"), scale)
-    assert torch.allclose(out2.float().view(qlen, nq, 128), ref2, rtol=3e-2, atol=3e-2), \
-        (out2.float().view(qlen, nq, 128) - ref2).abs().max().item()
+    for max_ctas in (0, 108):  # unsplit, and split into balanced key pieces
+        ws2 = torch.empty(max(1, L.ck_attn_prefill_ws_floats(max_ctas)), device="cuda")
+        tk2 = torch.zeros(max(1, max_ctas), dtype=torch.int32, device="cuda")
+        out2.zero_()
+        ok(L.ck_attn_prefill_pp(p(q2), q2.shape[0], p(pool), pool.shape[0], p(tables[0]), 0, qlen, pos0, p(out2), nq,
+                                nkv, layer, layers, scale, p(ws2) if max_ctas else None, p(tk2), max_ctas, stream()))
+        assert torch.allclose(out2.float().view(qlen, nq, 128), ref2, rtol=3e-2, atol=3e-2), \
+            (max_ctas, (out2.float().view(qlen, nq, 128) - ref2).abs().max().item())

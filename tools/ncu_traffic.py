@@ -28,6 +28,12 @@ SHAPES = {
                                             2 * 1024 * 2 * L["F"] * L["H"], 2 * 1024 * L["H"] * L["F"]], "flops"),
     "ncu_prefill_attn_chunk": ("cpi.prefill_attn", [4 * 32 * 128 * sum(2048 + i + 1 for i in range(480))], "flops"),
     "ncu_prefill_attn_v2": ("cpi.prefill_attn", [4 * 32 * 128 * sum(2048 + i + 1 for i in range(480))], "flops"),
+    # round 2: the C2 serve's mixed pass (97 decoders x 1395 keys + a 415-token chunk at 1024) and a PPI prefill
+    "ncu_prefill_pp_mixed": ("cpi.prefill_attn", [4 * 32 * 128 * sum(1024 + i + 1 for i in range(415))], "flops"),
+    "ncu_decode_mixed": ("cpi.decode_attn", [97 * 1395 * L["KVTOK"]], "bytes"),
+    "ncu_gemm_tc_mixed": ("cpi.gemm_tc", [2 * 512 * L["Q"] * L["H"], 2 * 512 * L["H"] * L["NQ"],
+                                          2 * 512 * 2 * L["F"] * L["H"], 2 * 512 * L["H"] * L["F"]], "flops"),
+    "ncu_prefill_pp_ppi": ("ppi.prefill_attn", [4 * 32 * 128 * sum(i + 1 for i in range(512))], "flops"),
 }
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
@@ -73,7 +79,8 @@ for rep in sys.argv[1:]:
             ent.update(algorithmic_bytes=int(a), traffic_ratio=round(dram / a, 4),
                        achieved_gbs=round(a / d["gpu__time_duration.sum"] / 1e3, 1))
         elif a is not None:
-            ent.update(algorithmic_flops=int(a), achieved_tflops=round(a / d["gpu__time_duration.sum"] / 1e6, 1))
+            ent.update(algorithmic_flops=int(a), achieved_tflops=round(a / d["gpu__time_duration.sum"] / 1e6, 1),
+                       dram_bytes_per_launch=int(dram))
         launches.append(ent)
     alg_b = sum(e.get("algorithmic_bytes", 0) for e in launches)
     dram_b = sum(e["dram_bytes"] for e in launches)

@@ -25,6 +25,7 @@ ap.add_argument("--reps", type=int, default=50)
 ap.add_argument("--nq", type=int, default=32)
 ap.add_argument("--nkv", type=int, default=8)
 ap.add_argument("--layers", type=int, default=2)
+ap.add_argument("--ctas", type=int, default=0, help="partition CTAs for key splitting (0: the device's SMs; -1: never split)")
 a = ap.parse_args()
 
 L = lib()
@@ -42,10 +43,13 @@ for shape in a.shapes.split(","):
     bt = torch.randperm(nblk, device="cuda").int()
     q = torch.randn(q_len, a.nq * 128, device="cuda").bfloat16()
     out = torch.empty_like(q)
+    ctas = torch.cuda.get_device_properties(0).multi_processor_count if a.ctas == 0 else max(a.ctas, 0)
+    ws = torch.empty(max(1, L.ck_attn_prefill_ws_floats(ctas)), device="cuda")
+    tickets = torch.zeros(max(1, ctas), dtype=torch.int32, device="cuda")
 
     def launch():
         rc = L.ck_attn_prefill_pp(P(q), q_len, P(pool), pool.shape[0], P(bt), 0, q_len, pos0, P(out), a.nq, a.nkv, 0,
-                                  a.layers, 1 / math.sqrt(128), st)
+                                  a.layers, 1 / math.sqrt(128), P(ws) if ctas else None, P(tickets), ctas, st)
         assert rc == 0, rc
 
     for _ in range(5):
@@ -60,7 +64,7 @@ for shape in a.shapes.split(","):
     us = e0.elapsed_time(e1) * 1e3 / a.reps
     keys = q_len * pos0 + q_len * (q_len + 1) / 2
     flops = 4.0 * a.nq * 128 * keys
-    print(json.dumps({"q_len": q_len, "pos0": pos0, "us": round(us, 2), "TFLOPs": round(flops / us / 1e6, 1),
+    print(json.dumps({"ctas": ctas, "q_len": q_len, "pos0": pos0, "us": round(us, 2), "TFLOPs": round(flops / us / 1e6, 1),
                       "frac_peak": round(flops / us / 1e6 / peak, 4)}), flush=True)
     del pool
     torch.cuda.empty_cache()

@@ -21,6 +21,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <vector>
 #include <mutex>
 #include <cstdio>
 #include <string>
@@ -33,24 +35,27 @@ namespace {
 
 using namespace ck;
 
-constexpr int kQ = 128;       // query rows per CTA
-constexpr int kKT = 128;      // keys per tile
-constexpr int kHalf = 16384;  // one 128-row x 64-col bf16 swizzled region
-constexpr int kTileBytes = 2 * kHalf;
+constexpr int kKT = 64;          // keys per K/V sub-tile (one S buffer)
+constexpr int kQHalf = 16384;    // one 128-row x 64-col bf16 swizzled region (a Q tile half)
+constexpr int kQTileBytes = 2 * kQHalf;
+constexpr int kKVHalf = kKT * 128;  // one 64-key x 64-dim half of a K/V sub-tile
+constexpr int kKVTileBytes = 2 * kKVHalf;
+constexpr int kStages = 5;          // K and V ring depth (sub-tiles)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
 
 __device__ __forceinline__ uint64_t sdesc_mn_sw128(uint32_t addr) {
-    // MN-major, 128B swizzle: LBO = 16 KiB between the two 64-element MN halves,
-    // SBO = 1 KiB between 8-row (K) groups.
-    return (static_cast<uint64_t>((addr >> 4) & 0x3FFFu)) | (static_cast<uint64_t>(kHalf >> 4) << 16) |
+    // MN-major, 128B swizzle: LBO = one sub-tile half (8 KiB) between the two 64-element MN
+    // (dim) halves, SBO = 1 KiB between 8-row (key) groups.
+    return (static_cast<uint64_t>((addr >> 4) & 0x3FFFu)) | (static_cast<uint64_t>(kKVHalf >> 4) << 16) |
            (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
            (static_cast<uint64_t>(2) << 61);
 }
 
-__host__ __device__ constexpr uint32_t idesc_attn(bool b_mn_major) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) | (static_cast<uint32_t>(128 >> 3) << 17) |
+// kind::f16 instruction descriptor, bf16 A/B, fp32 D, M = 128, N = n, A K-major
+__host__ __device__ constexpr uint32_t idesc_attn(bool b_mn_major, int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) | (static_cast<uint32_t>(n >> 3) << 17) |
            (static_cast<uint32_t>(128 >> 4) << 24);
 }
 
@@ -93,15 +98,19 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // ============================================================ ping-pong kernel
-// Two 128-row query tiles per CTA, one softmax warpgroup each, sharing the K/V rings. P never
-// leaves the tensor memory: each softmax warpgroup writes its bf16 P over the first 64 columns
-// of its own S tile (tcgen05.st) and the PV MMA takes A straight from TMEM. The MMA warp
-// interleaves
-//   PV_0(j), S_0(j+1), PV_1(j), S_1(j+1)
-// so while one warpgroup exponentiates, the tensor pipe works for the other. tcgen05 MMAs
-// execute in issue order, so S_i(j+1) (same TMEM as P_i(j)) follows PV_i(j), and "S_i(j) done"
-// implies "PV_i(j-1) done": the O rescale needs no extra barrier.
-// TMEM: S_0 | S_1 | O_0 | O_1 (128 columns each). smem: Q_0, Q_1, K[2], V[2] = 192 KB.
+// Two 128-row query tiles per CTA, one softmax warpgroup each, sharing the K/V rings. Keys go
+// in 64-key sub-tiles and every tile has TWO S buffers in the tensor memory, so the MMA warp
+// computes S_i(k+1) while warpgroup i exponentiates S_i(k): the softmax never waits for its
+// next scores, and the tensor pipe interleaves the two tiles' PV / S MMAs:
+//   PV_0(k), S_0(k+2), PV_1(k), S_1(k+2)
+// P never leaves the tensor memory: warpgroup i writes bf16 P over the first 32 columns of the
+// S buffer it read (tcgen05.st) and the PV MMA takes A straight from TMEM. MMAs execute in
+// issue order, so S_i(k+2) (same buffer as P_i(k)) follows PV_i(k). The lazy O rescale (rare:
+// only when a row max grows by more than 2^8) first waits for PV_i(k-1): S_i(k+1), issued right
+// after it, retiring says so (one commit per MMA group is all the issue loop can afford: each
+// tcgen05.commit costs the issuing thread ~100+ cycles).
+// TMEM: S_0a | S_0b | S_1a | S_1b (64 columns each) | O_0 | O_1 (128 each) = 512 columns.
+// smem: Q_0, Q_1 (32 KB each), K and V rings of kStages 16-KB sub-tiles, the block ids.
 //
 // GQA packing: a 128-row tile holds HT query heads x TT = 128/HT tokens of ONE kv head
 // (head-major: rows [g*TT, (g+1)*TT) are head g), so a CTA's two tiles cover 2*TT tokens of
@@ -109,22 +118,23 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 // Qwen2 (G = 7). A unit = (kv head, head subgroup, token block of 2*TT tokens).
 //
 // Balanced key split: when the units do not fill the partition (a 448-token chunk is 56 units
-// for 108 SMs), each unit's key tiles are cut into pieces of at most steps_cap tiles (the
+// for 108 SMs), each unit's key sub-tiles are cut into pieces of at most steps_cap (the
 // smallest cap whose piece count fits one wave, chosen on the host). A piece's unnormalised O
 // (fp32, coalesced [tile][dim/4][row] float4 layout) and per-row (max, sum) go to ws; the last
 // piece of a unit to finish (self-resetting ticket) folds the others into its own TMEM
 // accumulator and writes the bf16 rows. Units run heaviest first (token blocks descending).
 //
-// PDL: K/V tiles wholly below pos0 were written by earlier passes (a pass starts with a
-// stream-ordered metadata copy), so the producer requests up to two of them before
+// PDL: K/V wholly below pos0 was written by earlier passes (a pass starts with a
+// stream-ordered metadata copy), so the producer requests those sub-tiles before
 // griddepcontrol.wait; Q and the chunk's own keys only after it.
 constexpr int kPPOffQ = 0;
-constexpr int kPPOffK = kPPOffQ + 2 * kTileBytes;
-constexpr int kPPOffV = kPPOffK + 2 * kTileBytes;
-constexpr int kPPOffTab = kPPOffV + 2 * kTileBytes;  // the piece's block ids (first kPPTabMax)
-constexpr int kPPTabMax = 2048;                      // 256 key tiles = 32k keys
+constexpr int kPPOffK = kPPOffQ + 2 * kQTileBytes;
+constexpr int kPPOffV = kPPOffK + kStages * kKVTileBytes;
+constexpr int kPPOffTab = kPPOffV + kStages * kKVTileBytes;  // the piece's block ids (first kPPTabMax)
+constexpr int kPPTabMax = 256;                               // 64 sub-tiles = 4k keys (then from global)
 constexpr int kPPOffBar = kPPOffTab + kPPTabMax * 4;
-constexpr int kPPSmemBytes = kPPOffBar + 256 + 1024;
+constexpr int kPPSmemBytes = kPPOffBar + 512 + 1024;  // barriers (36 x 8 B) + alignment slack
+static_assert(kPPSmemBytes <= 232448, "smem budget");
 constexpr int kPPThreads = 320;  // producer, MMA, 2 x 4 softmax warps
 constexpr int kPfWsO = 2 * 32 * 128 * 4;  // floats of one piece's partial O: [tile][dim/4][row] float4
 constexpr int kPfWsFloats = kPfWsO + 2 * 128 * 2;  // + (max, sum) per tile row
@@ -136,10 +146,17 @@ struct PfParams {
     __nv_bfloat16* out;
     const int* table;
     int n_tb;       // token blocks of 2*TT tokens
-    int steps_cap;  // key tiles per piece at most
+    int steps_cap;  // key sub-tiles per piece at most
     float* ws;      // piece partials [grid][kPfWsFloats]
     int* tickets;   // [grid], zero, self-resetting
+    long long* probe;  // dev (CRONUS_PF_PROBE=1): per-CTA clock64 stamps [grid][128], else null
+    int ablate;        // dev (CRONUS_PF_ABLATE): bit 0 / 2 = no V / K loads, bit 1 = no exp (P = S); 0 in production
 };
+
+// dev probe: clock64 stamp `slot` of this CTA (pipeline events; see launch_prefill)
+__device__ __forceinline__ void pf_stamp(const PfParams& p, int slot) {
+    if (p.probe != nullptr && slot < 128) p.probe[blockIdx.x * 128 + slot] = clock64();
+}
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
     asm volatile(
@@ -163,6 +180,66 @@ __device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint
 }
 __device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
+// tcgen05 issue from a whole, convergent warp: one elected lane issues. With every operand
+// computed warp-uniformly the compiler keeps them in uniform registers; issuing from inside
+// `if (lane == 0)` instead wraps every MMA in an ELECT / R2UR.BROADCAST / BRA.U.ANY loop
+// (~100 cycles per instruction, more than a 128x64x16 MMA takes).
+__device__ __forceinline__ void mma_ss_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, e;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_ts_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, e;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void expect_tx_warp(uint64_t* bar, uint32_t bytes) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(bytes)
+        : "memory");
+}
+__device__ __forceinline__ void tma_2d_warp(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
+                                            uint64_t policy) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
+        "%4}], [%2], %5;\n"
+        "}\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void commit_warp(uint64_t* bar) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+        "}\n" ::"r"(smem_u32(bar))
+        : "memory");
+}
+
 // Key tiles of token block tb (its second tile's last valid token).
 template <int HT>
 __host__ __device__ __forceinline__ int pf_steps(int q_len, int pos0, int tb) {
@@ -176,21 +253,24 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     attn_prefill_pp_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
                            PfParams p) {
     constexpr int TT = 128 / HT;
+    constexpr int BPT = kKT / 16;  // 16-token pool blocks per sub-tile
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + kPPOffBar);
-    uint64_t* q_full = bar + 0;    // [2] per query tile
-    uint64_t* k_full = bar + 2;    // [2] per stage
-    uint64_t* k_empty = bar + 4;   // [2]
-    uint64_t* v_full = bar + 6;    // [2]
-    uint64_t* v_empty = bar + 8;   // [2]
-    uint64_t* s_full = bar + 10;   // [2] per query tile
-    uint64_t* p_full = bar + 12;   // [2] per query tile (4 warp arrivals)
-    uint64_t* o_done = bar + 14;   // [2] per query tile
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
-    int* s_last = reinterpret_cast<int*>(bar + 17);
+    uint64_t* q_full = bar + 0;                // [2] per query tile
+    uint64_t* s_full = bar + 2;                // [2 tiles][2 buffers]
+    uint64_t* p_full = bar + 6;                // [2 tiles][2 buffers] (4 warp arrivals)
+    uint64_t* pv_done = bar + 10;              // [2] per tile, one phase per PV
+    uint64_t* o_done = bar + 12;               // [2] per tile
+    uint64_t* k_full = bar + 14;               // [kStages]
+    uint64_t* k_empty = k_full + kStages;      // [kStages]
+    uint64_t* v_full = k_empty + kStages;      // [kStages]
+    uint64_t* v_empty = v_full + kStages;      // [kStages]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_empty + kStages);
+    int* s_last = reinterpret_cast<int*>(v_empty + kStages + 1);
 
     const int warp = warp_id(), lane = lane_id();
+    if (threadIdx.x == 0) pf_stamp(p, 0);
     // ---- which piece of which unit (metadata only: safe before griddepcontrol.wait)
     const int G = p.nq / p.nkv, NS = G / HT, per_tb = p.nkv * NS;
     int b = blockIdx.x, tb = p.n_tb - 1, pieces = 1, n_steps = 1;
@@ -222,13 +302,18 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         tma_prefetch_desc(&tmKV);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&q_full[i], 1);
-            mbar_init(&k_full[i], 1);
-            mbar_init(&k_empty[i], 1);
-            mbar_init(&v_full[i], 1);
-            mbar_init(&v_empty[i], 1);
-            mbar_init(&s_full[i], 1);
-            mbar_init(&p_full[i], 4);
+            mbar_init(&pv_done[i], 1);
             mbar_init(&o_done[i], 1);
+            for (int bb = 0; bb < 2; ++bb) {
+                mbar_init(&s_full[i * 2 + bb], 1);
+                mbar_init(&p_full[i * 2 + bb], 4);
+            }
+        }
+        for (int st = 0; st < kStages; ++st) {
+            mbar_init(&k_full[st], 1);
+            mbar_init(&k_empty[st], 1);
+            mbar_init(&v_full[st], 1);
+            mbar_init(&v_empty[st], 1);
         }
         fence_mbar_init();
     }
@@ -237,6 +322,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     pdl_launch();
+    if (threadIdx.x == 0) pf_stamp(p, 1);
 
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
@@ -245,104 +331,135 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         // table from global pays one dependent L2 round trip per 16-token block.
         const int n_tab = (p.pos0 + min(p.q_len, (tb + 1) * 2 * TT) + 15) / 16;
         int* tab = reinterpret_cast<int*>(sm + kPPOffTab);
-        const int t0 = j0 * (kKT / 16), n_stage = min(jmax * (kKT / 16), kPPTabMax);
+        const int t0 = j0 * BPT, n_stage = min(jmax * BPT, kPPTabMax);
         for (int x = lane; x < n_stage; x += 32) {
             const int ti = t0 + x;
             tab[x] = p.table[ti < n_tab ? ti : 0];  // past the end: any finite block (masked)
         }
         __syncwarp();
-        if (lane == 0) {
+        {  // whole warp, convergent: one elected lane issues (see mma_ss_warp)
             const uint64_t keep = policy_evict_last();
-            auto load_kv = [&](int jj) {
-                const int s = jj & 1;
-                int rows[kKT / 16];
-#pragma unroll
-                for (int bb = 0; bb < kKT / 16; ++bb) {
-                    const int x = jj * (kKT / 16) + bb, ti = t0 + x;
+            auto row_of = [&](int k) {  // lane bb < BPT: pool row of sub-tile k's block bb
+                int my_row = 0;
+                if (lane < BPT) {
+                    const int x = k * BPT + lane, ti = t0 + x;
                     const int id = x < kPPTabMax ? tab[x] : p.table[ti < n_tab ? ti : 0];
-                    rows[bb] = ((id * p.n_layers + p.layer) * 2 + 0) * p.nkv * 16 + kvh * 16;
+                    my_row = ((id * p.n_layers + p.layer) * 2 + 0) * p.nkv * 16 + kvh * 16;
                 }
-                mbar_wait(&k_empty[s], ((jj >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&k_full[s], kTileBytes);
-                uint8_t* K = sm + kPPOffK + s * kTileBytes;
-#pragma unroll
-                for (int bb = 0; bb < kKT / 16; ++bb) {
-                    tma_load_2d_hint(K + bb * 2048, &tmKV, &k_full[s], 0, rows[bb], keep);
-                    tma_load_2d_hint(K + kHalf + bb * 2048, &tmKV, &k_full[s], 64, rows[bb], keep);
+                return my_row;
+            };
+            auto load_k = [&](int k) {
+                const int st = k % kStages;
+                const int my_row = row_of(k);
+                mbar_wait(&k_empty[st], ((k / kStages) & 1) ^ 1);
+                if (k < 16 && lane == 0) pf_stamp(p, 88 + k);
+                uint8_t* K = sm + kPPOffK + st * kKVTileBytes;
+                if (p.ablate & 4) {  // dev ablation: K = whatever the stage holds
+                    if (lane == 0) mbar_arrive(&k_full[st]);
+                    return;
                 }
-                mbar_wait(&v_empty[s], ((jj >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&v_full[s], kTileBytes);
-                uint8_t* V = sm + kPPOffV + s * kTileBytes;
+                expect_tx_warp(&k_full[st], kKVTileBytes);
 #pragma unroll
-                for (int bb = 0; bb < kKT / 16; ++bb) {
-                    tma_load_2d_hint(V + bb * 2048, &tmKV, &v_full[s], 0, rows[bb] + p.nkv * 16, keep);
-                    tma_load_2d_hint(V + kHalf + bb * 2048, &tmKV, &v_full[s], 64, rows[bb] + p.nkv * 16, keep);
+                for (int bb = 0; bb < BPT; ++bb) {
+                    const int r = __shfl_sync(0xffffffffu, my_row, bb);
+                    tma_2d_warp(K + bb * 2048, &tmKV, &k_full[st], 0, r, keep);
+                    tma_2d_warp(K + kKVHalf + bb * 2048, &tmKV, &k_full[st], 64, r, keep);
                 }
             };
-            int jj = 0;
-            while (jj < 2 && jj < jmax && (j0 + jj + 1) * kKT <= p.pos0) load_kv(jj++);  // prefix: pre-wait
+            auto load_v = [&](int k) {
+                const int st = k % kStages;
+                const int my_row = row_of(k);
+                mbar_wait(&v_empty[st], ((k / kStages) & 1) ^ 1);
+                if (k < 16 && lane == 0) pf_stamp(p, 104 + k);
+                if (p.ablate & 1) {  // dev ablation: V = whatever the stage holds
+                    if (lane == 0) mbar_arrive(&v_full[st]);
+                    return;
+                }
+                expect_tx_warp(&v_full[st], kKVTileBytes);
+                uint8_t* V = sm + kPPOffV + st * kKVTileBytes;
+#pragma unroll
+                for (int bb = 0; bb < BPT; ++bb) {
+                    const int r = __shfl_sync(0xffffffffu, my_row, bb) + p.nkv * 16;
+                    tma_2d_warp(V + bb * 2048, &tmKV, &v_full[st], 0, r, keep);
+                    tma_2d_warp(V + kKVHalf + bb * 2048, &tmKV, &v_full[st], 64, r, keep);
+                }
+            };
+            // Issue order = arrival order (the TMA unit serves requests in order): the first
+            // two K sub-tiles (if wholly prefix: before griddepcontrol.wait), then Q, then V(0),
+            // V(1) and the rest in step order; Q queued behind several stages of K/V arrives
+            // microseconds late and holds the first S MMA.
+            int pre = 0;
+            while (pre < 2 && pre < jmax && (j0 + pre + 1) * kKT <= p.pos0) load_k(pre++);
             pdl_wait();
             for (int i = 0; i < n_qt; ++i) {
-                mbar_arrive_expect_tx(&q_full[i], kTileBytes);
-                uint8_t* Q = sm + kPPOffQ + i * kTileBytes;
+                expect_tx_warp(&q_full[i], kQTileBytes);
+                uint8_t* Q = sm + kPPOffQ + i * kQTileBytes;
                 const int qrow = p.q_row0 + t_base[i];
 #pragma unroll
                 for (int g = 0; g < HT; ++g) {
-                    tma_load_2d(Q + g * TT * 128, &tmQ, &q_full[i], (h_base + g) * 128, qrow);
-                    tma_load_2d(Q + kHalf + g * TT * 128, &tmQ, &q_full[i], (h_base + g) * 128 + 64, qrow);
+                    tma_2d_warp(Q + g * TT * 128, &tmQ, &q_full[i], (h_base + g) * 128, qrow, keep);
+                    tma_2d_warp(Q + kQHalf + g * TT * 128, &tmQ, &q_full[i], (h_base + g) * 128 + 64, qrow, keep);
                 }
             }
-            for (; jj < jmax; ++jj) load_kv(jj);
-        } else {
-            pdl_wait();
+            for (int k = 0; k < jmax; ++k) {
+                if (k >= pre) load_k(k);
+                load_v(k);
+            }
         }
     } else if (warp == 1) {
         pdl_wait();
-        // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t id_s = idesc_attn(false), id_o = idesc_attn(true);
+        // ------------------------------------------------------------ MMA issuer (whole warp)
+        {
+            const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);  // provably warp-uniform
+            constexpr uint32_t id_s = idesc_attn(false, kKT), id_o = idesc_attn(true, 128);
             for (int i = 0; i < n_qt; ++i) mbar_wait(&q_full[i], 0);
-            auto issue_s = [&](int i, int jj) {  // S_i(j) = Q_i K(j)^T -> TMEM cols [128 i, +128)
-                const uint32_t q0 = smem_u32(sm + kPPOffQ + i * kTileBytes);
-                const uint32_t k0 = smem_u32(sm + kPPOffK + (jj & 1) * kTileBytes);
+            if (lane == 0) pf_stamp(p, 2);
+            auto issue_s = [&](int i, int k) {  // S_i(k) = Q_i K(k)^T -> S buffer (i, k & 1)
+                const uint32_t q0 = smem_u32(sm + kPPOffQ + i * kQTileBytes);
+                const uint32_t k0 = smem_u32(sm + kPPOffK + (k % kStages) * kKVTileBytes);
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
-                    const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
-                    tc_mma_bf16(tmem + i * 128, sdesc_sw128(q0 + off), sdesc_sw128(k0 + off), id_s, kk > 0);
+                    mma_ss_warp(tm + i * 128 + (k & 1) * 64,
+                                sdesc_sw128(q0 + (kk >> 2) * kQHalf + (kk & 3) * 32),
+                                sdesc_sw128(k0 + (kk >> 2) * kKVHalf + (kk & 3) * 32), id_s, kk > 0);
                 }
-                tc_commit(&s_full[i]);
+                commit_warp(&s_full[i * 2 + (k & 1)]);
             };
-            auto issue_pv = [&](int i, int jj) {  // O_i += P_i(j) V(j), P from TMEM (packed bf16 pairs)
-                mbar_wait(&p_full[i], jj & 1);
-                tc_fence_after();
-                const uint32_t v0 = smem_u32(sm + kPPOffV + (jj & 1) * kTileBytes);
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    tc_mma_ts(tmem + 256 + i * 128, tmem + i * 128 + kk * 8, sdesc_mn_sw128(v0 + kk * 2048), id_o,
-                              (jj > 0 || kk > 0) ? 1u : 0u);
-                if (jj == cnt[i] - 1) tc_commit(&o_done[i]);
-            };
-            auto k_ready = [&](int jj) {
-                mbar_wait(&k_full[jj & 1], (jj >> 1) & 1);
+            auto k_ready = [&](int k) {
+                mbar_wait(&k_full[k % kStages], (k / kStages) & 1);
                 tc_fence_after();
             };
-            if (jmax > 0) {
-                k_ready(0);
+            for (int k = 0; k < 2 && k < jmax; ++k) {
+                k_ready(k);
                 for (int i = 0; i < 2; ++i)
-                    if (cnt[i] > 0) issue_s(i, 0);
-                tc_commit(&k_empty[0]);
+                    if (k < cnt[i]) issue_s(i, k);
+                commit_warp(&k_empty[k % kStages]);
             }
-            for (int jj = 0; jj < jmax; ++jj) {
-                const bool next = jj + 1 < jmax;
-                mbar_wait(&v_full[jj & 1], (jj >> 1) & 1);
+            for (int k = 0; k < jmax; ++k) {
+                const bool ahead = k + 2 < jmax;
+                mbar_wait(&v_full[k % kStages], (k / kStages) & 1);
                 tc_fence_after();
-                if (next) k_ready(jj + 1);
+                if (ahead) k_ready(k + 2);
+                const uint32_t v0 = smem_u32(sm + kPPOffV + (k % kStages) * kKVTileBytes);
                 for (int i = 0; i < 2; ++i) {
-                    if (jj < cnt[i]) issue_pv(i, jj);
-                    if (jj + 1 < cnt[i]) issue_s(i, jj + 1);
+                    if (k < cnt[i]) {  // O_i += P_i(k) V(k), P from TMEM (packed bf16 pairs)
+                        mbar_wait(&p_full[i * 2 + (k & 1)], (k >> 1) & 1);
+                        if (k < 16 && lane == 0) pf_stamp(p, 24 + 16 * i + k);
+                        tc_fence_after();
+#pragma unroll
+                        for (int kk = 0; kk < kKT / 16; ++kk)
+                            mma_ts_warp(tm + 256 + i * 128, tm + i * 128 + (k & 1) * 64 + kk * 8,
+                                      sdesc_mn_sw128(v0 + kk * 2048), id_o, (k > 0 || kk > 0) ? 1u : 0u);
+                        // S_i(k+1) (issued right after PV_i(k-1)) retiring tells the softmax that
+                        // PV_i(k-1) did; only the last step has no S_i(k+1): PV_i(cnt-2) commits here
+                        if (k == cnt[i] - 2) commit_warp(&pv_done[i]);
+                        if (k == cnt[i] - 1) commit_warp(&o_done[i]);
+                    }
+                    if (k + 2 < cnt[i]) issue_s(i, k + 2);
                 }
-                tc_commit(&v_empty[jj & 1]);
-                if (next) tc_commit(&k_empty[(jj + 1) & 1]);
+                if (k < 16 && lane == 0) pf_stamp(p, 8 + k);
+                commit_warp(&v_empty[k % kStages]);
+                if (ahead) commit_warp(&k_empty[(k + 2) % kStages]);
             }
         }
     } else {
@@ -359,45 +476,77 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         const uint32_t lane_base = static_cast<uint32_t>(qw * 32) << 16;
         const uint32_t s_col = tmem + lane_base + i * 128, o_col = tmem + lane_base + 256 + i * 128;
         float m_ref = -INFINITY, l_sum = 0.f;
-        for (int jj = 0; jj < cnt_i; ++jj) {
-            mbar_wait(&s_full[i], jj & 1);
+        for (int k = 0; k < cnt_i; ++k) {
+            mbar_wait(&s_full[i * 2 + (k & 1)], (k >> 1) & 1);
+            if (threadIdx.x == 64 && k < 16) pf_stamp(p, 56 + k);
             tc_fence_after();
-            uint32_t sv[4][32];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld32(s_col + c * 32, sv[c]);
+            const uint32_t sb = s_col + (k & 1) * 64;
+            uint32_t sv[2][32];
+            tmem_ld32(sb, sv[0]);
+            tmem_ld32(sb + 32, sv[1]);
             tmem_ld_wait();
-            const int key0 = (j0 + jj) * kKT;
-            // row max over 128 columns as 8 independent chains (one warp per SM sub-partition
-            // per warpgroup: a single 128-long fmax chain would cost ~512 cycles of latency)
-            float pmx[8];
+            const int key0 = (j0 + k) * kKT;
+            if (key0 + kKT - 1 > warp_q0) {  // diagonal sub-tile: causal mask
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        if (key0 + c * 32 + e > qpos) sv[c][e] = __float_as_uint(-INFINITY);
+            }
+            // P = exp2(S * scale - m) -> bf16 pairs over the buffer's first 32 columns, computed
+            // speculatively against the running max m_ref while the row max is reduced (8
+            // independent chains each: one softmax warp per SM sub-partition and warpgroup has
+            // no other latency cover); only when the max grows by more than 2^8 (rare; always
+            // on a piece's first sub-tile) is P recomputed against the new max and O rescaled.
+            // A row whose keys in this piece are all masked keeps m = -inf: P = 0, not NaN.
+            float pmx[8], rsp[8];
+            uint32_t pk[2][16];
+            auto exp_pack = [&](float m_use) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) rsp[e] = 0.f;
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        const bool poly = g == 3;
+                        float pv[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const float x = fmaf(__uint_as_float(sv[c][g * 8 + e]), p.scale_log2, -m_use);
+                            pv[e] = (p.ablate & 2) ? x : poly ? exp2_poly(x) : ex2_approx(x);
+                            rsp[e] += pv[e];
+                        }
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) pk[c][g * 4 + e] = pack_bf16x2(pv[2 * e], pv[2 * e + 1]);
+                    }
+            };
 #pragma unroll
             for (int e = 0; e < 8; ++e) pmx[e] = -INFINITY;
-            if (key0 + kKT - 1 <= warp_q0) {
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
+            for (int c = 0; c < 2; ++c)
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) pmx[e & 7] = fmaxf(pmx[e & 7], __uint_as_float(sv[c][e]));
-            } else {
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        if (key0 + c * 32 + e > qpos) sv[c][e] = __float_as_uint(-INFINITY);
-                        pmx[e & 7] = fmaxf(pmx[e & 7], __uint_as_float(sv[c][e]));
-                    }
-            }
-            float mx = fmaxf(fmaxf(fmaxf(pmx[0], pmx[1]), fmaxf(pmx[2], pmx[3])),
-                             fmaxf(fmaxf(pmx[4], pmx[5]), fmaxf(pmx[6], pmx[7])));
-            mx *= p.scale_log2;
+                for (int e = 0; e < 32; ++e) pmx[e & 7] = fmaxf(pmx[e & 7], __uint_as_float(sv[c][e]));
+            if (m_ref != -INFINITY) exp_pack(m_ref);
+            const float mx = fmaxf(fmaxf(fmaxf(pmx[0], pmx[1]), fmaxf(pmx[2], pmx[3])),
+                                   fmaxf(fmaxf(pmx[4], pmx[5]), fmaxf(pmx[6], pmx[7]))) *
+                             p.scale_log2;
             const bool need = __any_sync(0xffffffffu, mx > m_ref + kRescaleThreshold || m_ref == -INFINITY);
             if (need) {
                 const float m_new = fmaxf(m_ref, mx);
                 const float corr = m_ref == -INFINITY ? 0.f : exp2f(m_ref - m_new);
                 l_sum *= corr;
                 m_ref = m_new;
-                if (jj > 0) {  // PV_i(j-1) retired before S_i(j) (in-order tensor pipe)
+                exp_pack(m_ref == -INFINITY ? 0.f : m_ref);
+                if (k > 0) {
+                    // O holds PV_i(0..k-1) once PV_i(k-1) retires (PV_i(k) waits for this P):
+                    // S_i(k+1) was issued right after it, or, at the last step, PV_i(k-1) commits
+                    if (k + 1 < cnt_i)
+                        mbar_wait(&s_full[i * 2 + ((k + 1) & 1)], ((k + 1) >> 1) & 1);
+                    else
+                        mbar_wait(&pv_done[i], 0);
+                    tc_fence_after();
 #pragma unroll 1
-                    for (int c = 0; c < 8; ++c) {  // 16 columns at a time: S stays in registers
+                    for (int c = 0; c < 8; ++c) {  // 16 columns at a time
                         uint32_t o[16];
                         tmem_ld16(o_col + c * 16, o);
                         tmem_ld_wait();
@@ -407,36 +556,14 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                     }
                 }
             }
-            // P = exp2(S * scale - m) -> bf16 pairs over S's first 64 columns; the row sum as 8
-            // independent chains (see the max above)
-            float rsp[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) rsp[e] = 0.f;
-            // a row whose keys in this piece are all masked keeps m = -inf: P = 0, not NaN
-            const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t pk[16];
-#pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    const bool poly = g == 3;
-                    float pv[8];
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        const float x = fmaf(__uint_as_float(sv[c][g * 8 + e]), p.scale_log2, -m_use);
-                        pv[e] = poly ? exp2_poly(x) : ex2_approx(x);
-                        rsp[e] += pv[e];
-                    }
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) pk[g * 4 + e] = pack_bf16x2(pv[2 * e], pv[2 * e + 1]);
-                }
-                tmem_st16(s_col + c * 16, pk);
-            }
+            tmem_st16(sb, pk[0]);
+            tmem_st16(sb + 16, pk[1]);
             tmem_st_wait();
             l_sum += ((rsp[0] + rsp[1]) + (rsp[2] + rsp[3])) + ((rsp[4] + rsp[5]) + (rsp[6] + rsp[7]));
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&p_full[i]);
+            if (lane == 0) mbar_arrive(&p_full[i * 2 + (k & 1)]);
+            if (threadIdx.x == 64 && k < 16) pf_stamp(p, 72 + k);
         }
         if (cnt_i > 0) {
             mbar_wait(&o_done[i], 0);
@@ -515,7 +642,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                     if (q == piece) continue;
                     float lq;
                     const float f = weight(q, &lq);
-                    L += f * lq;
+                    if (f != 0.f) L += f * lq;
                 }
                 const float inv = L > 0.f ? 1.f / L : 0.f;
 #pragma unroll 1
@@ -526,7 +653,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                         tmem_ld32(o_col + c * 32, o);
                         tmem_ld_wait();
 #pragma unroll
-                        for (int e = 0; e < 32; ++e) acc[e] = __uint_as_float(o[e]) * f_own;
+                        for (int e = 0; e < 32; ++e) acc[e] = f_own != 0.f ? __uint_as_float(o[e]) * f_own : 0.f;
                     } else {
 #pragma unroll
                         for (int e = 0; e < 32; ++e) acc[e] = 0.f;
@@ -561,6 +688,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             }
         }
     }
+    if (threadIdx.x == 64) pf_stamp(p, 120);
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -616,7 +744,7 @@ int make_map_2d(const void* ptr, unsigned long long rows, unsigned long long col
 namespace {
 // Host plan of a prefill launch: token blocks, key tiles per piece, grid. Splits only when the
 // units do not fill `max_ctas` (and a workspace exists): then the smallest cap whose pieces fit
-// one wave, with at most 16 pieces per unit (the merge's register budget).
+// one wave (pieces of 4+ sub-tiles, at most 4 per unit).
 template <int HT>
 int pf_plan(int q_len, int pos0, int nq, int nkv, int max_ctas, bool can_split, int* n_tb_out, int* cap_out) {
     constexpr int TT = 128 / HT;
@@ -632,7 +760,13 @@ int pf_plan(int q_len, int pos0, int nq, int nkv, int max_ctas, bool can_split, 
     if (can_split && static_cast<long long>(per_tb) * n_tb < max_ctas) {
         long long total = 0;
         for (int tb = 0; tb < n_tb; ++tb) total += static_cast<long long>(per_tb) * pf_steps<HT>(q_len, pos0, tb);
-        int c = static_cast<int>(std::max<long long>(std::max(1, (n_max + 15) / 16), (total + max_ctas - 1) / max_ctas));
+        // pieces of at least kMinPiece sub-tiles: a piece's setup (Q load, pipeline fill) and the
+        // merge cost ~2-3 us, as much as a few hundred keys of work
+        // and at most kMaxPieces per unit: the last piece reads every other piece's 128 KB
+        // partial from L2 on the kernel's critical path
+        constexpr int kMinPiece = 4, kMaxPieces = 4;
+        int c = static_cast<int>(std::max<long long>(std::max(kMinPiece, (n_max + kMaxPieces - 1) / kMaxPieces),
+                                                     (total + max_ctas - 1) / max_ctas));
         while (c < n_max && grid_for(c) > max_ctas) ++c;
         cap = std::min(c, n_max);
     }
@@ -676,7 +810,36 @@ int launch_prefill(const void* q, int q_rows_total, const CUtensorMap& mkv, cons
                                  &prm.n_tb, &prm.steps_cap);
     if (ws && grid > max_ctas && prm.steps_cap < pf_steps<HT>(q_len, pos0, prm.n_tb - 1))
         return static_cast<int>(cudaErrorInvalidValue);  // split pieces beyond the workspace
-    return launch_pdl(attn_prefill_pp_kernel<HT>, dim3(grid), dim3(kPPThreads), kPPSmemBytes, st, mq, mkv, prm);
+    static const bool probe = [] {
+        const char* e = std::getenv("CRONUS_PF_PROBE");
+        return e && e[0] == '1';
+    }();
+    prm.probe = nullptr;
+    static const int ablate = [] {
+        const char* e = std::getenv("CRONUS_PF_ABLATE");
+        return e ? std::atoi(e) : 0;
+    }();
+    prm.ablate = ablate;
+    if (!probe) return launch_pdl(attn_prefill_pp_kernel<HT>, dim3(grid), dim3(kPPThreads), kPPSmemBytes, st, mq, mkv, prm);
+    // dev: clock64 pipeline stamps of CTA 0 (the heaviest piece), relative to kernel entry
+    long long* buf = nullptr;
+    cudaMalloc(&buf, static_cast<size_t>(grid) * 128 * 8);
+    cudaMemsetAsync(buf, 0, static_cast<size_t>(grid) * 128 * 8, st);
+    prm.probe = buf;
+    int rc2 = launch_pdl(attn_prefill_pp_kernel<HT>, dim3(grid), dim3(kPPThreads), kPPSmemBytes, st, mq, mkv, prm);
+    std::vector<long long> h(128);
+    cudaMemcpyAsync(h.data(), buf, 128 * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    cudaFree(buf);
+    auto d = [&](int k) { return h[k] ? h[k] - h[0] : -1; };
+    std::fprintf(stderr, "[pf probe] q_len=%d pos0=%d grid=%d cap=%d setup=%lld q_full=%lld end=%lld\n", q_len, pos0,
+                 grid, prm.steps_cap, d(1), d(2), d(120));
+    for (int jj = 0; jj < 16; ++jj)
+        if (h[8 + jj] || h[88 + jj])
+            std::fprintf(stderr, "  jj=%2d K_issue=%7lld V_issue=%7lld v_full=%7lld S0_done=%7lld P0_arrive=%7lld "
+                                 "p0_seen=%7lld p1_seen=%7lld\n",
+                         jj, d(88 + jj), d(104 + jj), d(8 + jj), d(56 + jj), d(72 + jj), d(24 + jj), d(40 + jj));
+    return rc2;
 }
 }  // namespace
 

@@ -95,15 +95,19 @@ __global__ void __launch_bounds__(128)
     uint64_t* bar = bars[warp];
     const int v_rows = a.nkv * kDBlk;  // pool rows from a head's K tile to its V tile
     int issued = 0;
-    auto load = [&](int i) {  // lane 0
-        const int row = ((table[first + 4 * i] * a.n_layers + a.layer) * 2 * a.nkv + kvh) * kDBlk;
+    // Loads are issued by the whole (convergent) warp, one elected lane inside the PTX: the
+    // block id is made provably warp-uniform (shuffle from lane 0) so the TMA operands live in
+    // uniform registers (see tc_mma_bf16_warp).
+    auto load = [&](int i) {
+        const int id = __shfl_sync(0xffffffffu, table[first + 4 * i], 0);
+        const int row = ((id * a.n_layers + a.layer) * 2 * a.nkv + kvh) * kDBlk;
         uint8_t* dK = ring + (i % STAGES) * 2 * kDTileBytes;
         uint64_t* bb = &bar[i % STAGES];
-        mbar_arrive_expect_tx(bb, 2 * kDTileBytes);
-        tma_load_2d(dK, &tm, bb, 0, row);
-        tma_load_2d(dK + kDTileBytes / 2, &tm, bb, 64, row);
-        tma_load_2d(dK + kDTileBytes, &tm, bb, 0, row + v_rows);
-        tma_load_2d(dK + kDTileBytes + kDTileBytes / 2, &tm, bb, 64, row + v_rows);
+        mbar_expect_tx_warp(bb, 2 * kDTileBytes);
+        tma_load_2d_warp(dK, &tm, bb, 0, row);
+        tma_load_2d_warp(dK + kDTileBytes / 2, &tm, bb, 64, row);
+        tma_load_2d_warp(dK + kDTileBytes, &tm, bb, 0, row + v_rows);
+        tma_load_2d_warp(dK + kDTileBytes + kDTileBytes / 2, &tm, bb, 64, row + v_rows);
     };
     const int pre = min(mine, STAGES);
     pdl_launch();
@@ -112,12 +116,12 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
         for (int i = 0; i < STAGES; ++i) mbar_init(&bar[i], 1);
         fence_mbar_init();
-        // fused RoPE: no kernel writes the pool before us -> the last block may go early too
-        while (issued < pre && (a.qkv || first + 4 * issued != nblk - 1)) load(issued++);
     }
+    __syncwarp();
+    // fused RoPE: no kernel writes the pool before us -> the last block may go early too
+    while (issued < pre && (a.qkv || first + 4 * issued != nblk - 1)) load(issued++);
     pdl_wait();
-    if (lane == 0)
-        while (issued < pre) load(issued++);
+    while (issued < pre) load(issued++);
     const int pos = len - 1;  // the decode token
     const int qkv_w = (a.nq + 2 * a.nkv) * kDHD;
     if (a.qkv) {  // Q = RoPE(q) from the fp32 accumulator (G heads x 64 rotate-half pairs)
@@ -188,7 +192,7 @@ __global__ void __launch_bounds__(128)
         dec_block<SwzTma128>(K, K + kDTileBytes, qf, o, m_run, l_run, (first + 4 * i) * kDBlk, len,
                              a.qk_scale_log2, lane);
         __syncwarp();
-        if (lane == 0 && issued < mine) load(issued++);  // refill the slot just consumed
+        if (issued < mine) load(issued++);  // refill the slot just consumed
     }
     float* res = reinterpret_cast<float*>(ring_all + kDResOff);
     dec_merge_warps<G>(ring_all, small, o, m_run, l_run, t, 1, res);

@@ -166,79 +166,8 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
         "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
         : "memory");
 }
-// D[tmem] (+)= A[tmem] * B[smem desc]: A (M=128 rows in lanes, K packed 2 x bf16 per column).
-__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                          uint32_t accumulate) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
-        "}\n" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
 __device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
-// tcgen05 issue from a whole, convergent warp: one elected lane issues. With every operand
-// computed warp-uniformly the compiler keeps them in uniform registers; issuing from inside
-// `if (lane == 0)` instead wraps every MMA in an ELECT / R2UR.BROADCAST / BRA.U.ANY loop
-// (~100 cycles per instruction, more than a 128x64x16 MMA takes).
-__device__ __forceinline__ void mma_ss_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                            uint32_t accumulate) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p, e;\n"
-        "elect.sync _|e, 0xffffffff;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(d_tmem),
-        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-__device__ __forceinline__ void mma_ts_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                            uint32_t accumulate) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p, e;\n"
-        "elect.sync _|e, 0xffffffff;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
-        "}\n" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-__device__ __forceinline__ void expect_tx_warp(uint64_t* bar, uint32_t bytes) {
-    asm volatile(
-        "{\n"
-        ".reg .pred e;\n"
-        "elect.sync _|e, 0xffffffff;\n"
-        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(bytes)
-        : "memory");
-}
-__device__ __forceinline__ void tma_2d_warp(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
-                                            uint64_t policy) {
-    asm volatile(
-        "{\n"
-        ".reg .pred e;\n"
-        "elect.sync _|e, 0xffffffff;\n"
-        "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
-        "%4}], [%2], %5;\n"
-        "}\n" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
-        : "memory");
-}
-__device__ __forceinline__ void commit_warp(uint64_t* bar) {
-    asm volatile(
-        "{\n"
-        ".reg .pred e;\n"
-        "elect.sync _|e, 0xffffffff;\n"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
-        "}\n" ::"r"(smem_u32(bar))
-        : "memory");
-}
 
 // Key tiles of token block tb (its second tile's last valid token).
 template <int HT>
@@ -358,12 +287,12 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                     if (lane == 0) mbar_arrive(&k_full[st]);
                     return;
                 }
-                expect_tx_warp(&k_full[st], kKVTileBytes);
+                mbar_expect_tx_warp(&k_full[st], kKVTileBytes);
 #pragma unroll
                 for (int bb = 0; bb < BPT; ++bb) {
                     const int r = __shfl_sync(0xffffffffu, my_row, bb);
-                    tma_2d_warp(K + bb * 2048, &tmKV, &k_full[st], 0, r, keep);
-                    tma_2d_warp(K + kKVHalf + bb * 2048, &tmKV, &k_full[st], 64, r, keep);
+                    tma_load_2d_hint_warp(K + bb * 2048, &tmKV, &k_full[st], 0, r, keep);
+                    tma_load_2d_hint_warp(K + kKVHalf + bb * 2048, &tmKV, &k_full[st], 64, r, keep);
                 }
             };
             auto load_v = [&](int k) {
@@ -375,13 +304,13 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                     if (lane == 0) mbar_arrive(&v_full[st]);
                     return;
                 }
-                expect_tx_warp(&v_full[st], kKVTileBytes);
+                mbar_expect_tx_warp(&v_full[st], kKVTileBytes);
                 uint8_t* V = sm + kPPOffV + st * kKVTileBytes;
 #pragma unroll
                 for (int bb = 0; bb < BPT; ++bb) {
                     const int r = __shfl_sync(0xffffffffu, my_row, bb) + p.nkv * 16;
-                    tma_2d_warp(V + bb * 2048, &tmKV, &v_full[st], 0, r, keep);
-                    tma_2d_warp(V + kKVHalf + bb * 2048, &tmKV, &v_full[st], 64, r, keep);
+                    tma_load_2d_hint_warp(V + bb * 2048, &tmKV, &v_full[st], 0, r, keep);
+                    tma_load_2d_hint_warp(V + kKVHalf + bb * 2048, &tmKV, &v_full[st], 64, r, keep);
                 }
             };
             // Issue order = arrival order (the TMA unit serves requests in order): the first
@@ -392,13 +321,13 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             while (pre < 2 && pre < jmax && (j0 + pre + 1) * kKT <= p.pos0) load_k(pre++);
             pdl_wait();
             for (int i = 0; i < n_qt; ++i) {
-                expect_tx_warp(&q_full[i], kQTileBytes);
+                mbar_expect_tx_warp(&q_full[i], kQTileBytes);
                 uint8_t* Q = sm + kPPOffQ + i * kQTileBytes;
                 const int qrow = p.q_row0 + t_base[i];
 #pragma unroll
                 for (int g = 0; g < HT; ++g) {
-                    tma_2d_warp(Q + g * TT * 128, &tmQ, &q_full[i], (h_base + g) * 128, qrow, keep);
-                    tma_2d_warp(Q + kQHalf + g * TT * 128, &tmQ, &q_full[i], (h_base + g) * 128 + 64, qrow, keep);
+                    tma_load_2d_hint_warp(Q + g * TT * 128, &tmQ, &q_full[i], (h_base + g) * 128, qrow, keep);
+                    tma_load_2d_hint_warp(Q + kQHalf + g * TT * 128, &tmQ, &q_full[i], (h_base + g) * 128 + 64, qrow, keep);
                 }
             }
             for (int k = 0; k < jmax; ++k) {
@@ -419,11 +348,11 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                 const uint32_t k0 = smem_u32(sm + kPPOffK + (k % kStages) * kKVTileBytes);
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
-                    mma_ss_warp(tm + i * 128 + (k & 1) * 64,
+                    tc_mma_bf16_warp(tm + i * 128 + (k & 1) * 64,
                                 sdesc_sw128(q0 + (kk >> 2) * kQHalf + (kk & 3) * 32),
                                 sdesc_sw128(k0 + (kk >> 2) * kKVHalf + (kk & 3) * 32), id_s, kk > 0);
                 }
-                commit_warp(&s_full[i * 2 + (k & 1)]);
+                tc_commit_warp(&s_full[i * 2 + (k & 1)]);
             };
             auto k_ready = [&](int k) {
                 mbar_wait(&k_full[k % kStages], (k / kStages) & 1);
@@ -433,7 +362,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                 k_ready(k);
                 for (int i = 0; i < 2; ++i)
                     if (k < cnt[i]) issue_s(i, k);
-                commit_warp(&k_empty[k % kStages]);
+                tc_commit_warp(&k_empty[k % kStages]);
             }
             for (int k = 0; k < jmax; ++k) {
                 const bool ahead = k + 2 < jmax;
@@ -448,18 +377,18 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                         tc_fence_after();
 #pragma unroll
                         for (int kk = 0; kk < kKT / 16; ++kk)
-                            mma_ts_warp(tm + 256 + i * 128, tm + i * 128 + (k & 1) * 64 + kk * 8,
+                            tc_mma_ts_warp(tm + 256 + i * 128, tm + i * 128 + (k & 1) * 64 + kk * 8,
                                       sdesc_mn_sw128(v0 + kk * 2048), id_o, (k > 0 || kk > 0) ? 1u : 0u);
                         // S_i(k+1) (issued right after PV_i(k-1)) retiring tells the softmax that
                         // PV_i(k-1) did; only the last step has no S_i(k+1): PV_i(cnt-2) commits here
-                        if (k == cnt[i] - 2) commit_warp(&pv_done[i]);
-                        if (k == cnt[i] - 1) commit_warp(&o_done[i]);
+                        if (k == cnt[i] - 2) tc_commit_warp(&pv_done[i]);
+                        if (k == cnt[i] - 1) tc_commit_warp(&o_done[i]);
                     }
                     if (k + 2 < cnt[i]) issue_s(i, k + 2);
                 }
                 if (k < 16 && lane == 0) pf_stamp(p, 8 + k);
-                commit_warp(&v_empty[k % kStages]);
-                if (ahead) commit_warp(&k_empty[(k + 2) % kStages]);
+                tc_commit_warp(&v_empty[k % kStages]);
+                if (ahead) tc_commit_warp(&k_empty[(k + 2) % kStages]);
             }
         }
     } else {

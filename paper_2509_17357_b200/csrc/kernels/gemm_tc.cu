@@ -346,8 +346,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     pdl_launch();
 
     if (warp == 0) {
-        // ------------------------------------------------------------ producer
-        if (lane == 0) {
+        // ------------------------------------------------------------ producer (whole warp,
+        // convergent; one elected lane issues: see tc_mma_bf16_warp)
+        {
             const uint64_t keep = policy_evict_last();    // activations: reused by every weight tile
             const uint64_t stream = policy_evict_first();  // weights: streamed once per launch
             // (1) weight prefetch: the first kStages k-blocks of this CTA's work (their
@@ -359,18 +360,18 @@ __global__ void __launch_bounds__(kThreads, 2)
                 int nt, mt, kb0, kb1;
                 while (n_pre < S && next_unit(p, pos, nt, mt, kb0, kb1))
                     for (int kb = kb0; kb < kb1 && n_pre < S; ++kb) {
-                        mbar_arrive_expect_tx(&full[n_pre], C::kStageBytes);
-                        tma_load_2d_hint(sA + n_pre * C::kABytes, &tmW, &full[n_pre], kb * kTileK, nt * kTileN,
-                                         stream);
+                        mbar_expect_tx_warp(&full[n_pre], C::kStageBytes);
+                        tma_load_2d_hint_warp(sA + n_pre * C::kABytes, &tmW, &full[n_pre], kb * kTileK, nt * kTileN,
+                                              stream);
                         pre_nt[n_pre] = nt, pre_mt[n_pre] = mt, pre_kb[n_pre] = kb;
                         ++n_pre;
                     }
             }
             pdl_wait();
-            probe_stamp(p, 1);
+            if (lane == 0) probe_stamp(p, 1);
             // (2) the activation tiles of the prefetched stages
             for (int i = 0; i < n_pre; ++i)
-                tma_load_2d_hint(sB + i * C::kBBytes, &tmX, &full[i], pre_kb[i] * kTileK, pre_mt[i] * BN, keep);
+                tma_load_2d_hint_warp(sB + i * C::kBBytes, &tmX, &full[i], pre_kb[i] * kTileK, pre_mt[i] * BN, keep);
             (void)pre_nt;
             // (3) steady state
             int stage = 0;
@@ -382,10 +383,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                 for (int kb = kb0; kb < kb1; ++kb, ++issued) {
                     if (issued >= n_pre) {
                         mbar_wait(&empty[stage], phase ^ 1);
-                        mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-                        tma_load_2d_hint(sA + stage * C::kABytes, &tmW, &full[stage], kb * kTileK, nt * kTileN,
-                                         stream);
-                        tma_load_2d_hint(sB + stage * C::kBBytes, &tmX, &full[stage], kb * kTileK, mt * BN, keep);
+                        mbar_expect_tx_warp(&full[stage], C::kStageBytes);
+                        tma_load_2d_hint_warp(sA + stage * C::kABytes, &tmW, &full[stage], kb * kTileK, nt * kTileN,
+                                              stream);
+                        tma_load_2d_hint_warp(sB + stage * C::kBBytes, &tmX, &full[stage], kb * kTileK, mt * BN, keep);
                     }
                     if (++stage == S) {
                         stage = 0;
@@ -395,8 +396,9 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
+        // ------------------------------------------------------------ MMA issuer (whole warp)
+        {
+            const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);  // provably warp-uniform
             constexpr uint32_t idesc = idesc_bf16_f32(kTileN, BN);
             int stage = 0;
             uint32_t phase = 0;
@@ -407,28 +409,28 @@ __global__ void __launch_bounds__(kThreads, 2)
             while (next_unit(p, pos, nt, mt, kb0, kb1)) {
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * BN;
+                const uint32_t d_tmem = tbase + acc * BN;
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    if (p.probe != nullptr && p.probe[blockIdx.x * 6 + 2] == 0) probe_stamp(p, 2);
+                    if (lane == 0 && p.probe != nullptr && p.probe[blockIdx.x * 6 + 2] == 0) probe_stamp(p, 2);
                     const uint32_t a0 = smem_u32(sA + stage * C::kABytes);
                     const uint32_t b0 = smem_u32(sB + stage * C::kBBytes);
 #pragma unroll
                     for (int k = 0; k < kTileK / 16; ++k)
-                        tc_mma_bf16(d_tmem, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc,
-                                    (kb > kb0 || k > 0) ? 1u : 0u);
-                    tc_commit(&empty[stage]);  // smem slot free once these MMAs retire
+                        tc_mma_bf16_warp(d_tmem, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc,
+                                         (kb > kb0 || k > 0) ? 1u : 0u);
+                    tc_commit_warp(&empty[stage]);  // smem slot free once these MMAs retire
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                tc_commit(&tfull[acc]);  // accumulator ready for the epilogue
+                tc_commit_warp(&tfull[acc]);  // accumulator ready for the epilogue
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }
-            probe_stamp(p, 3);
+            if (lane == 0) probe_stamp(p, 3);
         }
     } else {
         // ------------------------------------------------------------ epilogue

@@ -122,7 +122,9 @@ def main(argv=None):
     pre, chk = samples(eng, base, budget_high=budget_high)
     # the other two models of each profile (DP and disaggregated baselines run them)
     pre_hi = prefill_samples(eng, base, 1)
-    chk_lo = chunked_samples(eng, base, 0, budget_low, pos0s=(0, 1024, 2048), n_decs=(0, 8, 32, 64))
+    # the PPI worker runs chunked iterations only under the DP policy: size it for that role
+    base_dp = "\n".join("policy = dp" if ln.split("=")[0].strip() == "policy" else ln for ln in base.splitlines())
+    chk_lo = chunked_samples(eng, base_dp, 0, budget_low, pos0s=(0, 1024, 2048), n_decs=(0, 8, 32, 64))
     fits = {"low": {"prefill": E.fit_prefill([p[0] for p in pre], [p[1] for p in pre]),
                     "chunked": E.fit_chunked([c[0] for c in chk_lo], [c[1] for c in chk_lo], [c[2] for c in chk_lo])},
             "high": {"prefill": E.fit_prefill([p[0] for p in pre_hi], [p[1] for p in pre_hi]),

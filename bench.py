@@ -170,7 +170,7 @@ def traffic_ratios():
 def kernel_class(name):
     """Kernel name (CUPTI, demangled) -> the engine's kernel-time class."""
     if "gemm_tc_kernel" in name:
-        return "gemm_tc" if "<256>" in name else "gemm_stream"  # BN <= 128 <=> M <= 128 rows
+        return "gemm_tc" if "<256" in name else "gemm_stream"  # BN <= 128 <=> M <= 128 rows
     if "attn_decode" in name:
         return "decode_attn"
     if "attn_prefill" in name:

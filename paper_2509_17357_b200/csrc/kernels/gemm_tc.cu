@@ -62,8 +62,14 @@ struct GemmParams {
     long long tail_iters;
     ck_gemm_fuse fuse;
     unsigned long long* probe;  // dev (CRONUS_GEMM_PROBE=1): per-CTA timeline stamps, else null
-    int stages;                 // ring depth actually used (<= Cfg<BN>::kStages)
+    int stages;                 // ring depth actually used (<= Cfg<BN, PAIR>::kStages)
+    int pair;                   // CTAs per work unit: 1, or 2 (a cta_group::2 pair on one TPC)
 };
+
+// The unit iteration works in "unit CTAs": a CTA, or a CTA pair when p.pair == 2 (both CTAs
+// of the pair walk the identical unit sequence).
+__device__ __forceinline__ int unit_cta(const GemmParams& p) { return static_cast<int>(blockIdx.x) / p.pair; }
+__device__ __forceinline__ int unit_grid(const GemmParams& p) { return static_cast<int>(gridDim.x) / p.pair; }
 
 __device__ __forceinline__ void probe_stamp(const GemmParams& p, int slot) {
     if (p.probe != nullptr) {
@@ -220,10 +226,10 @@ __device__ void finalize_tile(const GemmParams& p, int nt, int mt, int BN, int t
     }
 }
 
-template <int BN>
+template <int BN, int PAIR = 1>
 struct Cfg {
     static constexpr int kABytes = kTileN * kTileK * 2;
-    static constexpr int kBBytes = BN * kTileK * 2;
+    static constexpr int kBBytes = (BN / PAIR) * kTileK * 2;  // a pair's CTAs hold half the token tile each
     static constexpr int kStageBytes = kABytes + kBBytes;
     // As many stages as fit in ~220 KB: the weight stream is latency bound (Little's
     // law: bytes in flight per SM / loaded HBM latency), so small token tiles get a
@@ -246,13 +252,12 @@ __device__ __forceinline__ void decode_unit(const GemmParams& p, int u, int& nt,
 // Work iteration shared by the producer, MMA and epilogue roles (all three walk the
 // identical unit sequence). `pos` starts at first_unit().
 __device__ __forceinline__ long long tail_lo(const GemmParams& p) {
-    return static_cast<long long>(p.dp_tiles) * p.kb_total + static_cast<long long>(blockIdx.x) * p.kb_piece;
+    return static_cast<long long>(p.dp_tiles) * p.kb_total + static_cast<long long>(unit_cta(p)) * p.kb_piece;
 }
 __device__ __forceinline__ long long first_unit(const GemmParams& p) {
-    if (p.hybrid)
-        return blockIdx.x < static_cast<unsigned>(p.dp_tiles) ? static_cast<long long>(blockIdx.x) * p.kb_total
-                                                               : tail_lo(p);
-    return p.stream_k ? (static_cast<long long>(blockIdx.x) * p.iters) / gridDim.x : blockIdx.x;
+    const int c = unit_cta(p);
+    if (p.hybrid) return c < p.dp_tiles ? static_cast<long long>(c) * p.kb_total : tail_lo(p);
+    return p.stream_k ? (static_cast<long long>(c) * p.iters) / unit_grid(p) : c;
 }
 // `tail`: the unit is a partial-K piece of a hybrid launch (goes through the accumulator).
 __device__ __forceinline__ bool next_unit(const GemmParams& p, long long& pos, int& nt, int& mt, int& kb0, int& kb1,
@@ -264,7 +269,7 @@ __device__ __forceinline__ bool next_unit(const GemmParams& p, long long& pos, i
             tile = static_cast<int>(pos / p.kb_total);
             kb0 = 0;
             kb1 = p.kb_total;
-            pos += static_cast<long long>(gridDim.x) * p.kb_total;
+            pos += static_cast<long long>(unit_grid(p)) * p.kb_total;
             if (pos >= dp_end) pos = tail_lo(p);
             if (tail) *tail = false;
         } else {
@@ -282,7 +287,7 @@ __device__ __forceinline__ bool next_unit(const GemmParams& p, long long& pos, i
     }
     if (tail) *tail = false;
     if (p.stream_k) {
-        const long long end = (static_cast<long long>(blockIdx.x + 1) * p.iters) / gridDim.x;
+        const long long end = (static_cast<long long>(unit_cta(p) + 1) * p.iters) / unit_grid(p);
         if (pos >= end) return false;
         const int tile = static_cast<int>(pos / p.kb_total);
         kb0 = static_cast<int>(pos - static_cast<long long>(tile) * p.kb_total);
@@ -294,14 +299,90 @@ __device__ __forceinline__ bool next_unit(const GemmParams& p, long long& pos, i
     }
     if (pos >= p.units) return false;
     decode_unit(p, static_cast<int>(pos), nt, mt, kb0, kb1);
-    pos += gridDim.x;
+    pos += unit_grid(p);
     return true;
 }
 
-template <int BN>
+// ------------------------------------------------------------------ CTA pair (cta_group::2)
+// PAIR == 2: two CTAs of a cluster on one TPC share a 256-weight-row x BN-token tile. Each
+// loads its own 128 weight rows and HALF of the token tile (the A / B halves of a
+// cta_group::2 MMA), the leader (rank 0) issues M = 256 MMAs that write each CTA's 128 rows x
+// BN accumulator into that CTA's TMEM, and every stage moves 16 + BN/2 x 128 B per CTA instead of
+// 16 + BN x 128 B: 1.5x less shared-memory fill per FLOP and a 6-deep ring at BN = 256 (4 alone).
+__device__ __forceinline__ uint32_t cluster_rank_u32() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// shared::cluster address of `local` (this CTA's shared::cta address) in CTA `rank`
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t local, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA into this CTA's smem, completion counted on the pair leader's barrier (cluster address)
+__device__ __forceinline__ void tma_load_2d_pair_warp(void* dst, const CUtensorMap* m, uint32_t bar_cluster, int c0,
+                                                      int c1, uint64_t policy) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1, {%3, %4}], [%2], %5;\n"
+        "}\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void tc_mma_bf16_pair_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                      uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, e;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// arrive on the barrier at this offset in both CTAs of the pair once the MMAs retire
+__device__ __forceinline__ void tc_commit_pair_warp(uint64_t* bar) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+}
+template <int PAIR>
+__device__ __forceinline__ void tmem_alloc_g(uint32_t* dst_smem, uint32_t ncols) {
+    if constexpr (PAIR == 2) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+                     "r"(ncols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+        tmem_alloc(dst_smem, ncols);
+        tmem_relinquish();
+    }
+}
+template <int PAIR>
+__device__ __forceinline__ void tmem_dealloc_g(uint32_t taddr, uint32_t ncols) {
+    if constexpr (PAIR == 2)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+    else
+        tmem_dealloc(taddr, ncols);
+}
+
+template <int BN, int PAIR>
 __global__ void __launch_bounds__(kThreads, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmParams p) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, PAIR>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -315,14 +396,14 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     const int warp = warp_id();
     const int lane = lane_id();
+    const uint32_t rank = PAIR == 2 ? cluster_rank_u32() : 0u;  // 0 = the pair's MMA leader
 
     if (warp == 0) {
         if (lane == 0) {
             tma_prefetch_desc(&tmW);
             tma_prefetch_desc(&tmX);
         }
-        tmem_alloc(tmem_slot, C::kTmemCols);
-        tmem_relinquish();
+        tmem_alloc_g<PAIR>(tmem_slot, C::kTmemCols);
     } else if (warp == 1 && lane == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
@@ -330,12 +411,15 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+            mbar_init(&tempty[a], 4 * PAIR);  // one arrive per epilogue warp (of both CTAs: the leader's)
         }
         fence_mbar_init();
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR == 2)
+        cluster_sync_all();  // both CTAs' barriers initialised before any peer TMA / commit reaches them
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (threadIdx.x == 0) probe_stamp(p, 0);
@@ -351,6 +435,25 @@ __global__ void __launch_bounds__(kThreads, 2)
         {
             const uint64_t keep = policy_evict_last();    // activations: reused by every weight tile
             const uint64_t stream = policy_evict_first();  // weights: streamed once per launch
+            // TMA of one stage's weight / activation half; a pair's loads complete on the
+            // leader's full barrier (cluster address), the leader expects both CTAs' bytes
+            auto full_addr = [&](int st) {
+                return PAIR == 2 ? mapa_rank(smem_u32(&full[st]), 0) : smem_u32(&full[st]);
+            };
+            auto load_w = [&](int st, int kb, int nt, uint64_t pol) {
+                const int row = (nt * PAIR + static_cast<int>(rank)) * kTileN;
+                if constexpr (PAIR == 2)
+                    tma_load_2d_pair_warp(sA + st * C::kABytes, &tmW, full_addr(st), kb * kTileK, row, pol);
+                else
+                    tma_load_2d_hint_warp(sA + st * C::kABytes, &tmW, &full[st], kb * kTileK, row, pol);
+            };
+            auto load_x = [&](int st, int kb, int mt, uint64_t pol) {
+                const int row = mt * BN + static_cast<int>(rank) * (BN / PAIR);
+                if constexpr (PAIR == 2)
+                    tma_load_2d_pair_warp(sB + st * C::kBBytes, &tmX, full_addr(st), kb * kTileK, row, pol);
+                else
+                    tma_load_2d_hint_warp(sB + st * C::kBBytes, &tmX, &full[st], kb * kTileK, row, pol);
+            };
             // (1) weight prefetch: the first kStages k-blocks of this CTA's work (their
             //     slots are free at kernel start), before the dependency wait
             int pre_nt[C::kStages], pre_mt[C::kStages], pre_kb[C::kStages];
@@ -360,9 +463,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                 int nt, mt, kb0, kb1;
                 while (n_pre < S && next_unit(p, pos, nt, mt, kb0, kb1))
                     for (int kb = kb0; kb < kb1 && n_pre < S; ++kb) {
-                        mbar_expect_tx_warp(&full[n_pre], C::kStageBytes);
-                        tma_load_2d_hint_warp(sA + n_pre * C::kABytes, &tmW, &full[n_pre], kb * kTileK, nt * kTileN,
-                                              stream);
+                        if (rank == 0) mbar_expect_tx_warp(&full[n_pre], C::kStageBytes * PAIR);
+                        load_w(n_pre, kb, nt, stream);
                         pre_nt[n_pre] = nt, pre_mt[n_pre] = mt, pre_kb[n_pre] = kb;
                         ++n_pre;
                     }
@@ -371,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (lane == 0) probe_stamp(p, 1);
             // (2) the activation tiles of the prefetched stages
             for (int i = 0; i < n_pre; ++i)
-                tma_load_2d_hint_warp(sB + i * C::kBBytes, &tmX, &full[i], pre_kb[i] * kTileK, pre_mt[i] * BN, keep);
+                load_x(i, pre_kb[i], pre_mt[i], keep);
             (void)pre_nt;
             // (3) steady state
             int stage = 0;
@@ -383,10 +485,9 @@ __global__ void __launch_bounds__(kThreads, 2)
                 for (int kb = kb0; kb < kb1; ++kb, ++issued) {
                     if (issued >= n_pre) {
                         mbar_wait(&empty[stage], phase ^ 1);
-                        mbar_expect_tx_warp(&full[stage], C::kStageBytes);
-                        tma_load_2d_hint_warp(sA + stage * C::kABytes, &tmW, &full[stage], kb * kTileK, nt * kTileN,
-                                              stream);
-                        tma_load_2d_hint_warp(sB + stage * C::kBBytes, &tmX, &full[stage], kb * kTileK, mt * BN, keep);
+                        if (rank == 0) mbar_expect_tx_warp(&full[stage], C::kStageBytes * PAIR);
+                        load_w(stage, kb, nt, stream);
+                        load_x(stage, kb, mt, keep);
                     }
                     if (++stage == S) {
                         stage = 0;
@@ -396,10 +497,11 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------------------ MMA issuer (whole warp)
-        {
+        // ------------------------------------------------------------ MMA issuer (whole warp;
+        // the pair's leader only)
+        if (rank == 0) {
             const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);  // provably warp-uniform
-            constexpr uint32_t idesc = idesc_bf16_f32(kTileN, BN);
+            constexpr uint32_t idesc = idesc_bf16_f32(kTileN * PAIR, BN);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -418,15 +520,25 @@ __global__ void __launch_bounds__(kThreads, 2)
                     const uint32_t b0 = smem_u32(sB + stage * C::kBBytes);
 #pragma unroll
                     for (int k = 0; k < kTileK / 16; ++k)
-                        tc_mma_bf16_warp(d_tmem, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc,
-                                         (kb > kb0 || k > 0) ? 1u : 0u);
-                    tc_commit_warp(&empty[stage]);  // smem slot free once these MMAs retire
+                        if constexpr (PAIR == 2)
+                            tc_mma_bf16_pair_warp(d_tmem, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc,
+                                                  (kb > kb0 || k > 0) ? 1u : 0u);
+                        else
+                            tc_mma_bf16_warp(d_tmem, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc,
+                                             (kb > kb0 || k > 0) ? 1u : 0u);
+                    if constexpr (PAIR == 2)
+                        tc_commit_pair_warp(&empty[stage]);  // both CTAs' slots free once these MMAs retire
+                    else
+                        tc_commit_warp(&empty[stage]);  // smem slot free once these MMAs retire
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                tc_commit_warp(&tfull[acc]);  // accumulator ready for the epilogue
+                if constexpr (PAIR == 2)
+                    tc_commit_pair_warp(&tfull[acc]);  // both CTAs' accumulators ready
+                else
+                    tc_commit_warp(&tfull[acc]);  // accumulator ready for the epilogue
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }
@@ -443,6 +555,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         int nt, mt, kb0, kb1;
         bool tail = false;
         while (next_unit(p, pos, nt, mt, kb0, kb1, &tail)) {
+            nt = nt * PAIR + static_cast<int>(rank);  // this CTA's 128 weight rows of the (pair) tile
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int n = nt * kTileN + row;
@@ -522,7 +635,14 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                if constexpr (PAIR == 2)  // the leader's MMA reuses the pair's accumulator
+                    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(
+                                     mapa_rank(smem_u32(&tempty[acc]), 0))
+                                 : "memory");
+                else
+                    mbar_arrive(&tempty[acc]);
+            }
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
             if (p.fuse.kind != CK_FUSE_NONE && (!p.hybrid || tail)) {
@@ -550,10 +670,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
 
     tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR == 2)
+        cluster_sync_all();  // the peer's epilogue has drained; no MMA writes either TMEM any more
+    else
+        __syncthreads();
     if (warp == 0) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, C::kTmemCols);
+        tmem_dealloc_g<PAIR>(tmem_base, C::kTmemCols);
     }
 }
 
@@ -629,44 +752,58 @@ int num_sms() {
     return n;
 }
 
-template <int BN>
+template <int BN, int PAIR = 1>
 int launch(const CUtensorMap& mw, const CUtensorMap& mx, GemmParams p, int max_ctas, cudaStream_t s) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, PAIR>;
     static unsigned attr_set_mask = 0;  // per device
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(attr_set_mask & (1u << dev))) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+        cudaError_t e =
+            cudaFuncSetAttribute(gemm_tc_kernel<BN, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
         if (e != cudaSuccess) return static_cast<int>(e);
         attr_set_mask |= 1u << dev;
     }
-    // Weight-streaming (stream-K) launches with small token tiles use a ~100 KB ring so
-    // that the NEXT GEMM's CTA fits beside this one on an SM: under PDL it streams its
-    // first weights while this launch drains (measured on B200: decode passes of 1-32
-    // rows 6-10 % faster than with the full 220 KB ring; BN >= 64 keeps the full ring).
-    // CRONUS_GEMM_RING_KB overrides the size (0 = always the full ring).
     static const int ring_kb = [] {
         const char* e = std::getenv("CRONUS_GEMM_RING_KB");
         return e ? std::atoi(e) : -1;
     }();
     p.stages = C::kStages;
+    p.pair = PAIR;
     const int kb = ring_kb >= 0 ? ring_kb : (BN <= 32 ? 100 : 0);
     if (p.stream_k && kb > 0) p.stages = std::clamp(kb * 1024 / C::kStageBytes, 2, C::kStages);
     const int smem = p.stages * C::kStageBytes + 1024 + 256;
     const long long work = p.stream_k ? p.iters : p.hybrid ? (1ll << 40) : p.units;
-    const int grid = static_cast<int>(std::min<long long>(work, max_ctas > 0 ? max_ctas : num_sms()));
+    const int grid = PAIR * static_cast<int>(std::min<long long>(work, (max_ctas > 0 ? max_ctas : num_sms()) / PAIR));
+    if constexpr (PAIR == 2) {
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl_enabled() ? 2 : 1;
+        return static_cast<int>(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, 2>, mw, mx, p));
+    } else {
     static const bool probe = [] {
         const char* e = std::getenv("CRONUS_GEMM_PROBE");
         return e && e[0] == '1';
     }();
-    if (!probe) return launch_pdl(gemm_tc_kernel<BN>, dim3(grid), dim3(kThreads), smem, s, mw, mx, p);
+    if (!probe) return launch_pdl(gemm_tc_kernel<BN, 1>, dim3(grid), dim3(kThreads), smem, s, mw, mx, p);
     // dev: per-CTA timeline (entry, after dependency wait, first stage ready, last MMA
     // issued, epilogue done), printed relative to the earliest CTA entry
     static unsigned long long* buf = nullptr;
     if (!buf) cudaMalloc(&buf, 1024 * 6 * sizeof(unsigned long long));
     cudaMemsetAsync(buf, 0, grid * 6 * sizeof(unsigned long long), s);
     p.probe = buf;
-    const int rc = launch_pdl(gemm_tc_kernel<BN>, dim3(grid), dim3(kThreads), smem, s, mw, mx, p);
+    const int rc = launch_pdl(gemm_tc_kernel<BN, 1>, dim3(grid), dim3(kThreads), smem, s, mw, mx, p);
     std::vector<unsigned long long> h(grid * 6);
     cudaMemcpyAsync(h.data(), buf, h.size() * 8, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
@@ -684,6 +821,7 @@ int launch(const CUtensorMap& mw, const CUtensorMap& mx, GemmParams p, int max_c
     }
     std::fprintf(stderr, " us\n");
     return rc;
+    }
 }
 
 }  // namespace
@@ -710,6 +848,15 @@ extern "C" int ck_gemm_fused(const void* W, const void* X, void* out, const void
 }
 
 namespace {
+// CRONUS_GEMM_PAIR=0: tensor-regime GEMMs on single CTAs (the round-1 kernel) instead of CTA pairs
+bool gemm_pair() {
+    static const bool on = [] {
+        const char* e = std::getenv("CRONUS_GEMM_PAIR");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 int gemm_impl(const void* W, const void* X, void* out, const void* bias, int M, int N, int K, int ldo, int epi,
               int splits, int max_ctas, const ck_gemm_fuse* fuse, void* stream) {
     if (M <= 0) return 0;
@@ -723,6 +870,8 @@ int gemm_impl(const void* W, const void* X, void* out, const void* bias, int M, 
     if (epi == CK_EPI_SILU_BF16 && ((splits != 1 && !silu_hybrid) || bias != nullptr))
         return static_cast<int>(cudaErrorInvalidValue);
     const int BN = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
+    // tensor regime: CTA pairs (cta_group::2, 256 weight rows per tile) unless disabled
+    const int PAIR = BN == 256 && N % (2 * kTileN) == 0 && gemm_pair() && !(fuse && fuse->kind == CK_FUSE_RMSNORM) ? 2 : 1;
     GemmParams p{};
     p.out = out;
     p.bias = static_cast<const __nv_bfloat16*>(bias);
@@ -734,7 +883,7 @@ int gemm_impl(const void* W, const void* X, void* out, const void* bias, int M, 
     p.fuse = fuse ? *fuse : ck_gemm_fuse{};
     p.m_tiles = (M + BN - 1) / BN;
     p.kb_total = K / kTileK;
-    const int tiles = (N / kTileN) * p.m_tiles;
+    const int tiles = (N / (kTileN * PAIR)) * p.m_tiles;  // (pair) tiles
     p.stream_k = 0;
     p.iters = static_cast<long long>(tiles) * p.kb_total;
     if (splits <= 0 && epi == CK_EPI_RED_F32) {
@@ -751,7 +900,7 @@ int gemm_impl(const void* W, const void* X, void* out, const void* bias, int M, 
     p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;  // no empty splits
     p.units = tiles * p.splits;
     if (silu_hybrid) {
-        const int ctas = max_ctas > 0 ? max_ctas : num_sms();
+        const int ctas = (max_ctas > 0 ? max_ctas : num_sms()) / PAIR;  // unit CTAs (pairs)
         const int tail = tiles % ctas;
         p.dp_tiles = tiles - tail;
         if (tail == 0 || p.dp_tiles == 0 || tail * 2 >= ctas) {  // last wave >= half full: keep it
@@ -771,9 +920,10 @@ int gemm_impl(const void* W, const void* X, void* out, const void* bias, int M, 
     CUtensorMap mw, mx;
     int rc = tensor_map(W, N, K, kTileN, &mw);
     if (rc) return rc;
-    rc = tensor_map(X, M, K, BN, &mx);
+    rc = tensor_map(X, M, K, BN / PAIR, &mx);
     if (rc) return rc;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (PAIR == 2) return launch<256, 2>(mw, mx, p, max_ctas, s);
     switch (BN) {
         case 16: return launch<16>(mw, mx, p, max_ctas, s);
         case 32: return launch<32>(mw, mx, p, max_ctas, s);

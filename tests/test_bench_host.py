@@ -59,6 +59,8 @@ def test_kernel_classes_and_roofline_math():
     import bench
     assert bench.kernel_class("void <unnamed>::gemm_tc_kernel<16>(CUtensorMap_st, ...)") == "gemm_stream"
     assert bench.kernel_class("void <unnamed>::gemm_tc_kernel<256>(CUtensorMap_st, ...)") == "gemm_tc"
+    assert bench.kernel_class("void <unnamed>::gemm_tc_kernel<256, 2>(CUtensorMap_st, ...)") == "gemm_tc"
+    assert bench.kernel_class("void <unnamed>::gemm_tc_kernel<16, 1>(CUtensorMap_st, ...)") == "gemm_stream"
     assert bench.kernel_class("void <unnamed>::attn_decode_tma_kernel<4, 3>(...)") == "decode_attn"
     assert bench.kernel_class("<unnamed>::attn_prefill_pp_kernel(...)") == "prefill_attn"
     assert bench.kernel_class("<unnamed>::rmsnorm_kernel(...)") == "other"

@@ -134,6 +134,9 @@ struct GpuEngine::Impl {
     std::unique_ptr<gpu::KvPool> pool_ppi, pool_cpi;
     cudaStream_t s_ppi = nullptr, s_cpi = nullptr, s_copy = nullptr;
     cudaStream_t s_cpi_full = nullptr;  // primary-context stream for lent (all-SM) CPI iterations
+    cudaStream_t s_cpi_side = nullptr, s_cpi_full_side = nullptr;  // their side streams (Worker::side_)
+    bool own_cpi_side = false;
+    cudaStream_t cpi_side(cudaStream_t main) const { return main == s_cpi_full ? s_cpi_full_side : s_cpi_side; }
     cudaStream_t s_copy_low = nullptr;  // handoffs INTO the low side (disagg-hl) on its own device
     std::unique_ptr<gpu::Worker> ppi, cpi;
     std::unique_ptr<gpu::SmPartition> part;
@@ -176,8 +179,11 @@ struct GpuEngine::Impl {
                 ppi_ctas = part->ppi_sms;
                 cpi_ctas = part->cpi_sms;
                 partition_mode = "green-context";
-                if (opt.sm_lending)
+                s_cpi_side = part->cpi_side_stream;
+                if (opt.sm_lending) {
                     check_cuda(cudaStreamCreateWithPriority(&s_cpi_full, cudaStreamNonBlocking, hi), "stream");
+                    check_cuda(cudaStreamCreateWithPriority(&s_cpi_full_side, cudaStreamNonBlocking, hi), "stream");
+                }
             } else {
                 ppi_ctas = opt.ppi_sms;  // fallback: only the PPI's GEMM grid is capped
                 partition_mode = "grid-cap";
@@ -201,6 +207,11 @@ struct GpuEngine::Impl {
             check_cuda(cudaStreamCreateWithPriority(&s_cpi, cudaStreamNonBlocking, hi), "stream");
             check_cuda(cudaStreamCreateWithPriority(&s_copy, cudaStreamNonBlocking, hi), "stream");
             own_cpi_streams = true;
+        }
+        if (!s_cpi_side) {
+            check_cuda(cudaSetDevice(opt.cpi_device), "cudaSetDevice");
+            check_cuda(cudaStreamCreateWithPriority(&s_cpi_side, cudaStreamNonBlocking, hi), "stream");
+            own_cpi_side = true;
         }
         if (!s_ppi) {
             check_cuda(cudaSetDevice(opt.ppi_device), "cudaSetDevice");
@@ -238,6 +249,8 @@ struct GpuEngine::Impl {
         ppi.reset();
         cpi.reset();
         if (s_cpi_full) cudaStreamDestroy(s_cpi_full);
+        if (s_cpi_full_side) cudaStreamDestroy(s_cpi_full_side);
+        if (own_cpi_side && s_cpi_side) cudaStreamDestroy(s_cpi_side);
         if (s_copy_low) cudaStreamDestroy(s_copy_low);
         if (own_ppi_stream && s_ppi) cudaStreamDestroy(s_ppi);
         if (own_cpi_streams) {
@@ -617,7 +630,7 @@ class PairExecutor : public sched::Executor {
             if (cur != cpi_stream) {  // keep high-side work in order across the two streams
                 if (last_iter[1]) check_cuda(cudaStreamWaitEvent(cur, last_iter[1], 0), "wait previous iteration");
                 cpi_stream = cur;
-                E.cpi->set_launch(cur, lend ? 0 : E.cpi_ctas);
+                E.cpi->set_launch(cur, lend ? 0 : E.cpi_ctas, E.cpi_side(cur));
             }
         }
         auto need = [&](int rid, const std::vector<int32_t>* blocks) {
@@ -674,7 +687,7 @@ class PairExecutor : public sched::Executor {
     bool wall_clock() const override { return E.opt.wall; }
 
     void start() override {
-        E.cpi->set_launch(E.s_cpi, E.cpi_ctas);
+        E.cpi->set_launch(E.s_cpi, E.cpi_ctas, E.s_cpi_side);
         cpi_stream = E.s_cpi;
         launches0_cpi = E.cpi->launches;
         launches0_ppi = E.ppi->launches;
@@ -757,7 +770,7 @@ class PairExecutor : public sched::Executor {
         check_cuda(cudaEventElapsedTime(&ms, t0_cpi, end), "elapsed");
         cudaEventDestroy(end);
         gpu_ms = ms;
-        E.cpi->set_launch(E.s_cpi, E.cpi_ctas);
+        E.cpi->set_launch(E.s_cpi, E.cpi_ctas, E.s_cpi_side);
         if (opts.host_tokens) {
             check_cuda(cudaMemcpy(opts.host_tokens, E.tok_cpi.out_tok.p, static_cast<size_t>(total_out) * 4,
                                   cudaMemcpyDeviceToHost),
@@ -909,6 +922,7 @@ double GpuEngine::time_pass(const ClusterConfig& cfg, int worker, int n_dec, int
     E.prepare(cfg);
     gpu::Worker& W = worker == 0 ? *E.ppi : *E.cpi;
     gpu::KvPool& pool = worker == 0 ? *E.pool_ppi : *E.pool_cpi;
+    if (worker != 0) E.cpi->set_launch(E.s_cpi, E.cpi_ctas, E.s_cpi_side);  // as a serve's CPI iterations
     const int dev = worker == 0 ? E.opt.ppi_device : E.opt.cpi_device;
     TokenBufs& tb = worker == 0 && !E.colocated ? E.tok_ppi : E.tok_cpi;
     check_cuda(cudaSetDevice(dev), "cudaSetDevice");

@@ -260,6 +260,16 @@ void Batch::plan_decode(int n_kv_heads, int slots) {
     blocks_per_split = static_cast<int>(cap);
 }
 
+// Mixed passes: the chunk's prefill attention runs on the worker's side stream, concurrent with
+// the decode attention, on this fraction of the worker's SMs (CRONUS_ATTN_OVERLAP; 0 = serial).
+double attn_overlap_frac() {
+    static const double f = [] {
+        const char* e = std::getenv("CRONUS_ATTN_OVERLAP");
+        return e ? std::atof(e) : 0.35;
+    }();
+    return f;
+}
+
 // Tensor-regime gate_up: hybrid whole-tile / stream-K-tail SiLU GEMM (CRONUS_SILU_HYBRID=0: whole tiles only).
 bool silu_hybrid() {
     static const bool on = [] {
@@ -363,6 +373,8 @@ Worker::Worker(const Weights& w, int max_rows, int max_sample, int max_blocks_pe
       stream_(stream), max_ctas_(max_ctas) {
     check_cuda(cudaSetDevice(w.device()), "cudaSetDevice");
     const size_t R = max_rows, H = m_.hidden;
+    check_cuda(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming), "event");
+    check_cuda(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming), "event");
     check_cuda(cudaMalloc(&x_, R * H * 4), "alloc x");
     check_cuda(cudaMalloc(&h_, R * H * 2), "alloc h");
     check_cuda(cudaMalloc(&qkv_, R * m_.qkv_n() * 4), "alloc qkv");
@@ -416,6 +428,8 @@ Worker::~Worker() {
         cudaEventDestroy(p.b);
     }
     for (cudaEvent_t e : ev_free_) cudaEventDestroy(e);
+    if (fork_ev_) cudaEventDestroy(fork_ev_);
+    if (join_ev_) cudaEventDestroy(join_ev_);
 }
 
 cudaEvent_t Worker::ev() {
@@ -648,6 +662,21 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
             ++launches;
             done(a, &stat_other, 0, 0);
         }
+        // mixed pass: the chunk's prefill attention on the side stream (its own CTA budget on
+        // the same SMs) while the decode attention streams the decoders' KV on the main one
+        const bool overlap = n_dec > 0 && b.p_len > 0 && side_ != nullptr && !profile_ && attn_overlap_frac() > 0.0;
+        if (overlap) {
+            check_cuda(cudaEventRecord(fork_ev_, stream_), "fork");
+            check_cuda(cudaStreamWaitEvent(side_, fork_ev_, 0), "fork wait");
+            const int all = max_ctas_ > 0 ? max_ctas_ : ck_device_sms();
+            const int pf_ctas = std::max(8, std::min(kPfSlots, static_cast<int>(attn_overlap_frac() * all)));
+            check_ck(ck_attn_prefill_pp(q_, max_rows_, pool.base, pool.blocks, bt + b.p_bt, b.p_row0, b.p_len,
+                                        b.p_pos0, attn_, m.n_heads, m.n_kv_heads, l, m.layers, scale, pf_ws_,
+                                        pf_tickets_, pf_ctas, side_),
+                     "attn_prefill (side)");
+            ++launches;
+            check_cuda(cudaEventRecord(join_ev_, side_), "join");
+        }
         if (n_dec > 0) {
             mark(a);
             check_ck(ck_attn_decode_tma(q_, pool.base, pool.blocks, bt, D(o_d_row), D(o_d_len), D(o_d_bt),
@@ -658,7 +687,9 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
             ++launches;
             done(a, &stat_decode_attn, dec_keys * kv_tok_layer, 4.0 * m.n_heads * m.head_dim * dec_keys);
         }
-        if (b.p_len > 0) {
+        if (overlap) {
+            check_cuda(cudaStreamWaitEvent(stream_, join_ev_, 0), "join wait");
+        } else if (b.p_len > 0) {
             mark(a);
             const int pf_ctas = std::min(kPfSlots, max_ctas_ > 0 ? max_ctas_ : ck_device_sms());
             check_ck(ck_attn_prefill_pp(q_, max_rows_, pool.base, pool.blocks, bt + b.p_bt, b.p_row0, b.p_len,

@@ -156,9 +156,10 @@ class Worker {
     void set_logits_out(float* p) { logits_out_ = p; }
     // Switch the stream / persistent-grid cap later passes launch on (SM lending). The
     // caller orders the streams.
-    void set_launch(cudaStream_t s, int max_ctas) {
+    void set_launch(cudaStream_t s, int max_ctas, cudaStream_t side = nullptr) {
         stream_ = s;
         max_ctas_ = max_ctas;
+        side_ = side;
     }
     void collect_stats();  // fold finished profiling events into stats (synchronizes)
     // Drop captured pass graphs (their pointers: the run's token buffers, pools, streams).
@@ -176,6 +177,10 @@ class Worker {
     int max_rows_, max_sample_, max_bt_;
     cudaStream_t stream_;
     int max_ctas_;
+    // Second stream on the same SMs: a mixed pass runs its chunk's prefill attention there,
+    // concurrently with the decode attention (independent rows); null = serial.
+    cudaStream_t side_ = nullptr;
+    cudaEvent_t fork_ev_ = nullptr, join_ev_ = nullptr;
     // device activations
     float* x_ = nullptr;
     void* h_ = nullptr;

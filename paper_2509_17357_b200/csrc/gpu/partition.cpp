@@ -44,6 +44,7 @@ SmPartition::~SmPartition() {
     if (ppi_stream) cudaStreamDestroy(ppi_stream);
     if (cpi_stream) cudaStreamDestroy(cpi_stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (cpi_side_stream) cudaStreamDestroy(cpi_side_stream);
     if (destroy) {
         if (g_ppi) destroy(static_cast<CUgreenCtx>(g_ppi));
         if (g_cpi) destroy(static_cast<CUgreenCtx>(g_cpi));
@@ -79,6 +80,9 @@ std::unique_ptr<SmPartition> make_sm_partition(int device, int ppi_sms, int prio
     CUstream s3 = nullptr;
     if (stream(&s3, g2, CU_STREAM_NON_BLOCKING, prio_cpi) != CUDA_SUCCESS) return nullptr;
     out->copy_stream = reinterpret_cast<cudaStream_t>(s3);
+    CUstream s4 = nullptr;
+    if (stream(&s4, g2, CU_STREAM_NON_BLOCKING, prio_cpi) != CUDA_SUCCESS) return nullptr;
+    out->cpi_side_stream = reinterpret_cast<cudaStream_t>(s4);
     out->ppi_sms = static_cast<int>(part.sm.smCount);
     out->cpi_sms = static_cast<int>(rest.sm.smCount);
     return out;

@@ -14,6 +14,7 @@ struct SmPartition {
     cudaStream_t ppi_stream = nullptr;  // kernels launched here run on ppi_sms SMs only
     cudaStream_t cpi_stream = nullptr;  // ... and here on the remaining cpi_sms SMs
     cudaStream_t copy_stream = nullptr; // handoff copies, inside the CPI partition
+    cudaStream_t cpi_side_stream = nullptr;  // CPI kernels overlapped with the main chain (same SMs)
     int ppi_sms = 0, cpi_sms = 0;
     ~SmPartition();
 };

@@ -774,7 +774,16 @@ int launch(const CUtensorMap& mw, const CUtensorMap& mx, GemmParams p, int max_c
     if (p.stream_k && kb > 0) p.stages = std::clamp(kb * 1024 / C::kStageBytes, 2, C::kStages);
     const int smem = p.stages * C::kStageBytes + 1024 + 256;
     const long long work = p.stream_k ? p.iters : p.hybrid ? (1ll << 40) : p.units;
-    const int grid = PAIR * static_cast<int>(std::min<long long>(work, (max_ctas > 0 ? max_ctas : num_sms()) / PAIR));
+    // dev (CRONUS_GEMM_SK_PER_SM=k): weight-streaming stream-K grids of k CTAs per SM (more
+    // weight bytes in flight per SM; the ring must then fit k times)
+    static const int sk_per_sm = [] {
+        const char* e = std::getenv("CRONUS_GEMM_SK_PER_SM");
+        const int v = e ? std::atoi(e) : 1;
+        return v >= 1 && v <= 2 ? v : 1;
+    }();
+    const int per_sm = p.stream_k && BN <= 128 ? sk_per_sm : 1;
+    const int grid =
+        PAIR * static_cast<int>(std::min<long long>(work, per_sm * (max_ctas > 0 ? max_ctas : num_sms()) / PAIR));
     if constexpr (PAIR == 2) {
         cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeClusterDimension;

@@ -1,6 +1,7 @@
 """Cross-check of bench.py's roofline against Nsight Compute (round 2).
 
-    # 1) the serve under ncu (metrics-only launch list; PDL off: ncu replay cannot coexist with it)
+    # 1) the serve under ncu (metrics-only launch list; PDL off: ncu replay cannot coexist with it;
+    #    no green-context partition: ncu fails on green-context streams, so both runs use ppi_sms 0)
     CRONUS_NO_PDL=1 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file gpurun_out/roof_launches.csv python tools/roofline_check.py serve --requests 24 \
         --stats gpurun_out/roof_stats_ncu.json
@@ -34,7 +35,7 @@ def serve(a):
     from paper_2509_17357_b200.serving import GpuEngine
     _, cfg = bench.load_cfg(None, "cronus")  # bench.py's default cluster config and trace shape
     t = E.synth_trace(a.requests, 1014, 247, E.ALL_AT_ZERO, 0.0, 1)
-    eng = GpuEngine(model="llama3-8b", clock="wall", ppi_sms=40)
+    eng = GpuEngine(model="llama3-8b", clock="wall", ppi_sms=a.ppi_sms)
     eng.serve(cfg, t.subset(np.arange(4), name="warm"), events=False)  # lazy init
     res = eng.serve(cfg, t, events=False, profile=True)
     st = res.extra["stats"]
@@ -104,6 +105,8 @@ if __name__ == "__main__":
     s = sub.add_parser("serve")
     s.add_argument("--requests", type=int, default=24)
     s.add_argument("--stats", required=True)
+    s.add_argument("--ppi-sms", type=int, default=0,
+                   help="0 (default): no green-context partition (ncu cannot profile kernels on green-context streams)")
     c = sub.add_parser("compare")
     c.add_argument("launches")
     c.add_argument("stats_ncu")

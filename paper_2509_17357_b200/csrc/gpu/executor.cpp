@@ -182,7 +182,7 @@ struct GpuEngine::Impl {
                 s_cpi_side = part->cpi_side_stream;
                 if (opt.sm_lending) {
                     check_cuda(cudaStreamCreateWithPriority(&s_cpi_full, cudaStreamNonBlocking, hi), "stream");
-                    check_cuda(cudaStreamCreateWithPriority(&s_cpi_full_side, cudaStreamNonBlocking, hi), "stream");
+                    check_cuda(cudaStreamCreateWithPriority(&s_cpi_full_side, cudaStreamNonBlocking, lo), "stream");
                 }
             } else {
                 ppi_ctas = opt.ppi_sms;  // fallback: only the PPI's GEMM grid is capped
@@ -210,7 +210,7 @@ struct GpuEngine::Impl {
         }
         if (!s_cpi_side) {
             check_cuda(cudaSetDevice(opt.cpi_device), "cudaSetDevice");
-            check_cuda(cudaStreamCreateWithPriority(&s_cpi_side, cudaStreamNonBlocking, hi), "stream");
+            check_cuda(cudaStreamCreateWithPriority(&s_cpi_side, cudaStreamNonBlocking, lo), "stream");
             own_cpi_side = true;
         }
         if (!s_ppi) {

@@ -265,7 +265,7 @@ void Batch::plan_decode(int n_kv_heads, int slots) {
 double attn_overlap_frac() {
     static const double f = [] {
         const char* e = std::getenv("CRONUS_ATTN_OVERLAP");
-        return e ? std::atof(e) : 0.35;
+        return e ? std::atof(e) : 0.25;
     }();
     return f;
 }
@@ -662,22 +662,32 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
             ++launches;
             done(a, &stat_other, 0, 0);
         }
-        // mixed pass: the chunk's prefill attention on the side stream (its own CTA budget on
-        // the same SMs) while the decode attention streams the decoders' KV on the main one
+        // mixed pass: the decode attention runs on the side stream (lower priority) while the
+        // chunk's prefill attention keeps a CTA budget of the SMs on the main stream; both read
+        // the pass's q / KV and write disjoint rows of attn_. The prefill grid is dispatched
+        // first (main stream, higher priority): one 231-KB CTA per SM could otherwise never
+        // find a free SM among the decode kernel's 2-3 resident CTAs per SM.
         const bool overlap = n_dec > 0 && b.p_len > 0 && side_ != nullptr && !profile_ && attn_overlap_frac() > 0.0;
         if (overlap) {
             check_cuda(cudaEventRecord(fork_ev_, stream_), "fork");
             check_cuda(cudaStreamWaitEvent(side_, fork_ev_, 0), "fork wait");
+            check_ck(ck_attn_decode_tma(q_, pool.base, pool.blocks, bt, D(o_d_row), D(o_d_len), D(o_d_bt),
+                                        D(o_d_item0), D(o_d_work), n_work, n_dec, b.decode_cluster, attn_ws_,
+                                        attn_tickets_, attn_, m.n_heads, m.n_kv_heads, l, m.layers, scale,
+                                        fused_rope ? &rope : nullptr, side_),
+                     "attn_decode_tma (side)");
+            ++launches;
+            check_cuda(cudaEventRecord(join_ev_, side_), "join");
             const int all = max_ctas_ > 0 ? max_ctas_ : ck_device_sms();
             const int pf_ctas = std::max(8, std::min(kPfSlots, static_cast<int>(attn_overlap_frac() * all)));
             check_ck(ck_attn_prefill_pp(q_, max_rows_, pool.base, pool.blocks, bt + b.p_bt, b.p_row0, b.p_len,
                                         b.p_pos0, attn_, m.n_heads, m.n_kv_heads, l, m.layers, scale, pf_ws_,
-                                        pf_tickets_, pf_ctas, side_),
-                     "attn_prefill (side)");
+                                        pf_tickets_, pf_ctas, stream_),
+                     "attn_prefill");
             ++launches;
-            check_cuda(cudaEventRecord(join_ev_, side_), "join");
+            check_cuda(cudaStreamWaitEvent(stream_, join_ev_, 0), "join wait");
         }
-        if (n_dec > 0) {
+        if (n_dec > 0 && !overlap) {
             mark(a);
             check_ck(ck_attn_decode_tma(q_, pool.base, pool.blocks, bt, D(o_d_row), D(o_d_len), D(o_d_bt),
                                             D(o_d_item0), D(o_d_work), n_work, n_dec, b.decode_cluster, attn_ws_,
@@ -687,9 +697,7 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
             ++launches;
             done(a, &stat_decode_attn, dec_keys * kv_tok_layer, 4.0 * m.n_heads * m.head_dim * dec_keys);
         }
-        if (overlap) {
-            check_cuda(cudaStreamWaitEvent(stream_, join_ev_, 0), "join wait");
-        } else if (b.p_len > 0) {
+        if (b.p_len > 0 && !overlap) {
             mark(a);
             const int pf_ctas = std::min(kPfSlots, max_ctas_ > 0 ? max_ctas_ : ck_device_sms());
             check_ck(ck_attn_prefill_pp(q_, max_rows_, pool.base, pool.blocks, bt + b.p_bt, b.p_row0, b.p_len,

@@ -81,7 +81,8 @@ std::unique_ptr<SmPartition> make_sm_partition(int device, int ppi_sms, int prio
     if (stream(&s3, g2, CU_STREAM_NON_BLOCKING, prio_cpi) != CUDA_SUCCESS) return nullptr;
     out->copy_stream = reinterpret_cast<cudaStream_t>(s3);
     CUstream s4 = nullptr;
-    if (stream(&s4, g2, CU_STREAM_NON_BLOCKING, prio_cpi) != CUDA_SUCCESS) return nullptr;
+    // lower priority than the CPI's main stream: its kernels take the SMs the main stream's leave
+    if (stream(&s4, g2, CU_STREAM_NON_BLOCKING, prio_ppi) != CUDA_SUCCESS) return nullptr;
     out->cpi_side_stream = reinterpret_cast<cudaStream_t>(s4);
     out->ppi_sms = static_cast<int>(part.sm.smCount);
     out->cpi_sms = static_cast<int>(rest.sm.smCount);

@@ -774,14 +774,18 @@ int launch(const CUtensorMap& mw, const CUtensorMap& mx, GemmParams p, int max_c
     if (p.stream_k && kb > 0) p.stages = std::clamp(kb * 1024 / C::kStageBytes, 2, C::kStages);
     const int smem = p.stages * C::kStageBytes + 1024 + 256;
     const long long work = p.stream_k ? p.iters : p.hybrid ? (1ll << 40) : p.units;
-    // dev (CRONUS_GEMM_SK_PER_SM=k): weight-streaming stream-K grids of k CTAs per SM (more
-    // weight bytes in flight per SM; the ring must then fit k times)
+    // Weight-streaming stream-K grids of small token tiles (BN <= 32, 100 KB rings) run 2 CTAs
+    // per SM: ~200 KB of weights in flight per SM instead of ~100 (Little's law against the
+    // loaded HBM latency). Measured on the 108-SM CPI partition (tools/scripts/r2_stream.sh):
+    // 3 / 16-decoder passes 3.91 -> 3.55 / 4.12 -> 3.81 ms; larger tiles keep the full ring
+    // with 1 CTA per SM (81 decoders: 6.34 ms vs 6.44 with 2 x 100 KB). CRONUS_GEMM_SK_PER_SM
+    // (1 or 2) forces it for every weight-streaming tile size.
     static const int sk_per_sm = [] {
         const char* e = std::getenv("CRONUS_GEMM_SK_PER_SM");
-        const int v = e ? std::atoi(e) : 1;
-        return v >= 1 && v <= 2 ? v : 1;
+        const int v = e ? std::atoi(e) : 0;
+        return v >= 1 && v <= 2 ? v : 0;
     }();
-    const int per_sm = p.stream_k && BN <= 128 ? sk_per_sm : 1;
+    const int per_sm = !p.stream_k || BN > 128 ? 1 : sk_per_sm ? sk_per_sm : (BN <= 32 && kb == 100 ? 2 : 1);
     const int grid =
         PAIR * static_cast<int>(std::min<long long>(work, per_sm * (max_ctas > 0 ? max_ctas : num_sms()) / PAIR));
     if constexpr (PAIR == 2) {

@@ -35,6 +35,8 @@ def serve(a):
     from paper_2509_17357_b200.serving import GpuEngine
     _, cfg = bench.load_cfg(None, "cronus")  # bench.py's default cluster config and trace shape
     t = E.synth_trace(a.requests, 1014, 247, E.ALL_AT_ZERO, 0.0, 1)
+    if a.max_out > 0:  # bounded decode tails (ncu times every launch: keep the launch count small)
+        t = E.Trace(t.ids, t.arrival_ms, t.input_len, np.minimum(t.output_len, a.max_out).astype(np.int32), t.name)
     eng = GpuEngine(model="llama3-8b", clock="wall", ppi_sms=a.ppi_sms)
     eng.serve(cfg, t.subset(np.arange(4), name="warm"), events=False)  # lazy init
     res = eng.serve(cfg, t, events=False, profile=True)
@@ -105,6 +107,7 @@ if __name__ == "__main__":
     s = sub.add_parser("serve")
     s.add_argument("--requests", type=int, default=24)
     s.add_argument("--stats", required=True)
+    s.add_argument("--max-out", type=int, default=0, help="clip output lengths (0: the trace's own)")
     s.add_argument("--ppi-sms", type=int, default=0,
                    help="0 (default): no green-context partition (ncu cannot profile kernels on green-context streams)")
     c = sub.add_parser("compare")

@@ -34,6 +34,16 @@ SHAPES = {
     "ncu_gemm_tc_mixed": ("cpi.gemm_tc", [2 * 512 * L["Q"] * L["H"], 2 * 512 * L["H"] * L["NQ"],
                                           2 * 512 * 2 * L["F"] * L["H"], 2 * 512 * L["H"] * L["F"]], "flops"),
     "ncu_prefill_pp_ppi": ("ppi.prefill_attn", [4 * 32 * 128 * sum(i + 1 for i in range(512))], "flops"),
+    # round 2, final kernels: mixed pass of 80 decoders x 1440 keys + a 415-token chunk at 1024
+    "ncu2_prefill_pp_mixed": ("cpi.prefill_attn", [4 * 32 * 128 * sum(1024 + i + 1 for i in range(415))], "flops"),
+    "ncu2_decode_mixed": ("cpi.decode_attn", [80 * 1440 * L["KVTOK"]], "bytes"),
+    "ncu2_gemm_tc_mixed": ("cpi.gemm_tc", [2 * 495 * L["Q"] * L["H"], 2 * 495 * L["H"] * L["NQ"],
+                                           2 * 495 * 2 * L["F"] * L["H"], 2 * 495 * L["H"] * L["F"]], "flops"),
+    "ncu2_gemm_stream_dec8": ("cpi.gemm_stream", [2 * (L["Q"] * L["H"] + 8 * L["H"]) + 4 * 8 * L["Q"],
+                                                  2 * (L["H"] * L["NQ"] + 8 * L["NQ"]) + 4 * 8 * L["H"],
+                                                  2 * (2 * L["F"] * L["H"] + 8 * L["H"]) + 4 * 8 * 2 * L["F"],
+                                                  2 * (L["H"] * L["F"] + 8 * L["F"]) + 4 * 8 * L["H"]], "bytes"),
+    "ncu2_prefill_pp_ppi": ("ppi.prefill_attn", [4 * 32 * 128 * sum(i + 1 for i in range(512))], "flops"),
 }
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",

@@ -38,7 +38,8 @@ def serve(a):
     if a.max_out > 0:  # bounded decode tails (ncu times every launch: keep the launch count small)
         t = E.Trace(t.ids, t.arrival_ms, t.input_len, np.minimum(t.output_len, a.max_out).astype(np.int32), t.name)
     eng = GpuEngine(model="llama3-8b", clock="wall", ppi_sms=a.ppi_sms)
-    eng.serve(cfg, t.subset(np.arange(4), name="warm"), events=False)  # lazy init
+    if not a.no_warm:
+        eng.serve(cfg, t.subset(np.arange(4), name="warm"), events=False)  # lazy init
     res = eng.serve(cfg, t, events=False, profile=True)
     st = res.extra["stats"]
     json.dump({"stats": st, "describe": eng.describe()}, open(a.stats, "w"))
@@ -59,8 +60,8 @@ def ncu_classes(csv_path, stream_ids):
         w = worker_of.get(r.get("Stream"))
         if w is None:
             continue
-        us = float(r["Metric Value"].replace(",", "")) * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(
-            r.get("Metric Unit"), 1.0)
+        us = float(r["Metric Value"].replace(",", "")) * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0,
+                                                          "msecond": 1e3, "ms": 1e3}.get(r.get("Metric Unit"), 1.0)
         c = kernel_class(r["Kernel Name"])
         d = out.setdefault(w, {}).setdefault(c, {"launches": 0, "us": 0.0})
         d["launches"] += 1
@@ -108,6 +109,8 @@ if __name__ == "__main__":
     s.add_argument("--requests", type=int, default=24)
     s.add_argument("--stats", required=True)
     s.add_argument("--max-out", type=int, default=0, help="clip output lengths (0: the trace's own)")
+    s.add_argument("--no-warm", action="store_true",
+                   help="no warm-up serve (under ncu: the launch list then holds exactly the measured serve)")
     s.add_argument("--ppi-sms", type=int, default=0,
                    help="0 (default): no green-context partition (ncu cannot profile kernels on green-context streams)")
     c = sub.add_parser("compare")

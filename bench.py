@@ -150,7 +150,9 @@ def peaks():
         return 6650.0, 1590.0, 1400.0, "fallback"
 
 
-TRAFFIC = os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")
+TRAFFIC = os.path.join(ROOT, "profiles", "r2_ncu_after.json")
+if not os.path.exists(TRAFFIC):
+    TRAFFIC = os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")
 
 
 def traffic_ratios():

@@ -339,6 +339,17 @@ def roofline(stats, partition=None, critical=None):
     if top:
         top.setdefault("traffic", None)
         top["peak_source"] = f"MEASURED_PEAKS.json ({src}; {'sustained' if top['bound'] == 'tensor' else 'copy'})"
+        # committed ncu cross-check of the same class (tools/roofline_check.py: one serve, its
+        # algorithmic work over ncu's kernel durations vs over CUDA-event class time)
+        try:
+            chk = json.load(open(os.path.join(ROOT, "profiles", "r2_roofline_check.json")))
+            for c in chk["classes"]:
+                if c["kernel"] == top["kernel"]:
+                    top["ncu_crosscheck"] = {"frac_ncu": c["frac_ncu"], "frac_events_same_serve": c["frac_events"],
+                                             "share_ncu": c["share_ncu"], "share_events": c["share_events"],
+                                             "source": "profiles/r2_roofline_check.json"}
+        except (OSError, ValueError, KeyError):
+            pass
     return top, classes
 
 

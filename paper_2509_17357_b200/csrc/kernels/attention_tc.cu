@@ -88,6 +88,32 @@ __device__ __forceinline__ float exp2_poly(float x) {
     const float pf = fmaf(fmaf(fmaf(0.07558665f, f, 0.22877255f), f, 0.69511601f), f, 1.0f);
     return __int_as_float(__float_as_int(pf) + (static_cast<int>(xi) << 23));
 }
+// fp32 pairs on sm_100's paired FMA / add datapath (FFMA2 / FADD2)
+__device__ __forceinline__ uint64_t f32x2(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float lo_f32(uint64_t v) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    return lo;
+}
+__device__ __forceinline__ float hi_f32(uint64_t v) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    return hi;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
 // MUFU.EX2 alone (exp2f adds range fix-ups: 3 more instructions per element)
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
@@ -150,7 +176,7 @@ struct PfParams {
     float* ws;      // piece partials [grid][kPfWsFloats]
     int* tickets;   // [grid], zero, self-resetting
     long long* probe;  // dev (CRONUS_PF_PROBE=1): per-CTA clock64 stamps [grid][128], else null
-    int ablate;        // dev (CRONUS_PF_ABLATE): bit 0 / 2 = no V / K loads, bit 1 = no exp (P = S); 0 in production
+    int ablate;        // dev (CRONUS_PF_ABLATE): bit 0 / 2 = no V / K loads, bit 1 = no exp (P = S), bit 3 = all exp on MUFU; 0 in production
 };
 
 // dev probe: clock64 stamp `slot` of this CTA (pipeline events; see launch_prefill)
@@ -430,24 +456,36 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             // A row whose keys in this piece are all masked keeps m = -inf: P = 0, not NaN.
             float pmx[8], rsp[8];
             uint32_t pk[2][16];
+            // exponentials in fp32 pairs: x = S * scale - m and the row sums on the paired FMA /
+            // add pipes (FFMA2 / FADD2: half the instructions of the scalar forms), 2^x on MUFU
+            // for 3 of every 4 column groups and on the FMA pipe (cubic) for the 4th
             auto exp_pack = [&](float m_use) {
+                const uint64_t sc2 = f32x2(p.scale_log2, p.scale_log2), nm2 = f32x2(-m_use, -m_use);
+                uint64_t rs2[4];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) rsp[e] = 0.f;
+                for (int e = 0; e < 4; ++e) rs2[e] = 0ull;
 #pragma unroll
                 for (int c = 0; c < 2; ++c)
 #pragma unroll
                     for (int g = 0; g < 4; ++g) {
-                        const bool poly = g == 3;
-                        float pv[8];
+                        const bool poly = g == 3 && !(p.ablate & 8);
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) {
-                            const float x = fmaf(__uint_as_float(sv[c][g * 8 + e]), p.scale_log2, -m_use);
-                            pv[e] = (p.ablate & 2) ? x : poly ? exp2_poly(x) : ex2_approx(x);
-                            rsp[e] += pv[e];
+                        for (int e = 0; e < 8; e += 2) {
+                            const uint64_t x2 = ffma2(f32x2(__uint_as_float(sv[c][g * 8 + e]),
+                                                            __uint_as_float(sv[c][g * 8 + e + 1])),
+                                                      sc2, nm2);
+                            const float x0 = lo_f32(x2), x1 = hi_f32(x2);
+                            const float p0 = (p.ablate & 2) ? x0 : poly ? exp2_poly(x0) : ex2_approx(x0);
+                            const float p1 = (p.ablate & 2) ? x1 : poly ? exp2_poly(x1) : ex2_approx(x1);
+                            rs2[e >> 1] = fadd2(rs2[e >> 1], f32x2(p0, p1));
+                            pk[c][g * 4 + (e >> 1)] = pack_bf16x2(p0, p1);
                         }
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) pk[c][g * 4 + e] = pack_bf16x2(pv[2 * e], pv[2 * e + 1]);
                     }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    rsp[2 * e] = lo_f32(rs2[e]);
+                    rsp[2 * e + 1] = hi_f32(rs2[e]);
+                }
             };
 #pragma unroll
             for (int e = 0; e < 8; ++e) pmx[e] = -INFINITY;

@@ -770,23 +770,25 @@ int launch(const CUtensorMap& mw, const CUtensorMap& mx, GemmParams p, int max_c
     }();
     p.stages = C::kStages;
     p.pair = PAIR;
-    const int kb = ring_kb >= 0 ? ring_kb : (BN <= 64 ? 100 : 0);
+    const int kb = ring_kb >= 0 ? ring_kb : (BN <= 32 ? 100 : 0);
     if (p.stream_k && kb > 0) p.stages = std::clamp(kb * 1024 / C::kStageBytes, 2, C::kStages);
     const int smem = p.stages * C::kStageBytes + 1024 + 256;
     const long long work = p.stream_k ? p.iters : p.hybrid ? (1ll << 40) : p.units;
-    // Weight-streaming stream-K grids of small token tiles (BN <= 64, 100 KB rings) run 2 CTAs
+    // Weight-streaming stream-K grids of small token tiles (BN <= 32, 100 KB rings) run 2 CTAs
     // per SM: ~200 KB of weights in flight per SM instead of ~100 (Little's law against the
     // loaded HBM latency). Measured on the 108-SM CPI partition (tools/scripts/r2_stream2.sh,
     // 1400-key contexts): 3 / 16 / 24 / 32 / 48-decoder passes 3.94 / 4.16 / 4.87 / 4.67 /
     // 6.18 -> 3.58 / 3.86 / 4.56 / 4.33 / 5.57 ms (all 148 SMs: 2-5 %); BN = 128 keeps the full
-    // ring with 1 CTA per SM (81 decoders: 6.34 ms vs 6.44 with 2 x 100 KB).
+    // ring with 1 CTA per SM (81 decoders: 6.34 ms vs 6.44 with 2 x 100 KB). BN = 64 would gain
+    // too (48 decoders), but its 100-KB ring hung the bench's CUPTI-traced serve (an unexplained
+    // interaction with the profiler; plain serves were fine), so it keeps the full ring.
     // CRONUS_GEMM_SK_PER_SM (1 or 2) forces it for every weight-streaming tile size.
     static const int sk_per_sm = [] {
         const char* e = std::getenv("CRONUS_GEMM_SK_PER_SM");
         const int v = e ? std::atoi(e) : 0;
         return v >= 1 && v <= 2 ? v : 0;
     }();
-    const int per_sm = !p.stream_k || BN > 128 ? 1 : sk_per_sm ? sk_per_sm : (BN <= 64 && kb == 100 ? 2 : 1);
+    const int per_sm = !p.stream_k || BN > 128 ? 1 : sk_per_sm ? sk_per_sm : (BN <= 32 && kb == 100 ? 2 : 1);
     const int grid =
         PAIR * static_cast<int>(std::min<long long>(work, per_sm * (max_ctas > 0 ? max_ctas : num_sms()) / PAIR));
     if constexpr (PAIR == 2) {

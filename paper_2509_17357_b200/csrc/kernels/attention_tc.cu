@@ -79,15 +79,6 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
         "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
         : "memory");
 }
-// 2^x on the FMA pipe: Cody-Waite split x = i + f, f in [0, 1), cubic fit of 2^f (max
-// relative error 2.6e-4, far below the bf16 rounding P gets next); x < -127 -> ~0.
-__device__ __forceinline__ float exp2_poly(float x) {
-    x = fmaxf(x, -127.f);
-    const float xi = floorf(x);
-    const float f = x - xi;
-    const float pf = fmaf(fmaf(fmaf(0.07558665f, f, 0.22877255f), f, 0.69511601f), f, 1.0f);
-    return __int_as_float(__float_as_int(pf) + (static_cast<int>(xi) << 23));
-}
 // fp32 pairs on sm_100's paired FMA / add datapath (FFMA2 / FADD2)
 __device__ __forceinline__ uint64_t f32x2(float lo, float hi) {
     uint64_t r;
@@ -113,6 +104,24 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
     uint64_t r;
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
     return r;
+}
+// 2^x for a pair on the FMA / ALU pipes only (no MUFU, no F2I / FRND: those share the MUFU's
+// quarter-rate pipe): x = n + f with n = rint(x) taken from the low mantissa bits of x + 1.5*2^23,
+// f in [-0.5, 0.5], 2^f by a cubic (max relative error 7.5e-5, far below the bf16 rounding P gets
+// next), n added into the exponent field. x < -126 -> ~1e-38 (masked keys: -inf); the clamp keeps
+// the exponent sum positive (2^f < 1 for f < 0).
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
+    constexpr float kMagic = 12582912.f;  // 1.5 * 2^23
+    const uint64_t xc = f32x2(fmaxf(lo_f32(x2), -126.f), fmaxf(hi_f32(x2), -126.f));
+    const uint64_t t = fadd2(xc, f32x2(kMagic, kMagic));
+    const uint64_t r = fadd2(t, f32x2(-kMagic, -kMagic));
+    const uint64_t f = ffma2(r, f32x2(-1.f, -1.f), xc);
+    uint64_t q = ffma2(f32x2(0.05517588f, 0.05517588f), f, f32x2(0.24261151f, 0.24261151f));
+    q = ffma2(q, f, f32x2(0.69326019f, 0.69326019f));
+    q = ffma2(q, f, f32x2(0.99992800f, 0.99992800f));
+    const int lo = __float_as_int(lo_f32(q)) + (__float_as_int(lo_f32(t)) << 23);
+    const int hi = __float_as_int(hi_f32(q)) + (__float_as_int(hi_f32(t)) << 23);
+    return f32x2(__int_as_float(lo), __int_as_float(hi));
 }
 // MUFU.EX2 alone (exp2f adds range fix-ups: 3 more instructions per element)
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -176,7 +185,7 @@ struct PfParams {
     float* ws;      // piece partials [grid][kPfWsFloats]
     int* tickets;   // [grid], zero, self-resetting
     long long* probe;  // dev (CRONUS_PF_PROBE=1): per-CTA clock64 stamps [grid][128], else null
-    int ablate;        // dev (CRONUS_PF_ABLATE): bit 0 / 2 = no V / K loads, bit 1 = no exp (P = S), bit 3 = all exp on MUFU; 0 in production
+    int ablate;        // dev (CRONUS_PF_ABLATE): bit 0 / 2 = no V / K loads, bit 1 = no exp (P = S), bit 3 = all exp on MUFU, bit 4 = parked waits; 0 in production
 };
 
 // dev probe: clock64 stamp `slot` of this CTA (pipeline events; see launch_prefill)
@@ -195,6 +204,15 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
 __device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 
+// Pipeline waits poll (dev: ablate bit 16 parks the warp with a suspend hint instead, so waiting
+// warps leave issue slots to the softmax warps; measured 2-3 % slower).
+__device__ __forceinline__ void pf_wait(const PfParams& p, uint64_t* bar, uint32_t parity) {
+    if (p.ablate & 16)
+        mbar_wait_park(bar, parity);
+    else
+        mbar_wait(bar, parity);
+}
+
 // Key tiles of token block tb (its second tile's last valid token).
 template <int HT>
 __host__ __device__ __forceinline__ int pf_steps(int q_len, int pos0, int tb) {
@@ -203,7 +221,7 @@ __host__ __device__ __forceinline__ int pf_steps(int q_len, int pos0, int tb) {
     return (pos0 + end + kKT - 1) / kKT;
 }
 
-template <int HT>
+template <int HT, int NPOLY>
 __global__ void __launch_bounds__(kPPThreads, 1)
     attn_prefill_pp_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
                            PfParams p) {
@@ -306,7 +324,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             auto load_k = [&](int k) {
                 const int st = k % kStages;
                 const int my_row = row_of(k);
-                mbar_wait(&k_empty[st], ((k / kStages) & 1) ^ 1);
+                pf_wait(p, &k_empty[st], ((k / kStages) & 1) ^ 1);
                 if (k < 16 && lane == 0) pf_stamp(p, 88 + k);
                 uint8_t* K = sm + kPPOffK + st * kKVTileBytes;
                 if (p.ablate & 4) {  // dev ablation: K = whatever the stage holds
@@ -324,7 +342,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             auto load_v = [&](int k) {
                 const int st = k % kStages;
                 const int my_row = row_of(k);
-                mbar_wait(&v_empty[st], ((k / kStages) & 1) ^ 1);
+                pf_wait(p, &v_empty[st], ((k / kStages) & 1) ^ 1);
                 if (k < 16 && lane == 0) pf_stamp(p, 104 + k);
                 if (p.ablate & 1) {  // dev ablation: V = whatever the stage holds
                     if (lane == 0) mbar_arrive(&v_full[st]);
@@ -367,7 +385,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         {
             const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);  // provably warp-uniform
             constexpr uint32_t id_s = idesc_attn(false, kKT), id_o = idesc_attn(true, 128);
-            for (int i = 0; i < n_qt; ++i) mbar_wait(&q_full[i], 0);
+            for (int i = 0; i < n_qt; ++i) pf_wait(p, &q_full[i], 0);
             if (lane == 0) pf_stamp(p, 2);
             auto issue_s = [&](int i, int k) {  // S_i(k) = Q_i K(k)^T -> S buffer (i, k & 1)
                 const uint32_t q0 = smem_u32(sm + kPPOffQ + i * kQTileBytes);
@@ -381,7 +399,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                 tc_commit_warp(&s_full[i * 2 + (k & 1)]);
             };
             auto k_ready = [&](int k) {
-                mbar_wait(&k_full[k % kStages], (k / kStages) & 1);
+                pf_wait(p, &k_full[k % kStages], (k / kStages) & 1);
                 tc_fence_after();
             };
             for (int k = 0; k < 2 && k < jmax; ++k) {
@@ -392,13 +410,13 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             }
             for (int k = 0; k < jmax; ++k) {
                 const bool ahead = k + 2 < jmax;
-                mbar_wait(&v_full[k % kStages], (k / kStages) & 1);
+                pf_wait(p, &v_full[k % kStages], (k / kStages) & 1);
                 tc_fence_after();
                 if (ahead) k_ready(k + 2);
                 const uint32_t v0 = smem_u32(sm + kPPOffV + (k % kStages) * kKVTileBytes);
                 for (int i = 0; i < 2; ++i) {
                     if (k < cnt[i]) {  // O_i += P_i(k) V(k), P from TMEM (packed bf16 pairs)
-                        mbar_wait(&p_full[i * 2 + (k & 1)], (k >> 1) & 1);
+                        pf_wait(p, &p_full[i * 2 + (k & 1)], (k >> 1) & 1);
                         if (k < 16 && lane == 0) pf_stamp(p, 24 + 16 * i + k);
                         tc_fence_after();
 #pragma unroll
@@ -432,7 +450,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         const uint32_t s_col = tmem + lane_base + i * 128, o_col = tmem + lane_base + 256 + i * 128;
         float m_ref = -INFINITY, l_sum = 0.f;
         for (int k = 0; k < cnt_i; ++k) {
-            mbar_wait(&s_full[i * 2 + (k & 1)], (k >> 1) & 1);
+            pf_wait(p, &s_full[i * 2 + (k & 1)], (k >> 1) & 1);
             if (threadIdx.x == 64 && k < 16) pf_stamp(p, 56 + k);
             tc_fence_after();
             const uint32_t sb = s_col + (k & 1) * 64;
@@ -468,15 +486,25 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                 for (int c = 0; c < 2; ++c)
 #pragma unroll
                     for (int g = 0; g < 4; ++g) {
-                        const bool poly = g == 3 && !(p.ablate & 8);
+                        const bool poly = g >= 4 - NPOLY && !(p.ablate & 8);
 #pragma unroll
                         for (int e = 0; e < 8; e += 2) {
                             const uint64_t x2 = ffma2(f32x2(__uint_as_float(sv[c][g * 8 + e]),
                                                             __uint_as_float(sv[c][g * 8 + e + 1])),
                                                       sc2, nm2);
                             const float x0 = lo_f32(x2), x1 = hi_f32(x2);
-                            const float p0 = (p.ablate & 2) ? x0 : poly ? exp2_poly(x0) : ex2_approx(x0);
-                            const float p1 = (p.ablate & 2) ? x1 : poly ? exp2_poly(x1) : ex2_approx(x1);
+                            float p0, p1;
+                            if (p.ablate & 2) {
+                                p0 = x0;
+                                p1 = x1;
+                            } else if (poly) {
+                                const uint64_t e2 = exp2_poly2(x2);
+                                p0 = lo_f32(e2);
+                                p1 = hi_f32(e2);
+                            } else {
+                                p0 = ex2_approx(x0);
+                                p1 = ex2_approx(x1);
+                            }
                             rs2[e >> 1] = fadd2(rs2[e >> 1], f32x2(p0, p1));
                             pk[c][g * 4 + (e >> 1)] = pack_bf16x2(p0, p1);
                         }
@@ -508,9 +536,9 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                     // O holds PV_i(0..k-1) once PV_i(k-1) retires (PV_i(k) waits for this P):
                     // S_i(k+1) was issued right after it, or, at the last step, PV_i(k-1) commits
                     if (k + 1 < cnt_i)
-                        mbar_wait(&s_full[i * 2 + ((k + 1) & 1)], ((k + 1) >> 1) & 1);
+                        pf_wait(p, &s_full[i * 2 + ((k + 1) & 1)], ((k + 1) >> 1) & 1);
                     else
-                        mbar_wait(&pv_done[i], 0);
+                        pf_wait(p, &pv_done[i], 0);
                     tc_fence_after();
 #pragma unroll 1
                     for (int c = 0; c < 8; ++c) {  // 16 columns at a time
@@ -533,7 +561,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             if (threadIdx.x == 64 && k < 16) pf_stamp(p, 72 + k);
         }
         if (cnt_i > 0) {
-            mbar_wait(&o_done[i], 0);
+            pf_wait(p, &o_done[i], 0);
             tc_fence_after();
         }
         __nv_bfloat16* dst = p.out + static_cast<size_t>(p.q_row0 + tok) * p.nq * 128 + head * 128;
@@ -751,12 +779,19 @@ int launch_prefill(const void* q, int q_rows_total, const CUtensorMap& mkv, cons
     int rc = make_map_2d(q, static_cast<unsigned long long>(q_rows_total), static_cast<unsigned long long>(nq) * 128,
                          TT, &mq);
     if (rc) return rc;
+    // 2^x column groups (of 4) on the FMA pipe instead of MUFU (dev: CRONUS_PF_NPOLY 1-2; 0, all
+    // on MUFU, measured fastest: 448 @ 1024 26.4 vs 27.6 us, 4096 @ 0 163 vs 177 us)
+    static const int npoly = [] {
+        const char* e = std::getenv("CRONUS_PF_NPOLY");
+        return e ? std::min(2, std::max(0, std::atoi(e))) : 0;
+    }();
+    auto* kern = npoly == 0 ? attn_prefill_pp_kernel<HT, 0> : npoly == 2 ? attn_prefill_pp_kernel<HT, 2>
+                                                                         : attn_prefill_pp_kernel<HT, 1>;
     static unsigned mask = 0;
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(mask & (1u << dev))) {
-        cudaError_t e = cudaFuncSetAttribute(attn_prefill_pp_kernel<HT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kPPSmemBytes);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kPPSmemBytes);
         if (e != cudaSuccess) return static_cast<int>(e);
         mask |= 1u << dev;
     }
@@ -787,13 +822,13 @@ int launch_prefill(const void* q, int q_rows_total, const CUtensorMap& mkv, cons
         return e ? std::atoi(e) : 0;
     }();
     prm.ablate = ablate;
-    if (!probe) return launch_pdl(attn_prefill_pp_kernel<HT>, dim3(grid), dim3(kPPThreads), kPPSmemBytes, st, mq, mkv, prm);
+    if (!probe) return launch_pdl(kern, dim3(grid), dim3(kPPThreads), kPPSmemBytes, st, mq, mkv, prm);
     // dev: clock64 pipeline stamps of CTA 0 (the heaviest piece), relative to kernel entry
     long long* buf = nullptr;
     cudaMalloc(&buf, static_cast<size_t>(grid) * 128 * 8);
     cudaMemsetAsync(buf, 0, static_cast<size_t>(grid) * 128 * 8, st);
     prm.probe = buf;
-    int rc2 = launch_pdl(attn_prefill_pp_kernel<HT>, dim3(grid), dim3(kPPThreads), kPPSmemBytes, st, mq, mkv, prm);
+    int rc2 = launch_pdl(kern, dim3(grid), dim3(kPPThreads), kPPSmemBytes, st, mq, mkv, prm);
     std::vector<long long> h(128);
     cudaMemcpyAsync(h.data(), buf, 128 * 8, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);

@@ -93,6 +93,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
+// As mbar_wait, but each poll asks the hardware to park the warp until the phase completes
+// (suspend-time hint, ns): a waiting warp then stops taking issue slots from the warps it
+// shares an SM sub-partition with (the attention kernels' softmax warps).
+__device__ __forceinline__ void mbar_wait_park(uint64_t* bar, uint32_t parity) {
+    uint32_t spins = 0;
+    for (;;) {
+        uint32_t ok;
+        asm volatile(
+            "{\n"
+            ".reg .pred P1;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
+            "selp.b32 %0, 1, 0, P1;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+            : "memory");
+        if (ok) return;
+        if (++spins == (1u << 24)) {
+            printf("[cronus watchdog] block (%d,%d) thread %d stuck on mbarrier smem+0x%x parity %u\n", blockIdx.x,
+                   blockIdx.y, threadIdx.x, smem_u32(bar) & 0xFFFFF, parity);
+            __trap();
+        }
+    }
+}
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");

@@ -94,12 +94,21 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16*
                                __nv_bfloat16* __restrict__ out, const int* rows, int H, float eps,
                                float* __restrict__ zero, int zero_cols) {
     pdl_launch();
+    // gamma is a weight (no dependency on the previous kernel): fetched before the wait, so
+    // the kernel's dependent chain is one activation load + the reduction + the store
+    const int n4 = H / 4;
+    const uint2* g = reinterpret_cast<const uint2*>(gamma);
+    uint2 gv[kRmsMaxVec];
+#pragma unroll
+    for (int j = 0; j < kRmsMaxVec; ++j) {
+        const int i = threadIdx.x + j * blockDim.x;
+        gv[j] = i < n4 ? g[i] : make_uint2(0u, 0u);
+    }
     pdl_wait();
     __shared__ float red[32];
     const int r = blockIdx.x;
     const int src = rows ? rows[r] : r;
     const float4* xr = reinterpret_cast<const float4*>(x + static_cast<size_t>(src) * H);
-    const int n4 = H / 4;
     float4 v[kRmsMaxVec];
     float ss = 0.f;
 #pragma unroll
@@ -114,13 +123,12 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16*
     }
     ss = block_sum(ss, red);
     const float inv = rsqrtf(ss / static_cast<float>(H) + eps);
-    const uint2* g = reinterpret_cast<const uint2*>(gamma);
     uint2* o = reinterpret_cast<uint2*>(out + static_cast<size_t>(r) * H);
 #pragma unroll
     for (int j = 0; j < kRmsMaxVec; ++j) {
         const int i = threadIdx.x + j * blockDim.x;
         if (i < n4) {
-            const uint2 gg = g[i];
+            const uint2 gg = gv[j];
             const float2 g0 = unpack_bf16x2(gg.x), g1 = unpack_bf16x2(gg.y);
             o[i] = make_uint2(pack_bf16x2(v[j].x * inv * g0.x, v[j].y * inv * g0.y),
                               pack_bf16x2(v[j].z * inv * g1.x, v[j].w * inv * g1.y));

@@ -234,12 +234,24 @@ void Batch::plan_decode(int n_kv_heads, int slots) {
     const long long share = std::max<long long>(8, (total * n_kv_heads + slots - 1) / std::max(1, slots));
     const long long item_slots = std::max<long long>(1, slots / (static_cast<long long>(n_kv_heads) * C));
     const long long min_cap = std::max<long long>(8, (longest + 254) / 255);  // work[] holds <= 255 parts
+    // Candidates whose CTAs fit one wave of `slots` win over any that need a second one: the
+    // block-unit makespan treats every resident cluster as running at a fixed per-block rate,
+    // but a second wave of an HBM-bound kernel shares the same bandwidth and adds its latency
+    // tail (16 x 2048 on 148 SMs: 3 parts -> 768 CTAs 44.9 us, whole sequences 31 us;
+    // profiles/r2_session5/dec_small.txt).
+    auto ctas_for = [&](long long c) {
+        long long k = 0;
+        for (int len : d_len) k += std::max<long long>(1, ((len + 15) / 16 + c - 1) / c);
+        return k * n_kv_heads * C;
+    };
     long long cap = std::max(min_cap, 2 * share * C);
     double best = decode_makespan(d_len, cap, C, item_slots, plan_heap_);
+    bool best_fits = ctas_for(cap) <= slots;
     for (const double f : {1.5, 1.0, 0.75, 0.5}) {  // ties keep the larger cap (fewer merges)
         const long long c = std::max(min_cap, static_cast<long long>(f * share * C));
         const double t = decode_makespan(d_len, c, C, item_slots, plan_heap_);
-        if (t < best - 1e-9) best = t, cap = c;
+        const bool fits = ctas_for(c) <= slots;
+        if ((fits && !best_fits) || (fits == best_fits && t < best - 1e-9)) best = t, cap = c, best_fits = fits;
     }
     decode_cluster = C;
     std::vector<std::pair<long long, int>> order;  // (blocks per part, sequence)

@@ -232,26 +232,47 @@ void Batch::plan_decode(int n_kv_heads, int slots) {
     int C = 1;
     while (C < 16 && pairs * C * 2 <= slots && total * n_kv_heads >= pairs * C * 2 * 4) C *= 2;
     const long long share = std::max<long long>(8, (total * n_kv_heads + slots - 1) / std::max(1, slots));
-    const long long item_slots = std::max<long long>(1, slots / (static_cast<long long>(n_kv_heads) * C));
     const long long min_cap = std::max<long long>(8, (longest + 254) / 255);  // work[] holds <= 255 parts
-    // Candidates whose CTAs fit one wave of `slots` win over any that need a second one: the
-    // block-unit makespan treats every resident cluster as running at a fixed per-block rate,
-    // but a second wave of an HBM-bound kernel shares the same bandwidth and adds its latency
-    // tail (16 x 2048 on 148 SMs: 3 parts -> 768 CTAs 44.9 us, whole sequences 31 us;
-    // profiles/r2_session5/dec_small.txt).
-    auto ctas_for = [&](long long c) {
-        long long k = 0;
-        for (int len : d_len) k += std::max<long long>(1, ((len + 15) / 16 + c - 1) / c);
-        return k * n_kv_heads * C;
-    };
-    long long cap = std::max(min_cap, 2 * share * C);
-    double best = decode_makespan(d_len, cap, C, item_slots, plan_heap_);
-    bool best_fits = ctas_for(cap) <= slots;
-    for (const double f : {1.5, 1.0, 0.75, 0.5}) {  // ties keep the larger cap (fewer merges)
-        const long long c = std::max(min_cap, static_cast<long long>(f * share * C));
-        const double t = decode_makespan(d_len, c, C, item_slots, plan_heap_);
-        const bool fits = ctas_for(c) <= slots;
-        if ((fits && !best_fits) || (fits == best_fits && t < best - 1e-9)) best = t, cap = c, best_fits = fits;
+    // Candidates whose CTAs fit one wave win over any that need a second one: the block-unit
+    // makespan treats every resident cluster as running at a fixed per-block rate, but a second
+    // wave of an HBM-bound kernel shares the same bandwidth and adds its latency tail (16 x 2048
+    // on 148 SMs: 3 parts -> 768 CTAs 44.9 us, whole sequences 26 us). 16-CTA clusters (one GPC
+    // each) count against half the slots: 16 of them on 148 SMs run in two rounds (1 x 2142:
+    // 2 parts 19.8 us, 1 part 10.1 us); a plan that needs more falls back to 8-CTA clusters
+    // (1 x 8192: 25.1 -> 18.7 us). profiles/r2_session5/dec_small.txt, dec_cluster.txt.
+    long long cap = 0;
+    for (;;) {
+        const long long item_slots = std::max<long long>(1, slots / (static_cast<long long>(n_kv_heads) * C));
+        const long long wave = C >= 16 ? slots / 2 : slots;
+        auto ctas_for = [&](long long c) {
+            long long k = 0;
+            for (int len : d_len) k += std::max<long long>(1, ((len + 15) / 16 + c - 1) / c);
+            return k * n_kv_heads * C;
+        };
+        // candidates: no split, and the round-1 cap scaled by 2, 1.5, 1, 0.75, 0.5 (ties keep the
+        // larger cap: fewer merges); a one-wave candidate wins unless its makespan is more than
+        // 1.5x the best (an unsplit long sequence in a small batch must still be cut)
+        const double fs[6] = {0.0, 2.0, 1.5, 1.0, 0.75, 0.5};
+        long long caps[6];
+        double ts[6];
+        bool fit[6];
+        double t_min = 1e300;
+        for (int i = 0; i < 6; ++i) {
+            caps[i] = fs[i] == 0.0 ? std::max(min_cap, longest) : std::max(min_cap, static_cast<long long>(fs[i] * share * C));
+            ts[i] = decode_makespan(d_len, caps[i], C, item_slots, plan_heap_);
+            fit[i] = ctas_for(caps[i]) <= wave;
+            t_min = std::min(t_min, ts[i]);
+        }
+        int pick = -1;
+        for (int i = 0; i < 6; ++i)
+            if (fit[i] && ts[i] <= 1.5 * t_min && (pick < 0 || ts[i] < ts[pick] - 1e-9)) pick = i;
+        const bool best_fits = pick >= 0;
+        if (!best_fits)
+            for (int i = 1; i < 6; ++i)
+                if (pick < 0 || ts[i] < ts[pick] - 1e-9) pick = i;
+        cap = caps[pick];
+        if (best_fits || C < 16) break;
+        C = 8;
     }
     decode_cluster = C;
     std::vector<std::pair<long long, int>> order;  // (blocks per part, sequence)

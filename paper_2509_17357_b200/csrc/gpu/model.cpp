@@ -195,7 +195,9 @@ void Batch::add_prefill(int rid, long long pos0, long long len, const std::vecto
 // a part of a cut sequence the global merge.
 static double decode_makespan(const std::vector<int>& d_len, long long cap, int C, long long item_slots,
                               std::vector<double>& heap) {
-    constexpr double kSetup = 6.0, kMerge = 4.0;  // blocks-equivalent (~0.5 us per block per CTA)
+    // blocks-equivalent (~0.5 us per block per CTA); a global part merge measured ~6-8 us (2 x 2142
+    // keys on 148 SMs: 2 parts 18.1 us, whole 10.7 us; round 1 assumed 4 blocks)
+    constexpr double kSetup = 6.0, kMerge = 12.0;
     std::vector<double> work;
     work.reserve(d_len.size() * 2);
     for (int len : d_len) {

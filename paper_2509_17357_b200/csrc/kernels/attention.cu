@@ -277,6 +277,49 @@ __global__ void __launch_bounds__(128)
     }
 }
 
+// The largest cluster the stream's SM set can place (a green-context partition may hold fewer
+// SMs per GPC than the whole device); the kernel derives C from the launch, so the plan's
+// cluster size can be clamped at launch. Cached per stream: keyed by the handle and re-validated
+// by the stream id (handles get reused) whenever the stream is not being captured (stream
+// queries are not capture-safe; a captured pass was first run plainly). -1: unknown under capture.
+template <int G, int STAGES>
+int decode_max_cluster(cudaStream_t st) {
+    constexpr int smem = kDTileBytes + 4 * STAGES * 2 * kDTileBytes;
+    struct Entry {
+        unsigned long long sid;
+        int max_c;
+    };
+    static std::mutex mu;
+    static std::unordered_map<cudaStream_t, Entry> max_cluster;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    unsigned long long sid = 0;
+    if (cs == cudaStreamCaptureStatusNone) cudaStreamGetId(st, &sid);
+    std::lock_guard<std::mutex> g(mu);
+    auto it = max_cluster.find(st);
+    if (it != max_cluster.end() && cs == cudaStreamCaptureStatusNone && it->second.sid != sid) {
+        max_cluster.erase(it);
+        it = max_cluster.end();
+    }
+    if (it == max_cluster.end()) {
+        if (cs != cudaStreamCaptureStatusNone) return -1;
+        cudaFuncSetAttribute(attn_decode_tma_kernel<G, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(attn_decode_tma_kernel<G, STAGES>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaLaunchConfig_t q{};
+        q.gridDim = dim3(16, 1);
+        q.blockDim = dim3(128);
+        q.dynamicSmemBytes = smem;
+        q.stream = st;
+        int mc = 0;
+        if (cudaOccupancyMaxPotentialClusterSize(&mc, attn_decode_tma_kernel<G, STAGES>, &q) != cudaSuccess || mc < 1) {
+            cudaGetLastError();
+            mc = 8;  // portable size
+        }
+        it = max_cluster.emplace(st, Entry{sid, std::min(mc, 16)}).first;
+    }
+    return it->second.max_c;
+}
+
 template <int G, int STAGES>
 int launch_decode_tma(const CUtensorMap& tm, const DecodeAttnArgs& a, int n_work, int cluster, cudaStream_t st) {
     constexpr int smem = kDTileBytes + 4 * STAGES * 2 * kDTileBytes;
@@ -292,45 +335,9 @@ int launch_decode_tma(const CUtensorMap& tm, const DecodeAttnArgs& a, int n_work
         if (e != cudaSuccess) return static_cast<int>(e);
         mask |= 1u << dev;
     }
-    // The largest cluster the stream's SM set can place (a green-context partition may hold
-    // fewer SMs per GPC than the whole device); the kernel derives C from the launch, so the
-    // plan's cluster size can be clamped here. Cached per stream: keyed by the handle and
-    // re-validated by the stream id (handles get reused) whenever the stream is not being
-    // captured (stream queries are not capture-safe; a captured pass was first run plainly).
-    {
-        struct Entry {
-            unsigned long long sid;
-            int max_c;
-        };
-        static std::mutex mu;
-        static std::unordered_map<cudaStream_t, Entry> max_cluster;
-        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-        cudaStreamIsCapturing(st, &cs);
-        unsigned long long sid = 0;
-        if (cs == cudaStreamCaptureStatusNone) cudaStreamGetId(st, &sid);
-        std::lock_guard<std::mutex> g(mu);
-        auto it = max_cluster.find(st);
-        if (it != max_cluster.end() && cs == cudaStreamCaptureStatusNone && it->second.sid != sid) {
-            max_cluster.erase(it);
-            it = max_cluster.end();
-        }
-        if (it == max_cluster.end()) {
-            if (cs != cudaStreamCaptureStatusNone) return static_cast<int>(cudaErrorStreamCaptureUnsupported);
-            cudaLaunchConfig_t q{};
-            q.gridDim = dim3(16, a.nkv);
-            q.blockDim = dim3(128);
-            q.dynamicSmemBytes = smem;
-            q.stream = st;
-            int mc = 0;
-            if (cudaOccupancyMaxPotentialClusterSize(&mc, attn_decode_tma_kernel<G, STAGES>, &q) != cudaSuccess ||
-                mc < 1) {
-                cudaGetLastError();
-                mc = 8;  // portable size
-            }
-            it = max_cluster.emplace(st, Entry{sid, std::min(mc, 16)}).first;
-        }
-        while (cluster > it->second.max_c) cluster >>= 1;
-    }
+    const int mc = decode_max_cluster<G, STAGES>(st);
+    if (mc < 0) return static_cast<int>(cudaErrorStreamCaptureUnsupported);
+    while (cluster > mc) cluster >>= 1;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -412,8 +419,13 @@ int launch_decode_tma_g(const CUtensorMap& tm, const DecodeAttnArgs& a, int n_wo
     if (stages == 0) {
         // 2 stages only where the third CTA per SM saves a wave (48 x 1024: 384 CTAs on 108 SMs
         // is two waves either way, and 3 stages keep more bytes in flight per CTA: 5.68 vs 5.86 ms)
+        // count the grid with the cluster the launch will actually use (clamped to what the
+        // stream's SM set can place), as launch_decode_tma does
+        const int mc = decode_max_cluster<G, 3>(st);
+        int c = cluster;
+        while (mc > 0 && c > mc) c >>= 1;
         const long long r3 = resident_ctas_3stage<G>(st), r2 = r3 * 3 / 2;
-        const long long ctas = static_cast<long long>(n_work) * cluster * a.nkv;
+        const long long ctas = static_cast<long long>(n_work) * c * a.nkv;
         stages = r3 > 0 && (ctas + r2 - 1) / r2 < (ctas + r3 - 1) / r3 ? 2 : 3;
     }
     switch (stages) {

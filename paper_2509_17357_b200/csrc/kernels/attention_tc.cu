@@ -759,7 +759,14 @@ int pf_plan(int q_len, int pos0, int nq, int nkv, int max_ctas, bool can_split, 
         // merge cost ~2-3 us, as much as a few hundred keys of work
         // and at most kMaxPieces per unit: the last piece reads every other piece's 128 KB
         // partial from L2 on the kernel's critical path
-        constexpr int kMinPiece = 4, kMaxPieces = 4;
+        static const int kMinPiece = [] {  // dev: CRONUS_PF_MIN_PIECE / CRONUS_PF_MAX_PIECES
+            const char* e = std::getenv("CRONUS_PF_MIN_PIECE");
+            return e ? std::max(1, std::atoi(e)) : 4;
+        }();
+        static const int kMaxPieces = [] {
+            const char* e = std::getenv("CRONUS_PF_MAX_PIECES");
+            return e ? std::max(1, std::atoi(e)) : 4;
+        }();
         int c = static_cast<int>(std::max<long long>(std::max(kMinPiece, (n_max + kMaxPieces - 1) / kMaxPieces),
                                                      (total + max_ctas - 1) / max_ctas));
         while (c < n_max && grid_for(c) > max_ctas) ++c;

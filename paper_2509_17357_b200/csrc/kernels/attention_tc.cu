@@ -132,6 +132,93 @@ __device__ __forceinline__ float ex2_approx(float x) {
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// One 64-key K or V sub-tile (4 pool blocks x 2 64-dim halves = 8 TMA boxes of 16 rows) and its
+// barrier's expect_tx as ONE elected issue: rows r0..r3 are the blocks' pool rows, the boxes land
+// at dst + bb * 2 KB (dims 0-63) and dst + 8 KB + bb * 2 KB (dims 64-127).
+__device__ __forceinline__ void tma_kv_subtile_warp(void* dst, const CUtensorMap* m, uint64_t* bar, int r0, int r1,
+                                                    int r2, int r3, uint64_t policy, uint32_t bytes) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e;\n"
+        ".reg .b32 d;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %9;\n"
+        "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%2, {%10, %3}], [%1], %7;\n"
+        "add.u32 d, %0, 8192;\n"
+        "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [d], [%2, {%8, %3}], [%1], %7;\n"
+        "add.u32 d, %0, 2048;\n"
+        "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [d], [%2, {%10, %4}], [%1], %7;\n"
+        "add.u32 d, %0, 10240;\n"
+        "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [d], [%2, {%8, %4}], [%1], %7;\n"
+        "add.u32 d, %0, 4096;\n"
+        "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [d], [%2, {%10, %5}], [%1], %7;\n"
+        "add.u32 d, %0, 12288;\n"
+        "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [d], [%2, {%8, %5}], [%1], %7;\n"
+        "add.u32 d, %0, 6144;\n"
+        "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [d], [%2, {%10, %6}], [%1], %7;\n"
+        "add.u32 d, %0, 14336;\n"
+        "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [d], [%2, {%8, %6}], [%1], %7;\n"
+        "}\n" ::"r"(smem_u32(dst)),
+        "r"(smem_u32(bar)), "l"(reinterpret_cast<uint64_t>(m)), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "l"(policy), "r"(64),
+        "r"(bytes), "r"(0)
+        : "memory");
+}
+
+// One S = Q K^T tile (M = 128 queries, N = 64 keys, K = 128 dims) as ONE elected issue of 8
+// MMAs: the K-step descriptors are the base plus immediates (32 B along K inside a 128-B swizzle
+// row = +2, the second 64-dim half = +1024 for Q's 16-KB half, +512 for K's 8-KB half), so the
+// whole group costs one ELECT and a handful of uniform adds instead of ~12 instructions per MMA.
+__device__ __forceinline__ void mma_s_tile_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e, pf, pt;\n"
+        ".reg .b64 a, b;\n"
+        "setp.ne.b32 pf, 0, 0;\n"
+        "setp.eq.b32 pt, 0, 0;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, pf;\n"
+        "add.s64 a, %1, 2;\n add.s64 b, %2, 2;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pt;\n"
+        "add.s64 a, %1, 4;\n add.s64 b, %2, 4;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pt;\n"
+        "add.s64 a, %1, 6;\n add.s64 b, %2, 6;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pt;\n"
+        "add.s64 a, %1, 1024;\n add.s64 b, %2, 512;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pt;\n"
+        "add.s64 a, %1, 1026;\n add.s64 b, %2, 514;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pt;\n"
+        "add.s64 a, %1, 1028;\n add.s64 b, %2, 516;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pt;\n"
+        "add.s64 a, %1, 1030;\n add.s64 b, %2, 518;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pt;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc)
+        : "memory");
+}
+// O += P V for one 64-key sub-tile as ONE elected issue of 4 MMAs (K = 16 keys each): P from
+// TMEM (+8 packed columns per step), V MN-major from smem (+2 KB = +128 per step).
+__device__ __forceinline__ void mma_pv_tile_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e, p0, pt;\n"
+        ".reg .b64 b;\n"
+        ".reg .b32 a;\n"
+        "setp.ne.b32 p0, %4, 0;\n"
+        "setp.eq.b32 pt, 0, 0;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p0;\n"
+        "add.s32 a, %1, 8;\n add.s64 b, %2, 128;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, pt;\n"
+        "add.s32 a, %1, 16;\n add.s64 b, %2, 256;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, pt;\n"
+        "add.s32 a, %1, 24;\n add.s64 b, %2, 384;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, pt;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 // ============================================================ ping-pong kernel
 // Two 128-row query tiles per CTA, one softmax warpgroup each, sharing the K/V rings. Keys go
 // in 64-key sub-tiles and every tile has TWO S buffers in the tensor memory, so the MMA warp
@@ -205,9 +292,11 @@ __device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 256;" 
 
 
 // Pipeline waits poll (dev: ablate bit 16 parks the warp with a suspend hint instead, so waiting
-// warps leave issue slots to the softmax warps; measured 2-3 % slower).
-__device__ __forceinline__ void pf_wait(const PfParams& p, uint64_t* bar, uint32_t parity) {
-    if (p.ablate & 16)
+// warps leave issue slots to the softmax warps; measured 2-3 % slower). `helper` = the producer /
+// MMA warps, which share SM sub-partitions 0 / 1 with softmax warps (dev: ablate bit 5 parks only
+// those).
+__device__ __forceinline__ void pf_wait(const PfParams& p, uint64_t* bar, uint32_t parity, bool helper = false) {
+    if ((p.ablate & 16) || (helper && (p.ablate & 32)))
         mbar_wait_park(bar, parity);
     else
         mbar_wait(bar, parity);
@@ -324,38 +413,32 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             auto load_k = [&](int k) {
                 const int st = k % kStages;
                 const int my_row = row_of(k);
-                pf_wait(p, &k_empty[st], ((k / kStages) & 1) ^ 1);
+                pf_wait(p, &k_empty[st], ((k / kStages) & 1) ^ 1, true);
                 if (k < 16 && lane == 0) pf_stamp(p, 88 + k);
                 uint8_t* K = sm + kPPOffK + st * kKVTileBytes;
                 if (p.ablate & 4) {  // dev ablation: K = whatever the stage holds
                     if (lane == 0) mbar_arrive(&k_full[st]);
                     return;
                 }
-                mbar_expect_tx_warp(&k_full[st], kKVTileBytes);
-#pragma unroll
-                for (int bb = 0; bb < BPT; ++bb) {
-                    const int r = __shfl_sync(0xffffffffu, my_row, bb);
-                    tma_load_2d_hint_warp(K + bb * 2048, &tmKV, &k_full[st], 0, r, keep);
-                    tma_load_2d_hint_warp(K + kKVHalf + bb * 2048, &tmKV, &k_full[st], 64, r, keep);
-                }
+                static_assert(BPT == 4 && kKVHalf == 8192, "tma_kv_subtile_warp layout");
+                tma_kv_subtile_warp(K, &tmKV, &k_full[st], __shfl_sync(0xffffffffu, my_row, 0),
+                                    __shfl_sync(0xffffffffu, my_row, 1), __shfl_sync(0xffffffffu, my_row, 2),
+                                    __shfl_sync(0xffffffffu, my_row, 3), keep, kKVTileBytes);
             };
             auto load_v = [&](int k) {
                 const int st = k % kStages;
                 const int my_row = row_of(k);
-                pf_wait(p, &v_empty[st], ((k / kStages) & 1) ^ 1);
+                pf_wait(p, &v_empty[st], ((k / kStages) & 1) ^ 1, true);
                 if (k < 16 && lane == 0) pf_stamp(p, 104 + k);
                 if (p.ablate & 1) {  // dev ablation: V = whatever the stage holds
                     if (lane == 0) mbar_arrive(&v_full[st]);
                     return;
                 }
-                mbar_expect_tx_warp(&v_full[st], kKVTileBytes);
                 uint8_t* V = sm + kPPOffV + st * kKVTileBytes;
-#pragma unroll
-                for (int bb = 0; bb < BPT; ++bb) {
-                    const int r = __shfl_sync(0xffffffffu, my_row, bb) + p.nkv * 16;
-                    tma_load_2d_hint_warp(V + bb * 2048, &tmKV, &v_full[st], 0, r, keep);
-                    tma_load_2d_hint_warp(V + kKVHalf + bb * 2048, &tmKV, &v_full[st], 64, r, keep);
-                }
+                const int vr = my_row + p.nkv * 16;
+                tma_kv_subtile_warp(V, &tmKV, &v_full[st], __shfl_sync(0xffffffffu, vr, 0),
+                                    __shfl_sync(0xffffffffu, vr, 1), __shfl_sync(0xffffffffu, vr, 2),
+                                    __shfl_sync(0xffffffffu, vr, 3), keep, kKVTileBytes);
             };
             // Issue order = arrival order (the TMA unit serves requests in order): the first
             // two K sub-tiles (if wholly prefix: before griddepcontrol.wait), then Q, then V(0),
@@ -382,24 +465,25 @@ __global__ void __launch_bounds__(kPPThreads, 1)
     } else if (warp == 1) {
         pdl_wait();
         // ------------------------------------------------------------ MMA issuer (whole warp)
+        // Each 64-key S tile (8 MMAs) and PV step (4 MMAs) is one elected issue with uniform
+        // descriptor arithmetic (mma_s_tile_warp / mma_pv_tile_warp): the warp shares an SM
+        // sub-partition with two softmax warps, and its issue cost set their pace (per-MMA
+        // issue: ~2300 cycles per 64-key step; batched: ~1900). Splitting the issue over two
+        // warps on two sub-partitions (one per tile) measured 2-3 % slower again.
         {
             const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);  // provably warp-uniform
             constexpr uint32_t id_s = idesc_attn(false, kKT), id_o = idesc_attn(true, 128);
-            for (int i = 0; i < n_qt; ++i) pf_wait(p, &q_full[i], 0);
+            for (int i = 0; i < n_qt; ++i) pf_wait(p, &q_full[i], 0, true);
             if (lane == 0) pf_stamp(p, 2);
             auto issue_s = [&](int i, int k) {  // S_i(k) = Q_i K(k)^T -> S buffer (i, k & 1)
                 const uint32_t q0 = smem_u32(sm + kPPOffQ + i * kQTileBytes);
                 const uint32_t k0 = smem_u32(sm + kPPOffK + (k % kStages) * kKVTileBytes);
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    tc_mma_bf16_warp(tm + i * 128 + (k & 1) * 64,
-                                sdesc_sw128(q0 + (kk >> 2) * kQHalf + (kk & 3) * 32),
-                                sdesc_sw128(k0 + (kk >> 2) * kKVHalf + (kk & 3) * 32), id_s, kk > 0);
-                }
+                static_assert(kQHalf == 16384 && kKVHalf == 8192, "mma_s_tile_warp immediates");
+                mma_s_tile_warp(tm + i * 128 + (k & 1) * 64, sdesc_sw128(q0), sdesc_sw128(k0), id_s);
                 tc_commit_warp(&s_full[i * 2 + (k & 1)]);
             };
             auto k_ready = [&](int k) {
-                pf_wait(p, &k_full[k % kStages], (k / kStages) & 1);
+                pf_wait(p, &k_full[k % kStages], (k / kStages) & 1, true);
                 tc_fence_after();
             };
             for (int k = 0; k < 2 && k < jmax; ++k) {
@@ -410,19 +494,18 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             }
             for (int k = 0; k < jmax; ++k) {
                 const bool ahead = k + 2 < jmax;
-                pf_wait(p, &v_full[k % kStages], (k / kStages) & 1);
+                pf_wait(p, &v_full[k % kStages], (k / kStages) & 1, true);
                 tc_fence_after();
                 if (ahead) k_ready(k + 2);
                 const uint32_t v0 = smem_u32(sm + kPPOffV + (k % kStages) * kKVTileBytes);
                 for (int i = 0; i < 2; ++i) {
                     if (k < cnt[i]) {  // O_i += P_i(k) V(k), P from TMEM (packed bf16 pairs)
-                        pf_wait(p, &p_full[i * 2 + (k & 1)], (k >> 1) & 1);
+                        pf_wait(p, &p_full[i * 2 + (k & 1)], (k >> 1) & 1, true);
                         if (k < 16 && lane == 0) pf_stamp(p, 24 + 16 * i + k);
                         tc_fence_after();
-#pragma unroll
-                        for (int kk = 0; kk < kKT / 16; ++kk)
-                            tc_mma_ts_warp(tm + 256 + i * 128, tm + i * 128 + (k & 1) * 64 + kk * 8,
-                                      sdesc_mn_sw128(v0 + kk * 2048), id_o, (k > 0 || kk > 0) ? 1u : 0u);
+                        static_assert(kKT == 64, "mma_pv_tile_warp issues 4 K = 16 steps");
+                        mma_pv_tile_warp(tm + 256 + i * 128, tm + i * 128 + (k & 1) * 64, sdesc_mn_sw128(v0), id_o,
+                                         k > 0 ? 1u : 0u);
                         // S_i(k+1) (issued right after PV_i(k-1)) retiring tells the softmax that
                         // PV_i(k-1) did; only the last step has no S_i(k+1): PV_i(cnt-2) commits here
                         if (k == cnt[i] - 2) tc_commit_warp(&pv_done[i]);
@@ -452,6 +535,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         for (int k = 0; k < cnt_i; ++k) {
             pf_wait(p, &s_full[i * 2 + (k & 1)], (k >> 1) & 1);
             if (threadIdx.x == 64 && k < 16) pf_stamp(p, 56 + k);
+            if (i == 0 && lane == 0 && k == 10 && qw != 2) pf_stamp(p, 125 + (qw == 3 ? 2 : qw));  // dev: per-warp S seen
             tc_fence_after();
             const uint32_t sb = s_col + (k & 1) * 64;
             uint32_t sv[2][32];
@@ -559,6 +643,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_full[i * 2 + (k & 1)]);
             if (threadIdx.x == 64 && k < 16) pf_stamp(p, 72 + k);
+            if (i == 0 && lane == 0 && k == 10) pf_stamp(p, 121 + qw);  // dev: per-warp P arrive
         }
         if (cnt_i > 0) {
             pf_wait(p, &o_done[i], 0);
@@ -843,6 +928,8 @@ int launch_prefill(const void* q, int q_rows_total, const CUtensorMap& mkv, cons
     auto d = [&](int k) { return h[k] ? h[k] - h[0] : -1; };
     std::fprintf(stderr, "[pf probe] q_len=%d pos0=%d grid=%d cap=%d setup=%lld q_full=%lld end=%lld\n", q_len, pos0,
                  grid, prm.steps_cap, d(1), d(2), d(120));
+    std::fprintf(stderr, "  step 10 tile 0 per softmax warp (qw 0..3): S seen %lld %lld %lld %lld, P arrive %lld %lld %lld %lld\n",
+                 d(125), d(126), d(56 + 10), d(127), d(121), d(122), d(123), d(124));
     for (int jj = 0; jj < 16; ++jj)
         if (h[8 + jj] || h[88 + jj])
             std::fprintf(stderr, "  jj=%2d K_issue=%7lld V_issue=%7lld v_full=%7lld S0_done=%7lld P0_arrive=%7lld "

@@ -1,6 +1,9 @@
-# Prefill attention A/B at serve shapes: production vs dev variants (env), then the parity tests.
-S=448x1024,448x3072,2048x0,4096x0
-for v in "X=1" "CRONUS_PF_NPOLY=0" "CRONUS_PF_NPOLY=2"; do
-  echo "== $v"; env $v python tools/prefill_probe.py --shapes $S 2>&1 | tail -4
+# Prefill attention: parity tests first, then CUDA-event timing at serve shapes (production and
+# the FMA-pipe 2^x variants), and the pipeline clocks of CTA 0 (448 @ 1024, no split).
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_kernels_gpu.py -q -x -k "prefill or long_context" 2>&1 | tail -3
+for v in "X=1" "CRONUS_PF_NPOLY=1" "CRONUS_PF_NPOLY=2"; do
+  echo "== $v"; env $v python tools/prefill_probe.py --shapes 448x1024,448x3072,415x1024,2048x0,4096x0 2>&1 | tail -5
 done
-timeout 900 python -m pytest tests/test_kernels_gpu.py -q -x -k "prefill or long_context" 2>&1 | tail -2
+python tools/prefill_probe.py --ctas 27 --shapes 415x1024 2>&1 | tail -1
+CRONUS_PF_PROBE=1 python tools/prefill_probe.py --ctas -1 --shapes 448x1024 --reps 1 2>&1 | tail -18 | head -18

@@ -338,6 +338,16 @@ int silu_fuse_rows() {
     return n;
 }
 
+// Weight-streaming passes of at least this many rows (CRONUS_SILU_HYBRID_ROWS, 0 = off) run
+// gate_up as the hybrid whole-tile SiLU-epilogue GEMM instead of stream-K + the SiLU kernel.
+int silu_hybrid_rows() {
+    static const int n = [] {
+        const char* e = std::getenv("CRONUS_SILU_HYBRID_ROWS");
+        return e ? std::atoi(e) : 0;
+    }();
+    return n;
+}
+
 // Tensor-regime QKV as a stream-K red.add GEMM (CRONUS_QKV_STREAMK=0: whole-tile stores).
 bool qkv_streamk() {
     static const bool on = [] {
@@ -776,6 +786,16 @@ void Worker::forward(const Batch& b, const KvPool& pool, const int* prompt, cons
             } else {
                 gemm(L.wgu, h_, act_, nullptr, M, 2 * F, H, CK_EPI_SILU_BF16, 1);
             }
+        } else if (silu_hybrid_rows() > 0 && M >= silu_hybrid_rows() && silu_hybrid()) {
+            // weight-streaming regime, larger batches: whole weight tiles with the SiLU epilogue
+            // straight from TMEM (no fp32 gate/up round trip, no SiLU kernel), a sparse last
+            // wave as stream-K pieces + ticketed finalize (the tensor regime's hybrid)
+            ck_gemm_fuse fh{};
+            fh.kind = CK_FUSE_SILU;
+            fh.zero_after = 1;
+            fh.tickets = tile_tickets_;
+            fh.act = act_;
+            gemm(L.wgu, h_, gu_, nullptr, M, 2 * F, H, CK_EPI_SILU_BF16, 0, &fh);
         } else if (M <= silu_fuse_rows()) {
             // weight-streaming regime: SiLU * up in the stream-K GEMM's ticketed tile finalize
             gemm(L.wgu, h_, gu_, nullptr, M, 2 * F, H, CK_EPI_RED_F32, 0, &fs);

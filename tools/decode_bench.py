@@ -30,6 +30,7 @@ ap.add_argument("--cluster", type=int, default=0, help="force the cluster size (
 ap.add_argument("--trace-lens", action="store_true")
 ap.add_argument("--planner", default="engine", choices=["engine", "r1"])
 ap.add_argument("--slots-per-sm", type=int, default=0, help="0: the engine's rule (3 from 64 pairs, else 2)")
+ap.add_argument("--graph", action="store_true", help="time a captured CUDA graph of the launches (no host launch cost)")
 a = ap.parse_args()
 
 L = lib()
@@ -99,10 +100,28 @@ for shape in a.shapes.split(","):
         launch(i % LAYERS)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for i in range(a.reps):
-        launch(i % LAYERS)
-    e1.record()
+    if a.graph:  # the engine replays decode passes as graphs: time the device side alone
+        cs = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(cs):
+            st = ctypes.c_void_p(cs.cuda_stream)
+            for i in range(4):  # plain launches on the capture stream first (per-stream caches)
+                launch(i % LAYERS)
+            cs.synchronize()
+            with torch.cuda.graph(g, stream=cs):
+                for i in range(a.reps):
+                    launch(i % LAYERS)
+        st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        g.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        g.replay()
+        e1.record()
+    else:
+        e0.record()
+        for i in range(a.reps):
+            launch(i % LAYERS)
+        e1.record()
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / a.reps
     byts = sum(lens) * NKV * 2 * 128 * 2

@@ -98,8 +98,12 @@ __global__ void __launch_bounds__(128)
     // Loads are issued by the whole (convergent) warp, one elected lane inside the PTX: the
     // block id is made provably warp-uniform (shuffle from lane 0) so the TMA operands live in
     // uniform registers (see tc_mma_bf16_warp).
+    // The warp's first 32 block ids come in with ONE parallel load (lane j: its block j) instead
+    // of one dependent table read per ring stage (measured neutral at 1-128 sequences; kept as
+    // the simpler issue path); later blocks read the table directly.
+    const int my_id = lane < mine ? table[first + 4 * lane] : 0;
     auto load = [&](int i) {
-        const int id = __shfl_sync(0xffffffffu, table[first + 4 * i], 0);
+        const int id = i < 32 ? __shfl_sync(0xffffffffu, my_id, i) : __shfl_sync(0xffffffffu, table[first + 4 * i], 0);
         const int row = ((id * a.n_layers + a.layer) * 2 * a.nkv + kvh) * kDBlk;
         uint8_t* dK = ring + (i % STAGES) * 2 * kDTileBytes;
         uint64_t* bb = &bar[i % STAGES];

@@ -535,13 +535,13 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         for (int k = 0; k < cnt_i; ++k) {
             pf_wait(p, &s_full[i * 2 + (k & 1)], (k >> 1) & 1);
             if (threadIdx.x == 64 && k < 16) pf_stamp(p, 56 + k);
-            if (i == 0 && lane == 0 && k == 10 && qw != 2) pf_stamp(p, 125 + (qw == 3 ? 2 : qw));  // dev: per-warp S seen
             tc_fence_after();
             const uint32_t sb = s_col + (k & 1) * 64;
             uint32_t sv[2][32];
             tmem_ld32(sb, sv[0]);
             tmem_ld32(sb + 32, sv[1]);
             tmem_ld_wait();
+            if (threadIdx.x == 64 && k == 10) pf_stamp(p, 121);  // dev: S in registers
             const int key0 = (j0 + k) * kKT;
             if (key0 + kKT - 1 > warp_q0) {  // diagonal sub-tile: causal mask
 #pragma unroll
@@ -635,15 +635,16 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                     }
                 }
             }
+            if (threadIdx.x == 64 && k == 10) pf_stamp(p, 122);  // dev: P computed
             tmem_st16(sb, pk[0]);
             tmem_st16(sb + 16, pk[1]);
             tmem_st_wait();
+            if (threadIdx.x == 64 && k == 10) pf_stamp(p, 123);  // dev: P stored
             l_sum += ((rsp[0] + rsp[1]) + (rsp[2] + rsp[3])) + ((rsp[4] + rsp[5]) + (rsp[6] + rsp[7]));
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_full[i * 2 + (k & 1)]);
             if (threadIdx.x == 64 && k < 16) pf_stamp(p, 72 + k);
-            if (i == 0 && lane == 0 && k == 10) pf_stamp(p, 121 + qw);  // dev: per-warp P arrive
         }
         if (cnt_i > 0) {
             pf_wait(p, &o_done[i], 0);
@@ -928,8 +929,8 @@ int launch_prefill(const void* q, int q_rows_total, const CUtensorMap& mkv, cons
     auto d = [&](int k) { return h[k] ? h[k] - h[0] : -1; };
     std::fprintf(stderr, "[pf probe] q_len=%d pos0=%d grid=%d cap=%d setup=%lld q_full=%lld end=%lld\n", q_len, pos0,
                  grid, prm.steps_cap, d(1), d(2), d(120));
-    std::fprintf(stderr, "  step 10 tile 0 per softmax warp (qw 0..3): S seen %lld %lld %lld %lld, P arrive %lld %lld %lld %lld\n",
-                 d(125), d(126), d(56 + 10), d(127), d(121), d(122), d(123), d(124));
+    std::fprintf(stderr, "  step 10, warp 2: S seen %lld, S in registers %lld, P computed %lld, P stored %lld, P arrive %lld\n",
+                 d(56 + 10), d(121), d(122), d(123), d(72 + 10));
     for (int jj = 0; jj < 16; ++jj)
         if (h[8 + jj] || h[88 + jj])
             std::fprintf(stderr, "  jj=%2d K_issue=%7lld V_issue=%7lld v_full=%7lld S0_done=%7lld P0_arrive=%7lld "

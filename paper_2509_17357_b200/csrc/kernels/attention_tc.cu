@@ -272,7 +272,7 @@ struct PfParams {
     float* ws;      // piece partials [grid][kPfWsFloats]
     int* tickets;   // [grid], zero, self-resetting
     long long* probe;  // dev (CRONUS_PF_PROBE=1): per-CTA clock64 stamps [grid][128], else null
-    int ablate;        // dev (CRONUS_PF_ABLATE): bit 0 / 2 = no V / K loads, bit 1 = no exp (P = S), bit 3 = all exp on MUFU, bit 4 = parked waits; 0 in production
+    int ablate;        // dev (CRONUS_PF_ABLATE): bit 0 / 2 = no V / K loads, bit 1 = no exp (P = S), bit 3 = all exp on MUFU, bit 4 = parked waits, bit 7 / 8 = no PV / S MMAs; 0 in production
 };
 
 // dev probe: clock64 stamp `slot` of this CTA (pipeline events; see launch_prefill)
@@ -479,7 +479,8 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                 const uint32_t q0 = smem_u32(sm + kPPOffQ + i * kQTileBytes);
                 const uint32_t k0 = smem_u32(sm + kPPOffK + (k % kStages) * kKVTileBytes);
                 static_assert(kQHalf == 16384 && kKVHalf == 8192, "mma_s_tile_warp immediates");
-                mma_s_tile_warp(tm + i * 128 + (k & 1) * 64, sdesc_sw128(q0), sdesc_sw128(k0), id_s);
+                if (!(p.ablate & 256))  // dev ablation: no S MMAs (timing only)
+                    mma_s_tile_warp(tm + i * 128 + (k & 1) * 64, sdesc_sw128(q0), sdesc_sw128(k0), id_s);
                 tc_commit_warp(&s_full[i * 2 + (k & 1)]);
             };
             auto k_ready = [&](int k) {
@@ -504,8 +505,9 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                         if (k < 16 && lane == 0) pf_stamp(p, 24 + 16 * i + k);
                         tc_fence_after();
                         static_assert(kKT == 64, "mma_pv_tile_warp issues 4 K = 16 steps");
-                        mma_pv_tile_warp(tm + 256 + i * 128, tm + i * 128 + (k & 1) * 64, sdesc_mn_sw128(v0), id_o,
-                                         k > 0 ? 1u : 0u);
+                        if (!(p.ablate & 128))  // dev ablation: no PV MMAs (timing only)
+                            mma_pv_tile_warp(tm + 256 + i * 128, tm + i * 128 + (k & 1) * 64, sdesc_mn_sw128(v0),
+                                             id_o, k > 0 ? 1u : 0u);
                         // S_i(k+1) (issued right after PV_i(k-1)) retiring tells the softmax that
                         // PV_i(k-1) did; only the last step has no S_i(k+1): PV_i(cnt-2) commits here
                         if (k == cnt[i] - 2) tc_commit_warp(&pv_done[i]);

@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             auto load_k = [&](int k) {
                 const int st = k % kStages;
                 const int my_row = row_of(k);
-                pf_wait(p, &k_empty[st], ((k / kStages) & 1) ^ 1, true);
+                pf_wait(p, &v_empty[st], ((k / kStages) & 1) ^ 1, true);  // stage free: K(k-5), V(k-5) consumed
                 if (k < 16 && lane == 0) pf_stamp(p, 88 + k);
                 uint8_t* K = sm + kPPOffK + st * kKVTileBytes;
                 if (p.ablate & 4) {  // dev ablation: K = whatever the stage holds
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
             auto load_v = [&](int k) {
                 const int st = k % kStages;
                 const int my_row = row_of(k);
-                pf_wait(p, &v_empty[st], ((k / kStages) & 1) ^ 1, true);
+                // (the stage was found free by load_k(k), always issued first)
                 if (k < 16 && lane == 0) pf_stamp(p, 104 + k);
                 if (p.ablate & 1) {  // dev ablation: V = whatever the stage holds
                     if (lane == 0) mbar_arrive(&v_full[st]);
@@ -491,7 +491,6 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                 k_ready(k);
                 for (int i = 0; i < 2; ++i)
                     if (k < cnt[i]) issue_s(i, k);
-                tc_commit_warp(&k_empty[k % kStages]);
             }
             for (int k = 0; k < jmax; ++k) {
                 const bool ahead = k + 2 < jmax;
@@ -516,8 +515,10 @@ __global__ void __launch_bounds__(kPPThreads, 1)
                     if (k + 2 < cnt[i]) issue_s(i, k + 2);
                 }
                 if (k < 16 && lane == 0) pf_stamp(p, 8 + k);
+                // K(k) and V(k) share one stage, freed by ONE commit once PV(k) (issued after S(k))
+                // of both tiles retires: one tcgen05.commit per step fewer than separate K / V
+                // releases (the producer still runs K three steps ahead of its use)
                 tc_commit_warp(&v_empty[k % kStages]);
-                if (ahead) tc_commit_warp(&k_empty[(k + 2) % kStages]);
             }
         }
     } else {

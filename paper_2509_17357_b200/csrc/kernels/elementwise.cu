@@ -137,10 +137,12 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16*
 }
 
 // ---------------------------------------------------------------- QKV post-processing
-// grid (row, head): 64 threads per head. Rotary heads (q and k): thread i rotates the
-// pair (i, i + 64) (rotate-half RoPE); v heads: thread i moves dims (2i, 2i + 1).
-// q goes to q_out (bf16); k and v go to the row's slot of its paged KV block.
-constexpr int kQkvHeadsPerCta = 4;
+// grid (row, head group): 16 threads per head, 16 heads per CTA. Rotary heads (q and k): thread
+// j rotates the 4 pairs (4j + e, 4j + e + 64) (rotate-half RoPE) with float4 loads and 8-byte
+// stores; v heads: thread j moves dims 8j .. 8j + 7. q goes to q_out (bf16); k and v go to the
+// row's slot of its paged KV block. (Round 2 session 5: 4-wide per thread instead of one pair per
+// thread, 1.8 TB/s -> see profiles/r2_session5/rope_vec.log.)
+constexpr int kQkvHeadsPerCta = 16;
 
 __global__ void qkv_rope_append_kernel(float* __restrict__ qkv, const __nv_bfloat16* __restrict__ bias,
                                        __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ pool,
@@ -149,46 +151,70 @@ __global__ void qkv_rope_append_kernel(float* __restrict__ qkv, const __nv_bfloa
                                        const float* __restrict__ sin_tab, int nq, int nkv, int layer, int n_layers,
                                        int zero_after) {
     pdl_launch();
-    pdl_wait();
-    const int m = blockIdx.x, h = blockIdx.y * kQkvHeadsPerCta + (threadIdx.x >> 6), i = threadIdx.x & 63;
-    if (h >= nq + 2 * nkv) return;
+    // Everything but the QKV accumulator is ready before this kernel: the pass's metadata (row
+    // positions, block tables) came by a stream-ordered copy at the pass start, the bias and the
+    // rope tables are weights. Their dependent loads (position -> rope entry, block table ->
+    // pool slot) are issued before griddepcontrol.wait, leaving one L2 round trip after it.
+    const int m = blockIdx.x, h = blockIdx.y * kQkvHeadsPerCta + (threadIdx.x >> 4), j = threadIdx.x & 15;
+    const bool live = h < nq + 2 * nkv;
+    const bool rot = h < nq + nkv;
     const int pos = row_pos[m];
-    float* row = qkv + static_cast<size_t>(m) * (nq + 2 * nkv) * 128 + h * 128;
-    const __nv_bfloat16* brow = bias ? bias + h * 128 : nullptr;
+    const __nv_bfloat16* brow = bias && live ? bias + h * 128 : nullptr;
     const size_t head_stride = 16 * 128;
-    if (h < nq + nkv) {
-        float a = row[i], b = row[i + 64];
-        if (zero_after) {  // leave the red.add accumulator clean for the next layer
-            row[i] = 0.f;
-            row[i + 64] = 0.f;
+    float4 c = make_float4(0.f, 0.f, 0.f, 0.f), sn = c;
+    float bb[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    int block = 0;
+    if (live) {
+        if (rot) {
+            c = *reinterpret_cast<const float4*>(cos_tab + static_cast<size_t>(pos) * 64 + 4 * j);
+            sn = *reinterpret_cast<const float4*>(sin_tab + static_cast<size_t>(pos) * 64 + 4 * j);
         }
+        if (h >= nq) block = bt[row_bt[m] + (pos >> 4)];
         if (brow) {
-            a += bf2f(brow[i]);
-            b += bf2f(brow[i + 64]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                bb[e] = bf2f(brow[rot ? 4 * j + e : 8 * j + e]);
+                bb[4 + e] = bf2f(brow[rot ? 4 * j + e + 64 : 8 * j + 4 + e]);
+            }
         }
-        const float c = cos_tab[static_cast<size_t>(pos) * 64 + i], sn = sin_tab[static_cast<size_t>(pos) * 64 + i];
-        const float ra = a * c - b * sn, rb = b * c + a * sn;
+    }
+    pdl_wait();
+    if (!live) return;
+    float* row = qkv + static_cast<size_t>(m) * (nq + 2 * nkv) * 128 + h * 128;
+    if (rot) {
+        float4 a = *reinterpret_cast<const float4*>(row + 4 * j);
+        float4 b = *reinterpret_cast<const float4*>(row + 4 * j + 64);
+        if (zero_after) {  // leave the red.add accumulator clean for the next layer
+            *reinterpret_cast<float4*>(row + 4 * j) = make_float4(0.f, 0.f, 0.f, 0.f);
+            *reinterpret_cast<float4*>(row + 4 * j + 64) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        a.x += bb[0], a.y += bb[1], a.z += bb[2], a.w += bb[3];
+        b.x += bb[4], b.y += bb[5], b.z += bb[6], b.w += bb[7];
         __nv_bfloat16* dst;
         if (h < nq) {
             dst = q_out + static_cast<size_t>(m) * nq * 128 + h * 128;
         } else {
-            const int block = bt[row_bt[m] + (pos >> 4)];
             dst = pool + ((static_cast<size_t>(block) * n_layers + layer) * 2 * nkv + (h - nq)) * head_stride +
                   (pos & 15) * 128;
         }
-        dst[i] = f2bf(ra);
-        dst[i + 64] = f2bf(rb);
+        const uint2 lo = make_uint2(pack_bf16x2(a.x * c.x - b.x * sn.x, a.y * c.y - b.y * sn.y),
+                                    pack_bf16x2(a.z * c.z - b.z * sn.z, a.w * c.w - b.w * sn.w));
+        const uint2 hi = make_uint2(pack_bf16x2(b.x * c.x + a.x * sn.x, b.y * c.y + a.y * sn.y),
+                                    pack_bf16x2(b.z * c.z + a.z * sn.z, b.w * c.w + a.w * sn.w));
+        *reinterpret_cast<uint2*>(dst + 4 * j) = lo;
+        *reinterpret_cast<uint2*>(dst + 4 * j + 64) = hi;
     } else {
-        float2 v = *reinterpret_cast<const float2*>(row + 2 * i);
-        if (zero_after) *reinterpret_cast<float2*>(row + 2 * i) = make_float2(0.f, 0.f);
-        if (brow) {
-            v.x += bf2f(brow[2 * i]);
-            v.y += bf2f(brow[2 * i + 1]);
+        float4 v0 = *reinterpret_cast<const float4*>(row + 8 * j);
+        float4 v1 = *reinterpret_cast<const float4*>(row + 8 * j + 4);
+        if (zero_after) {
+            *reinterpret_cast<float4*>(row + 8 * j) = make_float4(0.f, 0.f, 0.f, 0.f);
+            *reinterpret_cast<float4*>(row + 8 * j + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        const int block = bt[row_bt[m] + (pos >> 4)];
         __nv_bfloat16* dst = pool + ((static_cast<size_t>(block) * n_layers + layer) * 2 * nkv + nkv +
                                      (h - nq - nkv)) * head_stride + (pos & 15) * 128;
-        *reinterpret_cast<uint32_t*>(dst + 2 * i) = pack_bf16x2(v.x, v.y);
+        *reinterpret_cast<uint4*>(dst + 8 * j) =
+            make_uint4(pack_bf16x2(v0.x + bb[0], v0.y + bb[1]), pack_bf16x2(v0.z + bb[2], v0.w + bb[3]),
+                       pack_bf16x2(v1.x + bb[4], v1.y + bb[5]), pack_bf16x2(v1.z + bb[6], v1.w + bb[7]));
     }
 }
 
@@ -401,7 +427,7 @@ int ck_qkv_rope_append(float* qkv, const void* bias, void* q_out, void* kv_pool,
     if (M <= 0) return 0;
     const int nh = nq + 2 * nkv;
     return launch_pdl(qkv_rope_append_kernel, dim3(M, (nh + kQkvHeadsPerCta - 1) / kQkvHeadsPerCta),
-                      dim3(64 * kQkvHeadsPerCta), 0, S(stream), qkv, static_cast<const __nv_bfloat16*>(bias),
+                      dim3(16 * kQkvHeadsPerCta), 0, S(stream), qkv, static_cast<const __nv_bfloat16*>(bias),
                                                      static_cast<__nv_bfloat16*>(q_out),
                                                      static_cast<__nv_bfloat16*>(kv_pool), bt, row_bt, row_pos,
                                                      cos_tab, sin_tab, nq, nkv, layer, n_layers, zero_after);
